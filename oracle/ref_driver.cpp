@@ -1,0 +1,458 @@
+// TEST INFRASTRUCTURE ONLY — never linked into or called from the product path.
+//
+// A thin extern "C" shim over the UNMODIFIED reference library (compiled from
+// /root/reference/proj/src by oracle/Makefile into oracle/_ref/libifgf_ref.so). It lets the
+// Python tests, __graft_entry__.smoke() and bench.py's CPU legs drive the reference's own
+// public API (geometry, CombinedOperator, ifgf_apply, level_d_fill, solve) and read back
+// its plan objects, so the B200 path can be checked against the real thing.
+//
+// Reference entry points wrapped here (file:line under /root/reference/proj):
+//   build_sphere / assemble_mesh          src/geometry.cpp:180-211, 121-178
+//   CombinedOperator ctor/apply/...       src/solver.cpp:43-167 (include/ifgf/solver.hpp:50-84)
+//   ifgf_apply / level_d_fill             src/ifgf.cpp:577-608, 312-391
+//   rp_singular_apply                     src/rp.cpp:421-451
+//   gmres_solve / solve                   src/solver.cpp:270-340
+//   save_beta_cache                       src/rp.cpp:515-536
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <numbers>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "ifgf/geometry.hpp"
+#include "ifgf/ifgf.hpp"
+#include "ifgf/rp.hpp"
+#include "ifgf/solver.hpp"
+
+using namespace ifgf;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct RefOp {
+    std::shared_ptr<SurfaceMesh> mesh;  // the operator borrows the mesh (solver.hpp:73)
+    std::unique_ptr<CombinedOperator> op;
+    DlStrategy strategy = DlStrategy::Hybrid;
+};
+
+int fail(const std::exception& e) {
+    g_err = e.what();
+    if (dynamic_cast<const InvalidArgument*>(&e)) return 1;
+    if (dynamic_cast<const ParseError*>(&e)) return 2;
+    if (dynamic_cast<const DegenerateGeometry*>(&e)) return 3;
+    if (dynamic_cast<const ConvergenceFailure*>(&e)) return 4;
+    if (dynamic_cast<const InternalError*>(&e)) return 5;
+    return 6;
+}
+
+std::vector<cplx> to_cplx(const double* v, std::size_t n) {
+    std::vector<cplx> out(n);
+    for (std::size_t i = 0; i < n; ++i) out[i] = cplx(v[2 * i], v[2 * i + 1]);
+    return out;
+}
+void from_cplx(const std::vector<cplx>& v, double* out) {
+    for (std::size_t i = 0; i < v.size(); ++i) {
+        out[2 * i] = v[i].real();
+        out[2 * i + 1] = v[i].imag();
+    }
+}
+
+DlStrategy strat(int s) {
+    return s == 0 ? DlStrategy::W4 : (s == 1 ? DlStrategy::W2W3 : DlStrategy::Hybrid);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// ---------------------------------------------------------------- geometry
+void* ref_mesh_sphere(double radius, int splits, int nu, int nv) {
+    try {
+        return new std::shared_ptr<SurfaceMesh>(
+            std::make_shared<SurfaceMesh>(build_sphere(radius, splits, nu, nv)));
+    } catch (const std::exception& e) {
+        fail(e);
+        return nullptr;
+    }
+}
+
+// Prolate spheroid: the cube-sphere patch series scaled per axis, derivative series
+// recomputed by assemble_mesh.
+void* ref_mesh_spheroid(int splits, int nu, int nv, double ax, double ay, double az) {
+    try {
+        SurfaceMesh s = build_sphere(1.0, splits, nu, nv);
+        std::vector<Patch> patches = s.patches;
+        const double sc[3] = {ax, ay, az};
+        for (auto& p : patches)
+            for (int c = 0; c < 3; ++c) {
+                for (auto& v : p.coeff[c]) v *= sc[c];
+                p.coeff_u[c].clear();
+                p.coeff_v[c].clear();
+            }
+        return new std::shared_ptr<SurfaceMesh>(
+            std::make_shared<SurfaceMesh>(assemble_mesh(std::move(patches), Vec3{0, 0, 0})));
+    } catch (const std::exception& e) {
+        fail(e);
+        return nullptr;
+    }
+}
+
+void ref_mesh_free(void* m) { delete static_cast<std::shared_ptr<SurfaceMesh>*>(m); }
+
+static SurfaceMesh& M(void* m) { return **static_cast<std::shared_ptr<SurfaceMesh>*>(m); }
+
+long ref_mesh_size(void* m) { return long(M(m).size()); }
+int ref_mesh_npatches(void* m) { return int(M(m).patches.size()); }
+double ref_mesh_diameter(void* m) { return M(m).diameter(); }
+
+void ref_mesh_nodes(void* m, double* pos, double* nrm, double* jac, double* w, double* pu,
+                    double* pv, int* patch_of) {
+    const SurfaceMesh& s = M(m);
+    for (std::size_t i = 0; i < s.size(); ++i) {
+        pos[3 * i] = s.pos[i].x;
+        pos[3 * i + 1] = s.pos[i].y;
+        pos[3 * i + 2] = s.pos[i].z;
+        nrm[3 * i] = s.normal[i].x;
+        nrm[3 * i + 1] = s.normal[i].y;
+        nrm[3 * i + 2] = s.normal[i].z;
+        jac[i] = s.jac[i];
+        w[i] = s.weight[i];
+        pu[i] = s.pu[i];
+        pv[i] = s.pv[i];
+        patch_of[i] = s.patch_of[i];
+    }
+}
+
+// dims = {nu, nv, du, dv}
+void ref_mesh_patch_dims(void* m, int q, int* dims, double* orient) {
+    const Patch& p = M(m).patches[q];
+    dims[0] = p.nu;
+    dims[1] = p.nv;
+    dims[2] = p.du;
+    dims[3] = p.dv;
+    *orient = p.orient;
+}
+
+// each output holds 3 * du * dv values: component-major, u index fastest
+void ref_mesh_patch_coeffs(void* m, int q, double* coeff, double* cu, double* cv) {
+    const Patch& p = M(m).patches[q];
+    const std::size_t n = std::size_t(p.du) * p.dv;
+    for (int c = 0; c < 3; ++c) {
+        std::memcpy(coeff + c * n, p.coeff[c].data(), n * sizeof(double));
+        std::memcpy(cu + c * n, p.coeff_u[c].data(), n * sizeof(double));
+        std::memcpy(cv + c * n, p.coeff_v[c].data(), n * sizeof(double));
+    }
+}
+
+// Seeded density exactly as the reference harness draws it (tools/main.cpp:252-254,
+// tests/test_solver.cpp:13-19): cplx(u(rng), u(rng)) with GCC's argument order.
+void ref_random_density(long n, unsigned long long seed, double* out) {
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> u(-1, 1);
+    std::vector<cplx> a(n);
+    for (auto& v : a) v = cplx(u(rng), u(rng));
+    from_cplx(a, out);
+}
+
+// ---------------------------------------------------------------- operator
+// strategy: 0 = W4, 1 = W2W3, 2 = Hybrid (default). gamma <= 0 selects max{3, A/lambda}.
+void* ref_op_create(void* mesh, double k, double gamma, int strategy, int workers,
+                    const char* beta_cache, int ps, int pang, int n_c0, int n_s0,
+                    double finest_box_lambda, int n_beta, int cov_d) {
+    try {
+        SolveConfig cfg;
+        cfg.k = k;
+        cfg.gamma = gamma;
+        cfg.dl_strategy = strat(strategy);
+        cfg.workers = workers;
+        if (beta_cache && *beta_cache) cfg.beta_cache_path = beta_cache;
+        if (ps > 0) cfg.cone.ps = ps;
+        if (pang > 0) cfg.cone.pang = pang;
+        if (n_c0 > 0) cfg.cone.n_c0 = n_c0;
+        if (n_s0 > 0) cfg.cone.n_s0 = n_s0;
+        if (finest_box_lambda > 0) cfg.finest_box_lambda = finest_box_lambda;
+        if (n_beta > 0) cfg.rp.n_beta = n_beta;
+        if (cov_d > 0) cfg.rp.cov_d = cov_d;
+        auto* r = new RefOp;
+        r->mesh = *static_cast<std::shared_ptr<SurfaceMesh>*>(mesh);
+        r->op = std::make_unique<CombinedOperator>(*r->mesh, cfg);
+        // resolved strategy, as the ctor does (solver.cpp:55-62)
+        r->strategy = cfg.dl_strategy;
+        if (r->strategy == DlStrategy::Hybrid) {
+            const double lambda = 2.0 * std::numbers::pi / k;
+            bool any_sub = false;
+            for (int d = 3; d <= r->op->tree().depth; ++d)
+                if (r->op->tree().side(d) / lambda < 0.5 - 1e-12) any_sub = true;
+            if (!any_sub) r->strategy = DlStrategy::W4;
+        }
+        return r;
+    } catch (const std::exception& e) {
+        fail(e);
+        return nullptr;
+    }
+}
+
+void ref_op_free(void* h) { delete static_cast<RefOp*>(h); }
+static RefOp& R(void* h) { return *static_cast<RefOp*>(h); }
+
+double ref_op_gamma(void* h) { return R(h).op->gamma(); }
+double ref_op_setup_seconds(void* h) { return R(h).op->setup_seconds(); }
+int ref_op_beta_cache_hit(void* h) { return R(h).op->beta_cache_was_reused() ? 1 : 0; }
+int ref_op_strategy(void* h) {
+    return R(h).strategy == DlStrategy::W4 ? 0 : (R(h).strategy == DlStrategy::W2W3 ? 1 : 2);
+}
+
+int ref_op_apply(void* h, const double* phi, double* out) {
+    try {
+        const auto n = R(h).mesh->size();
+        from_cplx(R(h).op->apply(to_cplx(phi, n)), out);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int ref_op_layer_potentials(void* h, const double* phi, double* S, double* D) {
+    try {
+        const auto n = R(h).mesh->size();
+        std::vector<cplx> s, d;
+        R(h).op->layer_potentials(to_cplx(phi, n), s, d);
+        from_cplx(s, S);
+        from_cplx(d, D);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int ref_op_apply_direct(void* h, const double* phi, double* out) {
+    try {
+        const auto n = R(h).mesh->size();
+        from_cplx(R(h).op->apply_direct(to_cplx(phi, n)), out);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// IFGF far part only, on quadrature-weighted sources a (original order). strategy < 0
+// uses the operator's resolved strategy.
+int ref_op_ifgf_apply(void* h, const double* a, int single, int dbl, int strategy, int workers,
+                      double* S, double* D) {
+    try {
+        const auto n = R(h).mesh->size();
+        IfgfRequest req;
+        req.single_layer = single != 0;
+        req.double_layer = dbl != 0;
+        req.strategy = strategy < 0 ? R(h).strategy : strat(strategy);
+        const auto o = ifgf_apply(R(h).op->plan(), to_cplx(a, n), req, workers);
+        from_cplx(o.single, S);
+        from_cplx(o.dbl, D);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// RP singular correction alone (accumulates into zeroed outputs), rp.cpp:421-451
+int ref_op_rp_apply(void* h, const double* phi, double* S, double* D) {
+    try {
+        const auto n = R(h).mesh->size();
+        std::vector<cplx> s(n), d(n);
+        rp_singular_apply(*R(h).mesh, R(h).op->proximity(), R(h).op->precompute(),
+                          to_cplx(phi, n), s, d, 0);
+        from_cplx(s, S);
+        from_cplx(d, D);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// level_d_fill with the given factor codes (1..4) on Morton-ordered sources; returns the
+// number of complex values written (segments * npipes * P), or -1 on error. out may be null
+// to query the size.
+long ref_op_level_d_fill(void* h, const double* a_perm, const int* pipes, int npipes,
+                         double* out) {
+    try {
+        const auto& plan = R(h).op->plan();
+        const int D = plan.tree->depth;
+        const std::size_t total = plan.level_segs[D - 1].segs.size() *
+                                  std::size_t(plan.level_cones[D - 1].points_per_seg()) *
+                                  std::size_t(npipes);
+        if (!out) return long(total);
+        std::vector<Factor> f(npipes);
+        for (int i = 0; i < npipes; ++i) f[i] = Factor(pipes[i]);
+        const auto data = level_d_fill(plan, to_cplx(a_perm, plan.pts.size()), f, 0);
+        from_cplx(data.blocks, out);
+        return long(data.blocks.size());
+    } catch (const std::exception& e) {
+        fail(e);
+        return -1;
+    }
+}
+
+// ---------------------------------------------------------------- plan export
+int ref_op_depth(void* h) { return R(h).op->tree().depth; }
+
+void ref_op_tree_geom(void* h, double* root_min3, double* root_side) {
+    const auto& t = R(h).op->tree();
+    root_min3[0] = t.root_min.x;
+    root_min3[1] = t.root_min.y;
+    root_min3[2] = t.root_min.z;
+    *root_side = t.root_side;
+}
+
+void ref_op_perm(void* h, std::uint32_t* perm) {
+    const auto& p = R(h).op->tree().perm;
+    std::memcpy(perm, p.data(), p.size() * sizeof(std::uint32_t));
+}
+
+void ref_op_leaf_of_point(void* h, std::int32_t* out) {
+    const auto& p = R(h).op->tree().leaf_of_point();
+    std::memcpy(out, p.data(), p.size() * sizeof(std::int32_t));
+}
+
+long ref_op_nboxes(void* h, int d) { return long(R(h).op->tree().levels[d - 1].size()); }
+
+void ref_op_boxes(void* h, int d, std::uint64_t* key, std::int32_t* coords3, std::uint32_t* begin,
+                  std::uint32_t* end, std::int32_t* parent, std::int32_t* children8) {
+    const auto& v = R(h).op->tree().levels[d - 1];
+    for (std::size_t b = 0; b < v.size(); ++b) {
+        key[b] = v[b].key;
+        for (int c = 0; c < 3; ++c) coords3[3 * b + c] = v[b].coords[c];
+        begin[b] = v[b].begin;
+        end[b] = v[b].end;
+        parent[b] = v[b].parent;
+        for (int c = 0; c < 8; ++c) children8[8 * b + c] = v[b].children[c];
+    }
+}
+
+// which: 0 = neighbours, 1 = cousins. ptr has nboxes+1 entries; idx may be null (size query).
+long ref_op_relation(void* h, int d, int which, std::int32_t* ptr, std::int32_t* idx) {
+    const auto& rel = R(h).op->relations();
+    const auto& lists = which == 0 ? rel.neighbors[d - 1] : rel.cousins[d - 1];
+    long total = 0;
+    for (std::size_t b = 0; b < lists.size(); ++b) {
+        if (ptr) ptr[b] = std::int32_t(total);
+        if (idx) std::memcpy(idx + total, lists[b].data(), lists[b].size() * sizeof(std::int32_t));
+        total += long(lists[b].size());
+    }
+    if (ptr) ptr[lists.size()] = std::int32_t(total);
+    return total;
+}
+
+// level cone parameters: {ns, nc, ps, pang}; returns relevant segment count
+long ref_op_level_cones(void* h, int d, int* params, double* deltas3) {
+    const auto& plan = R(h).op->plan();
+    const auto& lc = plan.level_cones[d - 1];
+    params[0] = lc.ns;
+    params[1] = lc.nc;
+    params[2] = lc.ps;
+    params[3] = lc.pang;
+    deltas3[0] = lc.ds;
+    deltas3[1] = lc.dth;
+    deltas3[2] = lc.dph;
+    return long(plan.level_segs[d - 1].segs.size());
+}
+
+void ref_op_level_segs(void* h, int d, std::int32_t* box, std::int32_t* gamma) {
+    const auto& s = R(h).op->plan().level_segs[d - 1].segs;
+    for (std::size_t i = 0; i < s.size(); ++i) {
+        box[i] = s[i].box;
+        gamma[i] = s[i].gamma;
+    }
+}
+
+long ref_op_npairs(void* h) { return long(R(h).op->proximity().pairs.size()); }
+long ref_op_nfar(void* h) { return long(R(h).op->proximity().far_nodes.size()); }
+
+void ref_op_pairs(void* h, std::uint32_t* target, std::int32_t* patch, double* ubar, double* vbar,
+                  std::uint32_t* far_begin, std::uint32_t* far_end, std::uint32_t* target_pair_begin,
+                  std::uint32_t* far_nodes) {
+    const auto& p = R(h).op->proximity();
+    for (std::size_t i = 0; i < p.pairs.size(); ++i) {
+        target[i] = p.pairs[i].target;
+        patch[i] = p.pairs[i].patch;
+        ubar[i] = p.pairs[i].ubar;
+        vbar[i] = p.pairs[i].vbar;
+        far_begin[i] = p.pairs[i].far_begin;
+        far_end[i] = p.pairs[i].far_end;
+    }
+    std::memcpy(target_pair_begin, p.target_pair_begin.data(),
+                p.target_pair_begin.size() * sizeof(std::uint32_t));
+    std::memcpy(far_nodes, p.far_nodes.data(), p.far_nodes.size() * sizeof(std::uint32_t));
+}
+
+void ref_op_delta(void* h, double* delta) {
+    const auto& p = R(h).op->proximity();
+    std::memcpy(delta, p.delta.data(), p.delta.size() * sizeof(double));
+}
+
+long ref_op_beta_size(void* h) { return long(R(h).op->precompute().beta_single.size()); }
+
+void ref_op_beta(void* h, std::uint64_t* offset, double* bs, double* bd) {
+    const auto& pc = R(h).op->precompute();
+    for (std::size_t i = 0; i < pc.offset.size(); ++i) offset[i] = pc.offset[i];
+    from_cplx(pc.beta_single, bs);
+    from_cplx(pc.beta_dbl, bd);
+}
+
+unsigned long long ref_op_beta_fingerprint(void* h) { return R(h).op->precompute().fingerprint; }
+
+int ref_op_save_beta_cache(void* h, const char* path) {
+    try {
+        save_beta_cache(path, R(h).op->precompute());
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// ---------------------------------------------------------------- timing helpers
+// Wall time of one CombinedOperator::apply (the reference's cmd_benchmark unit,
+// tools/main.cpp:256-264).
+double ref_op_time_apply(void* h, const double* phi, double* out) {
+    const auto n = R(h).mesh->size();
+    const auto in = to_cplx(phi, n);
+    const auto t0 = std::chrono::steady_clock::now();
+    auto o = R(h).op->apply(in);
+    const double dt =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (out) from_cplx(o, out);
+    return dt;
+}
+
+// ---------------------------------------------------------------- GMRES solve
+// Plane-wave solve (solver.cpp:302-340). Returns iterations, or -rc on error.
+int ref_solve(void* mesh, double k, double gamma, double theta, double phi, double tol,
+              int max_iter, int restart, int workers, double* density_out, double* hist_out,
+              int hist_cap) {
+    try {
+        SolveConfig cfg;
+        cfg.k = k;
+        cfg.gamma = gamma;
+        cfg.tol = tol;
+        cfg.max_iter = max_iter;
+        cfg.restart = restart;
+        cfg.workers = workers;
+        IncidentField inc;
+        inc.theta = theta;
+        inc.phi = phi;
+        const auto res = solve(M(mesh), inc, cfg);
+        from_cplx(res.density, density_out);
+        for (int i = 0; i < int(res.residual_history.size()) && i < hist_cap; ++i)
+            hist_out[i] = res.residual_history[i];
+        return res.iterations;
+    } catch (const std::exception& e) {
+        return -fail(e);
+    }
+}
+
+}  // extern "C"

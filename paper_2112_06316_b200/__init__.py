@@ -1,0 +1,16 @@
+"""B200-native combined-field operator apply of the IFGF/RP-accelerated CFIE solver
+(arXiv 2112.06316): host setup in C++, hot path in hand-written sm_100a CUDA, behind the
+C-ABI of include/ifgf_b200.h. This package is the Python mirror of the reference's C++
+operator API (solver.hpp / geometry.hpp / ifgf.hpp / rp.hpp)."""
+from ._lib import (ConvergenceFailure, DegenerateGeometry, DeviceError, IfgfError, InternalError,
+                   InvalidArgument, ParseError, lib)
+from .operator import (CombinedOperator, ConeConfig, DlStrategy, Factor, GmresResult, HostPlan,
+                       IncidentField, RpConfig, SolveConfig, SurfaceMesh, gmres_solve, random_density,
+                       solve)
+
+__all__ = [
+    "CombinedOperator", "ConeConfig", "DlStrategy", "Factor", "GmresResult", "HostPlan", "IncidentField",
+    "RpConfig", "SolveConfig", "SurfaceMesh", "gmres_solve", "random_density", "solve", "lib",
+    "IfgfError", "InvalidArgument", "ParseError", "DegenerateGeometry", "ConvergenceFailure",
+    "InternalError", "DeviceError",
+]

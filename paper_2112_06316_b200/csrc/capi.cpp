@@ -1,0 +1,762 @@
+// extern "C" boundary of the B200 CF-operator engine (declared in include/ifgf_b200.h).
+// Every entry point catches C++ exceptions and converts them to the status codes of the
+// reference's error taxonomy; messages are kept thread-local for ifgf_last_error().
+#include <chrono>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <random>
+#include <string>
+
+#include "../../include/ifgf_b200.h"
+#include "engine.hpp"
+#include "host/chebyshev.hpp"
+#include "host/gmres.hpp"
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+using namespace ifgfb200;
+
+namespace ifgfb200 {
+int worker_count(int requested) {
+#ifdef _OPENMP
+    if (requested > 0) return requested;
+    return std::max(1, omp_get_max_threads());
+#else
+    (void)requested;
+    return 1;
+#endif
+}
+}  // namespace ifgfb200
+
+struct ifgf_surface {
+    std::shared_ptr<Surface> s;
+};
+
+struct ifgf_plan {
+    std::shared_ptr<const Surface> surf;
+    ifgf_config cfg{};
+    double k = 0, gamma = 0;
+    DlStrategy strategy = DlStrategy::Hybrid;
+    BoxTree tree;
+    BoxRelations rel;
+    ConePlanHost cones;
+    PairList pairs;
+    double setup_seconds = 0;
+};
+
+struct ifgf_operator {
+    std::shared_ptr<ifgf_plan> plan;
+    std::unique_ptr<Engine> eng;
+};
+
+namespace {
+
+thread_local std::string g_error;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const EngineError& e) {
+        g_error = e.what();
+        return e.status;
+    } catch (const std::bad_alloc& e) {
+        g_error = std::string("out of memory: ") + e.what();
+        return kInternalError;
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return kInternalError;
+    }
+}
+
+std::vector<cplx> as_cplx(const double* v, std::size_t n) {
+    std::vector<cplx> out(n);
+    std::memcpy(static_cast<void*>(out.data()), v, n * sizeof(cplx));
+    return out;
+}
+
+void need(const void* p, const char* what) {
+    if (!p) throw InvalidArgument(std::string(what) + ": null pointer");
+}
+
+std::shared_ptr<ifgf_plan> make_plan(std::shared_ptr<const Surface> s, const ifgf_config& c) {
+    if (c.k <= 0) throw InvalidArgument("CombinedOperator: wavenumber must be positive");
+    auto p = std::make_shared<ifgf_plan>();
+    p->surf = s;
+    p->cfg = c;
+    p->k = c.k;
+    const double lambda = 2.0 * kPi / c.k;
+    if (c.gamma > 0) {
+        p->gamma = c.gamma;
+    } else {
+        const double diam = s->extent();
+        if (diam <= 0 || lambda <= 0) throw InvalidArgument("coupling_gamma: diameter and lambda must be positive");
+        p->gamma = std::max(3.0, diam / lambda);
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    p->tree = build_boxtree(s->pos, c.k, c.finest_box_lambda);
+    p->rel = build_relations(p->tree);
+    std::vector<Vec3> pts(s->size());
+    for (std::size_t t = 0; t < pts.size(); ++t) pts[t] = s->pos[p->tree.perm[t]];
+    ConeParams cp;
+    cp.n_c0 = c.n_c0;
+    cp.n_s0 = c.n_s0;
+    cp.ps = c.ps;
+    cp.pang = c.pang;
+    p->cones = build_cone_plan(p->tree, p->rel, pts, cp, c.workers);
+    RpParams rp;
+    rp.delta_rel = c.delta_rel;
+    rp.delta_abs = c.delta_abs;
+    rp.n_beta = c.n_beta;
+    rp.cov_d = c.cov_d;
+    p->pairs = classify_pairs(*s, p->tree, p->rel, rp, c.workers);
+    p->strategy = c.strategy == 0 ? DlStrategy::W4 : (c.strategy == 1 ? DlStrategy::W2W3 : DlStrategy::Hybrid);
+    if (p->strategy == DlStrategy::Hybrid) {  // solver.cpp:55-62
+        bool any_sub = false;
+        for (int d = 3; d <= p->tree.depth; ++d)
+            if (p->tree.side(d) / lambda < 0.5 - 1e-12) any_sub = true;
+        if (!any_sub) p->strategy = DlStrategy::W4;
+    }
+    p->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return p;
+}
+
+std::unique_ptr<Engine> make_engine(const ifgf_plan& p, int device) {
+    OperatorSetup s;
+    s.k = p.k;
+    s.gamma = p.gamma;
+    s.strategy = p.strategy;
+    s.surf = p.surf.get();
+    s.tree = &p.tree;
+    s.rel = &p.rel;
+    s.plan = &p.cones;
+    s.pairs = &p.pairs;
+    return std::make_unique<Engine>(s, device);
+}
+
+std::uint64_t fnv_bytes(const void* d, std::size_t n, std::uint64_t h) {
+    const auto* b = static_cast<const unsigned char*>(d);
+    for (std::size_t i = 0; i < n; ++i) {
+        h ^= b[i];
+        h *= 1099511628211ULL;
+    }
+    return h;
+}
+
+DlStrategy strategy_of(int s, DlStrategy dflt) {
+    if (s < 0) return dflt;
+    return s == 0 ? DlStrategy::W4 : (s == 1 ? DlStrategy::W2W3 : DlStrategy::Hybrid);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ifgf_last_error(void) { return g_error.c_str(); }
+int ifgf_version(void) { return 1; }
+
+void ifgf_config_default(ifgf_config* c) {
+    if (!c) return;
+    c->k = 0;
+    c->gamma = -1.0;
+    c->strategy = 2;
+    c->finest_box_lambda = 0.5;
+    c->n_c0 = 2;
+    c->n_s0 = 1;
+    c->ps = 3;
+    c->pang = 5;
+    c->delta_rel = 1.0;
+    c->delta_abs = -1.0;
+    c->n_beta = 96;
+    c->cov_d = 6;
+    c->workers = 0;
+    c->device = 0;
+}
+
+// ------------------------------------------------------------------ surfaces
+int ifgf_surface_sphere(double radius, int splits, int nu, int nv, ifgf_surface** out) {
+    return guarded([&] {
+        need(out, "ifgf_surface_sphere");
+        *out = new ifgf_surface{std::make_shared<Surface>(make_sphere(radius, splits, nu, nv))};
+    });
+}
+
+int ifgf_surface_spheroid(int splits, int nu, int nv, double ax, double ay, double az, ifgf_surface** out) {
+    return guarded([&] {
+        need(out, "ifgf_surface_spheroid");
+        *out = new ifgf_surface{std::make_shared<Surface>(make_spheroid(splits, nu, nv, ax, ay, az))};
+    });
+}
+
+int ifgf_surface_from_series(int npatch, const int32_t* dims, const double* coeff, const double interior[3],
+                             ifgf_surface** out) {
+    return guarded([&] {
+        need(out, "ifgf_surface_from_series");
+        need(dims, "dims");
+        need(coeff, "coeff");
+        if (npatch < 1) throw InvalidArgument("surface: patch count must be positive");
+        std::vector<Patch> ps(npatch);
+        std::size_t off = 0;
+        for (int q = 0; q < npatch; ++q) {
+            Patch& p = ps[q];
+            p.nu = dims[4 * q];
+            p.nv = dims[4 * q + 1];
+            p.du = dims[4 * q + 2];
+            p.dv = dims[4 * q + 3];
+            if (p.nu < 1 || p.nv < 1 || p.du < 1 || p.dv < 1) throw InvalidArgument("surface: nonpositive patch dimensions");
+            const std::size_t m = std::size_t(p.du) * p.dv;
+            for (int c = 0; c < 3; ++c) p.pos_c[c].assign(coeff + off + c * m, coeff + off + (c + 1) * m);
+            off += 3 * m;
+        }
+        const Vec3 in = interior ? Vec3{interior[0], interior[1], interior[2]} : Vec3{0, 0, 0};
+        *out = new ifgf_surface{std::make_shared<Surface>(assemble_surface(std::move(ps), in))};
+    });
+}
+
+int ifgf_surface_import(int npatch, const int32_t* dims, const double* orient, const double* coeff,
+                        const double* coeff_u, const double* coeff_v, const double interior[3], int64_t n,
+                        const double* pos, const double* normal, const double* jac, const double* weight,
+                        const double* pu, const double* pv, ifgf_surface** out) {
+    return guarded([&] {
+        need(out, "ifgf_surface_import");
+        for (const void* p : {(const void*)dims, (const void*)orient, (const void*)coeff, (const void*)coeff_u,
+                              (const void*)coeff_v, (const void*)pos, (const void*)normal, (const void*)jac,
+                              (const void*)weight, (const void*)pu, (const void*)pv})
+            need(p, "ifgf_surface_import");
+        auto s = std::make_shared<Surface>();
+        s->patches.resize(npatch);
+        s->interior = interior ? Vec3{interior[0], interior[1], interior[2]} : Vec3{0, 0, 0};
+        s->patch_start.assign(npatch + 1, 0);
+        std::size_t off = 0;
+        for (int q = 0; q < npatch; ++q) {
+            Patch& p = s->patches[q];
+            p.nu = dims[4 * q];
+            p.nv = dims[4 * q + 1];
+            p.du = dims[4 * q + 2];
+            p.dv = dims[4 * q + 3];
+            p.orient = orient[q];
+            const std::size_t m = std::size_t(p.du) * p.dv;
+            for (int c = 0; c < 3; ++c) {
+                p.pos_c[c].assign(coeff + off + c * m, coeff + off + (c + 1) * m);
+                p.du_c[c].assign(coeff_u + off + c * m, coeff_u + off + (c + 1) * m);
+                p.dv_c[c].assign(coeff_v + off + c * m, coeff_v + off + (c + 1) * m);
+            }
+            off += 3 * m;
+            s->patch_start[q + 1] = s->patch_start[q] + std::size_t(p.nu) * p.nv;
+        }
+        if (std::int64_t(s->patch_start.back()) != n) throw InvalidArgument("surface import: node count mismatch");
+        s->pos.resize(n);
+        s->nrm.resize(n);
+        s->jac.assign(jac, jac + n);
+        s->wt.assign(weight, weight + n);
+        s->pu.assign(pu, pu + n);
+        s->pv.assign(pv, pv + n);
+        s->patch_of.resize(n);
+        for (std::int64_t i = 0; i < n; ++i) {
+            s->pos[i] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+            s->nrm[i] = {normal[3 * i], normal[3 * i + 1], normal[3 * i + 2]};
+        }
+        for (int q = 0; q < npatch; ++q)
+            for (std::size_t l = s->patch_start[q]; l < s->patch_start[q + 1]; ++l) s->patch_of[l] = q;
+        *out = new ifgf_surface{s};
+    });
+}
+
+int64_t ifgf_surface_size(const ifgf_surface* s) { return s ? int64_t(s->s->size()) : -1; }
+int ifgf_surface_npatches(const ifgf_surface* s) { return s ? int(s->s->patches.size()) : -1; }
+double ifgf_surface_diameter(const ifgf_surface* s) { return s ? s->s->extent() : -1.0; }
+
+int ifgf_surface_nodes(const ifgf_surface* sf, double* pos, double* normal, double* jac, double* weight,
+                       double* pu, double* pv, int32_t* patch_of) {
+    return guarded([&] {
+        need(sf, "ifgf_surface_nodes");
+        const Surface& s = *sf->s;
+        for (std::size_t i = 0; i < s.size(); ++i) {
+            if (pos) {
+                pos[3 * i] = s.pos[i].x;
+                pos[3 * i + 1] = s.pos[i].y;
+                pos[3 * i + 2] = s.pos[i].z;
+            }
+            if (normal) {
+                normal[3 * i] = s.nrm[i].x;
+                normal[3 * i + 1] = s.nrm[i].y;
+                normal[3 * i + 2] = s.nrm[i].z;
+            }
+            if (jac) jac[i] = s.jac[i];
+            if (weight) weight[i] = s.wt[i];
+            if (pu) pu[i] = s.pu[i];
+            if (pv) pv[i] = s.pv[i];
+            if (patch_of) patch_of[i] = s.patch_of[i];
+        }
+    });
+}
+
+int ifgf_surface_patch(const ifgf_surface* sf, int q, int32_t* dims4, double* orient, double* coeff,
+                       double* coeff_u, double* coeff_v) {
+    return guarded([&] {
+        need(sf, "ifgf_surface_patch");
+        if (q < 0 || q >= int(sf->s->patches.size())) throw InvalidArgument("surface: patch index out of range");
+        const Patch& p = sf->s->patches[q];
+        if (dims4) {
+            dims4[0] = p.nu;
+            dims4[1] = p.nv;
+            dims4[2] = p.du;
+            dims4[3] = p.dv;
+        }
+        if (orient) *orient = p.orient;
+        const std::size_t m = std::size_t(p.du) * p.dv;
+        for (int c = 0; c < 3; ++c) {
+            if (coeff) std::memcpy(coeff + c * m, p.pos_c[c].data(), m * sizeof(double));
+            if (coeff_u) std::memcpy(coeff_u + c * m, p.du_c[c].data(), m * sizeof(double));
+            if (coeff_v) std::memcpy(coeff_v + c * m, p.dv_c[c].data(), m * sizeof(double));
+        }
+    });
+}
+
+void ifgf_surface_free(ifgf_surface* s) { delete s; }
+
+int ifgf_random_density(int64_t n, uint64_t seed, double* out) {
+    return guarded([&] {
+        need(out, "ifgf_random_density");
+        std::mt19937_64 rng(seed);
+        std::uniform_real_distribution<double> u(-1, 1);
+        for (int64_t i = 0; i < n; ++i) {
+            // GCC evaluates cplx(u(rng), u(rng)) right to left: the first draw is the
+            // imaginary part (SURVEY.md §0 finding 7); state it explicitly here
+            const double im = u(rng);
+            const double re = u(rng);
+            out[2 * i] = re;
+            out[2 * i + 1] = im;
+        }
+    });
+}
+
+// ------------------------------------------------------------------ plan
+int ifgf_plan_create(const ifgf_surface* s, const ifgf_config* cfg, ifgf_plan** out) {
+    return guarded([&] {
+        need(s, "surface");
+        need(cfg, "config");
+        need(out, "out");
+        auto p = make_plan(s->s, *cfg);
+        *out = new ifgf_plan(std::move(*p));
+    });
+}
+
+void ifgf_plan_free(ifgf_plan* p) { delete p; }
+int ifgf_plan_depth(const ifgf_plan* p) { return p ? p->tree.depth : -1; }
+double ifgf_plan_gamma(const ifgf_plan* p) { return p ? p->gamma : 0.0; }
+int ifgf_plan_strategy(const ifgf_plan* p) { return p ? int(p->strategy) : -1; }
+double ifgf_plan_setup_seconds(const ifgf_plan* p) { return p ? p->setup_seconds : 0.0; }
+
+int ifgf_plan_perm(const ifgf_plan* p, uint32_t* perm) {
+    return guarded([&] {
+        need(p, "plan");
+        std::memcpy(perm, p->tree.perm.data(), p->tree.perm.size() * sizeof(uint32_t));
+    });
+}
+
+int ifgf_plan_tree_geom(const ifgf_plan* p, double root_min[3], double* root_side) {
+    return guarded([&] {
+        need(p, "plan");
+        root_min[0] = p->tree.root_min.x;
+        root_min[1] = p->tree.root_min.y;
+        root_min[2] = p->tree.root_min.z;
+        *root_side = p->tree.root_side;
+    });
+}
+
+int64_t ifgf_plan_nboxes(const ifgf_plan* p, int level) {
+    if (!p || level < 1 || level > p->tree.depth) return -1;
+    return int64_t(p->tree.level[level - 1].size());
+}
+
+int ifgf_plan_boxes(const ifgf_plan* p, int level, uint64_t* key, int32_t* cell3, uint32_t* begin, uint32_t* end,
+                    int32_t* parent, int32_t* child8) {
+    return guarded([&] {
+        need(p, "plan");
+        if (level < 1 || level > p->tree.depth) throw InvalidArgument("plan: level out of range");
+        const BoxLevel& B = p->tree.level[level - 1];
+        for (std::size_t b = 0; b < B.size(); ++b) {
+            if (key) key[b] = B.key[b];
+            for (int c = 0; c < 3; ++c)
+                if (cell3) cell3[3 * b + c] = B.cell[b][c];
+            if (begin) begin[b] = B.begin[b];
+            if (end) end[b] = B.end[b];
+            if (parent) parent[b] = B.parent[b];
+            for (int c = 0; c < 8; ++c)
+                if (child8) child8[8 * b + c] = B.child[b][c];
+        }
+    });
+}
+
+int64_t ifgf_plan_relation(const ifgf_plan* p, int level, int which, int32_t* ptr, int32_t* idx) {
+    if (!p || level < 1 || level > p->tree.depth) return -1;
+    const Adjacency& a = which == 0 ? p->rel.nbr[level - 1] : p->rel.cousin[level - 1];
+    if (ptr) std::memcpy(ptr, a.ptr.data(), a.ptr.size() * sizeof(int32_t));
+    if (idx) std::memcpy(idx, a.idx.data(), a.idx.size() * sizeof(int32_t));
+    return int64_t(a.idx.size());
+}
+
+int64_t ifgf_plan_level(const ifgf_plan* p, int level, int32_t* params4, double* deltas3, int32_t* seg_box,
+                        int32_t* seg_gamma) {
+    if (!p || level < 3 || level > p->tree.depth) return -1;
+    const ConeLevel& L = p->cones.level[level - 1];
+    if (params4) {
+        params4[0] = L.ns;
+        params4[1] = L.nc;
+        params4[2] = L.ps;
+        params4[3] = L.pang;
+    }
+    if (deltas3) {
+        deltas3[0] = L.ds;
+        deltas3[1] = L.dth;
+        deltas3[2] = L.dph;
+    }
+    if (seg_box) std::memcpy(seg_box, L.seg_box.data(), L.seg_box.size() * sizeof(int32_t));
+    if (seg_gamma) std::memcpy(seg_gamma, L.seg_gamma.data(), L.seg_gamma.size() * sizeof(int32_t));
+    return int64_t(L.nseg());
+}
+
+int64_t ifgf_plan_evaluations(const ifgf_plan* p, int level, int which) {
+    if (!p || level < 3 || level > p->tree.depth) return -1;
+    const ConeLevel& L = p->cones.level[level - 1];
+    return int64_t(which == 0 ? L.cev_seg.size() : L.pev_seg.size());
+}
+
+int64_t ifgf_plan_npairs(const ifgf_plan* p) { return p ? int64_t(p->pairs.size()) : -1; }
+int64_t ifgf_plan_nfar(const ifgf_plan* p) { return p ? int64_t(p->pairs.far_nodes.size()) : -1; }
+
+int ifgf_plan_pairs(const ifgf_plan* p, uint32_t* target, int32_t* patch, double* ubar, double* vbar,
+                    uint32_t* far_begin, uint32_t* far_end, uint32_t* tpb, uint32_t* far_nodes) {
+    return guarded([&] {
+        need(p, "plan");
+        const PairList& L = p->pairs;
+        const std::size_t np = L.size();
+        if (target) std::memcpy(target, L.target.data(), np * sizeof(uint32_t));
+        if (patch) std::memcpy(patch, L.patch.data(), np * sizeof(int32_t));
+        if (ubar) std::memcpy(ubar, L.ubar.data(), np * sizeof(double));
+        if (vbar) std::memcpy(vbar, L.vbar.data(), np * sizeof(double));
+        if (far_begin) std::memcpy(far_begin, L.far_begin.data(), np * sizeof(uint32_t));
+        if (far_end) std::memcpy(far_end, L.far_end.data(), np * sizeof(uint32_t));
+        if (tpb) std::memcpy(tpb, L.target_pair_begin.data(), L.target_pair_begin.size() * sizeof(uint32_t));
+        if (far_nodes) std::memcpy(far_nodes, L.far_nodes.data(), L.far_nodes.size() * sizeof(uint32_t));
+    });
+}
+
+uint64_t ifgf_plan_beta_fingerprint(const ifgf_plan* p) { return p ? beta_key(*p->surf, p->pairs, p->k) : 0; }
+
+int ifgf_plan_diagnostics(const ifgf_plan* p, char* buf, size_t cap) {
+    return guarded([&] {
+        need(p, "plan");
+        const std::string s = plan_diagnostics(p->tree, p->cones);
+        if (buf && cap) {
+            const std::size_t n = std::min(cap - 1, s.size());
+            std::memcpy(buf, s.data(), n);
+            buf[n] = 0;
+        }
+    });
+}
+
+// ------------------------------------------------------------------ operator
+int ifgf_operator_create(const ifgf_surface* s, const ifgf_config* cfg, ifgf_operator** out) {
+    return guarded([&] {
+        need(s, "surface");
+        need(cfg, "config");
+        need(out, "out");
+        auto op = std::make_unique<ifgf_operator>();
+        op->plan = make_plan(s->s, *cfg);
+        op->eng = make_engine(*op->plan, cfg->device);
+        op->eng->compute_beta();
+        *out = op.release();
+    });
+}
+
+int ifgf_operator_from_plan(ifgf_plan* p, int device, int compute_beta, ifgf_operator** out) {
+    return guarded([&] {
+        need(p, "plan");
+        need(out, "out");
+        auto op = std::make_unique<ifgf_operator>();
+        // the operator shares the plan; the caller's handle stays valid and owns its copy
+        op->plan = std::make_shared<ifgf_plan>(*p);
+        op->eng = make_engine(*op->plan, device);
+        if (compute_beta) op->eng->compute_beta();
+        *out = op.release();
+    });
+}
+
+void ifgf_operator_free(ifgf_operator* op) { delete op; }
+int64_t ifgf_operator_size(const ifgf_operator* op) { return op ? int64_t(op->eng->size()) : -1; }
+double ifgf_operator_gamma(const ifgf_operator* op) { return op ? op->plan->gamma : 0.0; }
+
+int ifgf_operator_apply(ifgf_operator* op, const double* phi, double* out) {
+    return guarded([&] {
+        need(op, "operator");
+        need(phi, "phi");
+        need(out, "out");
+        op->eng->apply(reinterpret_cast<const cplx*>(phi), reinterpret_cast<cplx*>(out));
+    });
+}
+
+int ifgf_operator_layer_potentials(ifgf_operator* op, const double* phi, double* S, double* D) {
+    return guarded([&] {
+        need(op, "operator");
+        need(phi, "phi");
+        need(S, "S");
+        need(D, "D");
+        std::vector<cplx> tmp(op->eng->size());
+        op->eng->apply(reinterpret_cast<const cplx*>(phi), tmp.data(), reinterpret_cast<cplx*>(S),
+                       reinterpret_cast<cplx*>(D));
+    });
+}
+
+int ifgf_operator_apply_device(ifgf_operator* op, const void* phi_dev, void* out_dev) {
+    return guarded([&] {
+        need(op, "operator");
+        need(phi_dev, "phi");
+        need(out_dev, "out");
+        op->eng->apply_device(phi_dev, out_dev);
+    });
+}
+
+int ifgf_operator_apply_direct(ifgf_operator* op, const double* phi, double* out) {
+    return guarded([&] {
+        need(op, "operator");
+        op->eng->apply_direct(reinterpret_cast<const cplx*>(phi), reinterpret_cast<cplx*>(out));
+    });
+}
+
+int ifgf_operator_ifgf_apply(ifgf_operator* op, const double* a, int single, int dbl, int strategy, double* S,
+                             double* D) {
+    return guarded([&] {
+        need(op, "operator");
+        need(a, "a");
+        op->eng->ifgf_apply(reinterpret_cast<const cplx*>(a), single != 0, dbl != 0,
+                            strategy_of(strategy, op->plan->strategy), reinterpret_cast<cplx*>(S),
+                            reinterpret_cast<cplx*>(D));
+    });
+}
+
+int64_t ifgf_operator_level_d_fill(ifgf_operator* op, const double* a_perm, const int32_t* pipes, int npipes,
+                                   double* out, int64_t capacity) {
+    int64_t written = 0;
+    const int rc = guarded([&] {
+        need(op, "operator");
+        need(pipes, "pipes");
+        const ifgf_plan& p = *op->plan;
+        const int D = p.tree.depth;
+        if (D < 3) return;
+        const ConeLevel& L = p.cones.level[D - 1];
+        const int64_t total = int64_t(L.nseg()) * L.nodes_per_seg() * npipes;
+        if (!out) {
+            written = total;
+            return;
+        }
+        if (capacity < total) throw InvalidArgument("level_d_fill: output too small");
+        std::vector<int> pv(pipes, pipes + npipes);
+        for (int f : pv)
+            if (f < 1 || f > 4) throw InvalidArgument("level_d_fill: factor codes are 1..4");
+        std::vector<cplx> blocks;
+        op->eng->level_d_fill(reinterpret_cast<const cplx*>(a_perm), pv, blocks);
+        std::memcpy(out, blocks.data(), blocks.size() * sizeof(cplx));
+        written = int64_t(blocks.size());
+    });
+    return rc ? -rc : written;
+}
+
+int ifgf_operator_rp_apply(ifgf_operator* op, const double* phi, double* S, double* D) {
+    return guarded([&] {
+        need(op, "operator");
+        op->eng->rp_apply(reinterpret_cast<const cplx*>(phi), reinterpret_cast<cplx*>(S),
+                          reinterpret_cast<cplx*>(D));
+    });
+}
+
+int64_t ifgf_operator_beta_entries(const ifgf_operator* op) {
+    if (!op) return -1;
+    int64_t total = 0;
+    const ifgf_plan& p = *op->plan;
+    for (std::size_t i = 0; i < p.pairs.size(); ++i) {
+        const Patch& q = p.surf->patches[p.pairs.patch[i]];
+        total += int64_t(q.nu) * q.nv;
+    }
+    return total;
+}
+
+int64_t ifgf_operator_npairs(const ifgf_operator* op) { return op ? int64_t(op->plan->pairs.size()) : -1; }
+
+int ifgf_operator_set_beta(ifgf_operator* op, const uint64_t* offset, const double* bs, const double* bd) {
+    return guarded([&] {
+        need(op, "operator");
+        std::vector<std::uint64_t> off(offset, offset + op->plan->pairs.size() + 1);
+        op->eng->upload_beta(off, reinterpret_cast<const cplx*>(bs), reinterpret_cast<const cplx*>(bd));
+    });
+}
+
+int ifgf_operator_get_beta(ifgf_operator* op, uint64_t* offset, double* bs, double* bd) {
+    return guarded([&] {
+        need(op, "operator");
+        std::vector<std::uint64_t> off;
+        std::vector<cplx> s, d;
+        op->eng->download_beta(off, s, d);
+        if (offset) std::memcpy(offset, off.data(), off.size() * sizeof(uint64_t));
+        if (bs) std::memcpy(bs, s.data(), s.size() * sizeof(cplx));
+        if (bd) std::memcpy(bd, d.data(), d.size() * sizeof(cplx));
+    });
+}
+
+// "rpbeta v1" layout of rp.cpp:515-536
+int ifgf_operator_save_beta_cache(ifgf_operator* op, const char* path) {
+    return guarded([&] {
+        need(op, "operator");
+        need(path, "path");
+        std::vector<std::uint64_t> off;
+        std::vector<cplx> s, d;
+        op->eng->download_beta(off, s, d);
+        std::ofstream f(path, std::ios::binary);
+        if (!f) throw InvalidArgument(std::string("save_beta_cache: cannot open ") + path);
+        f << "rpbeta v1\n";
+        auto put = [&](const void* p, std::size_t n) { f.write(static_cast<const char*>(p), std::streamsize(n)); };
+        const ifgf_plan& p = *op->plan;
+        const std::uint64_t fp = beta_key(*p.surf, p.pairs, p.k);
+        const double k = p.k;
+        const std::int32_t nb = p.pairs.cfg.n_beta, cd = p.pairs.cfg.cov_d;
+        const std::uint64_t npairs = off.size() - 1, ntab = s.size();
+        put(&fp, 8);
+        put(&k, 8);
+        put(&nb, 4);
+        put(&cd, 4);
+        put(&npairs, 8);
+        put(&ntab, 8);
+        put(off.data(), off.size() * 8);
+        put(s.data(), ntab * sizeof(cplx));
+        put(d.data(), ntab * sizeof(cplx));
+        std::uint64_t chk = 14695981039346656037ULL;
+        chk = fnv_bytes(off.data(), off.size() * 8, chk);
+        chk = fnv_bytes(s.data(), ntab * sizeof(cplx), chk);
+        chk = fnv_bytes(d.data(), ntab * sizeof(cplx), chk);
+        put(&chk, 8);
+    });
+}
+
+int ifgf_operator_load_beta_cache(ifgf_operator* op, const char* path) {
+    int used = 0;
+    const int rc = guarded([&] {
+        need(op, "operator");
+        need(path, "path");
+        std::ifstream f(path, std::ios::binary);
+        if (!f) return;
+        std::string header;
+        if (!std::getline(f, header) || header != "rpbeta v1") return;
+        auto get = [&](void* p, std::size_t n) {
+            f.read(static_cast<char*>(p), std::streamsize(n));
+            return bool(f);
+        };
+        std::uint64_t fp = 0, npairs = 0, ntab = 0;
+        double k = 0;
+        std::int32_t nb = 0, cd = 0;
+        if (!get(&fp, 8) || !get(&k, 8) || !get(&nb, 4) || !get(&cd, 4) || !get(&npairs, 8) || !get(&ntab, 8)) return;
+        const ifgf_plan& p = *op->plan;
+        if (fp != beta_key(*p.surf, p.pairs, p.k)) return;
+        if (npairs != p.pairs.size() || ntab > (1ULL << 40)) return;
+        std::vector<std::uint64_t> off(npairs + 1);
+        std::vector<cplx> s(ntab), d(ntab);
+        if (!get(off.data(), off.size() * 8) || !get(s.data(), ntab * sizeof(cplx)) || !get(d.data(), ntab * sizeof(cplx)))
+            return;
+        std::uint64_t want = 0;
+        if (!get(&want, 8)) return;
+        std::uint64_t chk = 14695981039346656037ULL;
+        chk = fnv_bytes(off.data(), off.size() * 8, chk);
+        chk = fnv_bytes(s.data(), ntab * sizeof(cplx), chk);
+        chk = fnv_bytes(d.data(), ntab * sizeof(cplx), chk);
+        if (chk != want) return;
+        op->eng->upload_beta(off, s.data(), d.data());
+        used = 1;
+    });
+    return rc ? -rc : used;
+}
+
+int ifgf_operator_upload_density(ifgf_operator* op, const double* phi) {
+    return guarded([&] {
+        need(op, "operator");
+        op->eng->upload_density(reinterpret_cast<const cplx*>(phi));
+    });
+}
+
+int ifgf_operator_time_applies(ifgf_operator* op, int iters, int flush_l2, double* ms) {
+    return guarded([&] {
+        need(op, "operator");
+        need(ms, "ms");
+        *ms = op->eng->time_device_applies(iters, flush_l2 != 0);
+    });
+}
+
+int ifgf_operator_time_phases(ifgf_operator* op, double* ms7) {
+    return guarded([&] {
+        need(op, "operator");
+        need(ms7, "ms7");
+        const PhaseTimes t = op->eng->time_phases();
+        const double v[7] = {t.weights, t.leaf, t.cousin, t.parent, t.near, t.rp, t.total};
+        std::memcpy(ms7, v, sizeof v);
+    });
+}
+
+int ifgf_operator_kernels_per_apply(const ifgf_operator* op) { return op ? op->eng->kernels_per_apply() : -1; }
+void* ifgf_operator_device_phi(ifgf_operator* op) { return op ? op->eng->device_phi() : nullptr; }
+void* ifgf_operator_device_out(ifgf_operator* op) { return op ? op->eng->device_out() : nullptr; }
+
+// ------------------------------------------------------------------ GMRES
+int ifgf_gmres_solve(ifgf_operator* op, const double* rhs, double tol, int max_iter, int restart, double* x,
+                     double* history, int history_cap, int* iterations, int* converged) {
+    return guarded([&] {
+        need(op, "operator");
+        need(rhs, "rhs");
+        const std::size_t n = op->eng->size();
+        const auto b = as_cplx(rhs, n);
+        ApplyFn apply = [&](const cplx* in, cplx* out) { op->eng->apply(in, out); };
+        GmresOutcome r;
+        try {
+            r = gmres(apply, b, tol, max_iter, restart);
+        } catch (const ConvergenceFailure& e) {
+            if (history)
+                for (int i = 0; i < history_cap && i < int(e.history.size()); ++i) history[i] = e.history[i];
+            if (iterations) *iterations = int(e.history.size());
+            throw;
+        }
+        if (x) std::memcpy(x, r.x.data(), n * sizeof(cplx));
+        if (history)
+            for (int i = 0; i < history_cap && i < int(r.history.size()); ++i) history[i] = r.history[i];
+        if (iterations) *iterations = r.iterations;
+        if (converged) *converged = r.converged ? 1 : 0;
+    });
+}
+
+int ifgf_solve(ifgf_operator* op, double theta, double phi, double tol, int max_iter, int restart, double* density,
+               double* history, int history_cap, int* iterations, int* converged) {
+    return guarded([&] {
+        need(op, "operator");
+        const Surface& s = *op->plan->surf;
+        const double k = op->plan->k;
+        const Vec3 dir{std::cos(theta) * std::sin(phi), std::sin(theta) * std::sin(phi), std::cos(phi)};
+        std::vector<double> rhs(2 * s.size());
+        for (std::size_t l = 0; l < s.size(); ++l) {
+            const cplx ui = std::polar(1.0, k * dot3(dir, s.pos[l]));
+            rhs[2 * l] = -ui.real();
+            rhs[2 * l + 1] = -ui.imag();
+        }
+        int it = 0, cv = 0;
+        const int rc = ifgf_gmres_solve(op, rhs.data(), tol, max_iter, restart, density, history, history_cap, &it, &cv);
+        if (iterations) *iterations = it;
+        if (converged) *converged = cv;
+        if (rc) throw EngineError(rc, g_error);
+        if (!cv)
+            throw ConvergenceFailure("solve: GMRES did not reach tolerance " + std::to_string(tol) + " in " +
+                                         std::to_string(it) + " iterations",
+                                     {});
+    });
+}
+
+}  // extern "C"

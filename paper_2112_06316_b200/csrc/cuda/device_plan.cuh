@@ -1,0 +1,42 @@
+// POD views of the HBM-resident plan, passed by value to the kernels.
+#pragma once
+
+#include <cstdint>
+
+namespace ifgfb200 {
+
+// Morton-ordered source/target points (structure of arrays)
+struct PointsDev {
+    const double *x, *y, *z;
+    const double *nx, *ny, *nz;
+};
+
+struct LevelDev {
+    int d = 0;
+    int nb = 0;      // boxes at this level
+    int nseg = 0;    // relevant segments
+    int ns = 0, nc = 0, ps = 0, pang = 0;
+    double ds = 0, dth = 0, dph = 0;
+    double h = 0;    // half diagonal of this level's boxes
+    const double *cx = nullptr, *cy = nullptr, *cz = nullptr;  // box centres
+    const std::uint32_t *beg = nullptr, *end = nullptr;       // Morton spans
+    const std::int32_t *cz_ptr = nullptr, *cz_idx = nullptr;  // cousin lists
+    const std::int64_t* cev_begin = nullptr;                  // per target box
+    const std::int32_t* cev_seg = nullptr;                    // per cousin evaluation
+    const std::int32_t *seg_box = nullptr, *seg_gamma = nullptr, *box_seg_begin = nullptr;
+    const std::int64_t* pev_begin = nullptr;  // per parent (level d-1) segment
+    const std::int32_t* pev_seg = nullptr;    // per parent-node evaluation into this level
+    const std::int32_t *ch_ptr = nullptr, *ch_idx = nullptr;  // children (level d+1) of this level's boxes
+    const double *s_nodes = nullptr, *th_nodes = nullptr, *ph_nodes = nullptr;
+    const std::int32_t *chunk_box = nullptr, *chunk_q0 = nullptr;  // cousin work chunks
+    int nchunk = 0;
+    int max_pts = 0;  // largest box
+};
+
+// factor codes carried by one level's coefficient store (W1..W4 = 1..4)
+struct Pipes {
+    int n = 0;
+    int f[3] = {0, 0, 0};
+};
+
+}  // namespace ifgfb200

@@ -1,0 +1,785 @@
+// Engine: uploads the host plan into HBM once and runs the per-apply kernel sequence
+//
+//   weights -> leaf_fill(D) -> [cousin_eval(d) -> parent_fill(d -> d-1)]_{d=D..4}
+//   -> cousin_eval(3) -> near_field -> density_coeffs -> rp_combine
+//
+// on one stream, captured into a CUDA graph after the first eager apply (ifgf_apply,
+// ifgf.cpp:577-608; layer_potentials + apply, solver.cpp:78-157). Only two IFGF levels of
+// coefficient blocks are live at a time (ifgf.cpp:589-597), in two ping-pong buffers.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <sstream>
+
+#include "../engine.hpp"
+#include "../host/chebyshev.hpp"
+#include "dev_common.cuh"
+#include "kernels.cuh"
+
+namespace ifgfb200 {
+
+namespace {
+
+constexpr int kChunk = 128;  // targets per CTA in the cousin / near-field work lists
+
+class DevBuf {
+  public:
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p_(o.p_), bytes_(o.bytes_) {
+        o.p_ = nullptr;
+        o.bytes_ = 0;
+    }
+    ~DevBuf() {
+        if (p_) cudaFree(p_);
+    }
+    void alloc(std::size_t bytes) {
+        if (p_) cudaFree(p_);
+        p_ = nullptr;
+        bytes_ = bytes;
+        if (bytes) IFGF_CUDA(cudaMalloc(&p_, bytes));
+    }
+    template <class T>
+    void upload(const std::vector<T>& v) {
+        alloc(v.size() * sizeof(T));
+        if (!v.empty()) IFGF_CUDA(cudaMemcpy(p_, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p_);
+    }
+    std::size_t bytes() const { return bytes_; }
+
+  private:
+    void* p_ = nullptr;
+    std::size_t bytes_ = 0;
+};
+
+struct LevelBufs {
+    DevBuf cx, cy, cz, beg, end, cz_ptr, cz_idx, cev_begin, cev_seg, seg_box, seg_gamma,
+        box_seg_begin, pev_begin, pev_seg, ch_ptr, ch_idx, s_nodes, th_nodes, ph_nodes,
+        chunk_box, chunk_q0;
+};
+
+Pipes make_pipes(const std::vector<int>& f) {
+    Pipes p;
+    p.n = int(f.size());
+    for (int i = 0; i < p.n && i < 3; ++i) p.f[i] = f[i];
+    return p;
+}
+
+}  // namespace
+
+struct Engine::Impl {
+    int dev = 0;
+    cudaStream_t st = nullptr;
+    std::mutex mu;
+    std::size_t n = 0;
+    int depth = 0;
+    double k = 0, gamma = 0;
+    DlStrategy strategy = DlStrategy::Hybrid;
+    int ps = 3, pang = 5;
+    const Surface* surf = nullptr;
+    const PairList* pairs = nullptr;
+    const BoxTree* tree = nullptr;
+
+    // points (Morton order)
+    DevBuf px, py, pz, pnx, pny, pnz, jw_p, ones_p, perm, pos, patch_p, identity;
+    // original order copies for the direct sum and beta
+    DevBuf ox, oy, oz, onx, ony, onz, ojw, opatch;
+    std::vector<LevelBufs> lb;   // [d-1]
+    std::vector<LevelDev> L;     // [d-1]
+    DevBuf Ms, Ma;
+    DevBuf storeA, storeB;
+    std::size_t store_elems = 0;
+    // near field
+    DevBuf nb_ptr, nb_idx, tpb, pair_patch, far_begin, far_end, far_pos, near_chunk_box, near_chunk_q0;
+    NearDev near;
+    // rp
+    DevBuf patch_nu, patch_nv, patch_start, mat_off, mats, beta_off, beta_s, beta_d, coeffs;
+    RpDev rp;
+    std::size_t beta_entries = 0;
+    bool beta_ready = false;
+    // beta inputs
+    DevBuf b_target, b_ubar, b_vbar, b_du, b_dv, b_orient, b_series_off, b_series, b_cutoff,
+        b_rule_x, b_rule_w;
+    int max_dudv = 1, max_nunv = 1;
+    // work vectors
+    DevBuf d_phi, d_out, d_S, d_D, a_p, Sp, Dp, scratch, flush;
+    PointsDev P;
+    DirectDev direct;
+    // graph of the full apply on (d_phi -> d_out, d_S, d_D)
+    cudaGraphExec_t graph = nullptr;
+    bool eager_done = false;
+    int kernels = 0;
+
+    std::vector<int> pipes_at(int d, bool single, bool dbl, DlStrategy s) const {
+        std::vector<int> p;
+        if (single) p.push_back(W1);
+        if (dbl) {
+            const auto x = dl_pipes(*tree, d, s);
+            p.insert(p.end(), x.begin(), x.end());
+        }
+        return p;
+    }
+
+    // the IFGF far field on a_p (Morton) into Sp/Dp (accumulated)
+    int run_ifgf(bool single, bool dbl, DlStrategy s, cudaEvent_t* ev = nullptr) {
+        int launches = 0;
+        if (depth < 3 || (!single && !dbl)) return 0;
+        double2* cur = storeA.as<double2>();
+        double2* nxt = storeB.as<double2>();
+        auto pipes_d = make_pipes(pipes_at(depth, single, dbl, s));
+        launch_leaf_fill(L[depth - 1], P, a_p.as<double2>(), k, pipes_d, Ms.as<double>(),
+                         Ma.as<double>(), cur, st);
+        ++launches;
+        if (ev) IFGF_CUDA(cudaEventRecord(ev[0], st));
+        for (int d = depth; d >= 3; --d) {
+            const Pipes pc = make_pipes(pipes_at(d, single, dbl, s));
+            launch_cousin_eval(L[d - 1], P, cur, k, pc, Sp.as<double2>(), Dp.as<double2>(), st);
+            ++launches;
+            if (d > 3) {
+                const Pipes pp = make_pipes(pipes_at(d - 1, single, dbl, s));
+                launch_parent_fill(L[d - 2], L[d - 1], cur, k, pp, pc, Ms.as<double>(),
+                                   Ma.as<double>(), nxt, st);
+                ++launches;
+                std::swap(cur, nxt);
+            }
+        }
+        return launches;
+    }
+
+    // full operator on d_phi -> out, S, D (device pointers)
+    int run_apply(const double2* phi, double2* out, double2* S, double2* D) {
+        int launches = 0;
+        IFGF_CUDA(cudaMemsetAsync(Sp.as<void>(), 0, n * sizeof(double2), st));
+        IFGF_CUDA(cudaMemsetAsync(Dp.as<void>(), 0, n * sizeof(double2), st));
+        launch_weights(int(n), perm.as<std::uint32_t>(), phi, jw_p.as<double>(), a_p.as<double2>(), st);
+        ++launches;
+        launches += run_ifgf(true, true, strategy);
+        launch_near_field(near, P, a_p.as<double2>(), k, Sp.as<double2>(), Dp.as<double2>(), st);
+        ++launches;
+        launch_density_coeffs(rp, phi, coeffs.as<double2>(), st);
+        launch_rp_combine(rp, coeffs.as<double2>(), phi, Sp.as<double2>(), Dp.as<double2>(), gamma,
+                          out, S, D, st);
+        launches += 2;
+        return launches;
+    }
+
+    void ensure_beta() {
+        if (!beta_ready) throw InternalError("beta tables not computed");
+    }
+
+    void apply_graph() {
+        if (!eager_done) {
+            kernels = run_apply(d_phi.as<double2>(), d_out.as<double2>(), d_S.as<double2>(),
+                                d_D.as<double2>());
+            IFGF_CUDA(cudaStreamSynchronize(st));
+            eager_done = true;
+            cudaGraph_t g;
+            IFGF_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            run_apply(d_phi.as<double2>(), d_out.as<double2>(), d_S.as<double2>(), d_D.as<double2>());
+            IFGF_CUDA(cudaStreamEndCapture(st, &g));
+            IFGF_CUDA(cudaGraphInstantiate(&graph, g, 0));
+            IFGF_CUDA(cudaGraphDestroy(g));
+            return;
+        }
+        IFGF_CUDA(cudaGraphLaunch(graph, st));
+    }
+};
+
+Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()) {
+    Impl& e = *d_;
+    e.dev = device;
+    IFGF_CUDA(cudaSetDevice(device));
+    IFGF_CUDA(cudaStreamCreateWithFlags(&e.st, cudaStreamNonBlocking));
+    const Surface& S = *s.surf;
+    const BoxTree& T = *s.tree;
+    const BoxRelations& R = *s.rel;
+    const ConePlanHost& C = *s.plan;
+    const PairList& PL = *s.pairs;
+    e.surf = s.surf;
+    e.pairs = s.pairs;
+    e.tree = s.tree;
+    e.n = S.size();
+    e.depth = T.depth;
+    e.k = s.k;
+    e.gamma = s.gamma;
+    e.strategy = s.strategy;
+    e.ps = C.params.ps;
+    e.pang = C.params.pang;
+    const std::size_t n = e.n;
+
+    // ---- points in Morton order
+    {
+        std::vector<double> x(n), y(n), z(n), nx(n), ny(n), nz(n), jw(n), one(n, 1.0);
+        std::vector<std::uint32_t> pos(n), ident(n);
+        std::vector<std::int32_t> pp(n);
+        for (std::size_t t = 0; t < n; ++t) {
+            const std::uint32_t l = T.perm[t];
+            x[t] = S.pos[l].x;
+            y[t] = S.pos[l].y;
+            z[t] = S.pos[l].z;
+            nx[t] = S.nrm[l].x;
+            ny[t] = S.nrm[l].y;
+            nz[t] = S.nrm[l].z;
+            jw[t] = S.jac[l] * S.wt[l];
+            pos[l] = std::uint32_t(t);
+            pp[t] = S.patch_of[l];
+            ident[t] = std::uint32_t(t);
+        }
+        e.px.upload(x);
+        e.py.upload(y);
+        e.pz.upload(z);
+        e.pnx.upload(nx);
+        e.pny.upload(ny);
+        e.pnz.upload(nz);
+        e.jw_p.upload(jw);
+        e.ones_p.upload(one);
+        e.perm.upload(T.perm);
+        e.pos.upload(pos);
+        e.patch_p.upload(pp);
+        e.identity.upload(ident);
+        e.P = {e.px.as<double>(), e.py.as<double>(), e.pz.as<double>(),
+               e.pnx.as<double>(), e.pny.as<double>(), e.pnz.as<double>()};
+        for (std::size_t l = 0; l < n; ++l) {
+            x[l] = S.pos[l].x;
+            y[l] = S.pos[l].y;
+            z[l] = S.pos[l].z;
+            nx[l] = S.nrm[l].x;
+            ny[l] = S.nrm[l].y;
+            nz[l] = S.nrm[l].z;
+            jw[l] = S.jac[l] * S.wt[l];
+        }
+        e.ox.upload(x);
+        e.oy.upload(y);
+        e.oz.upload(z);
+        e.onx.upload(nx);
+        e.ony.upload(ny);
+        e.onz.upload(nz);
+        e.ojw.upload(jw);
+        e.opatch.upload(S.patch_of);
+    }
+
+    // ---- IFGF levels
+    e.lb.resize(T.depth);
+    e.L.resize(T.depth);
+    std::size_t store = 0;
+    for (int d = 3; d <= T.depth; ++d) {
+        const BoxLevel& B = T.level[d - 1];
+        const ConeLevel& CL = C.level[d - 1];
+        LevelBufs& b = e.lb[d - 1];
+        LevelDev& L = e.L[d - 1];
+        const std::size_t nb = B.size();
+        std::vector<double> cx(nb), cy(nb), cz(nb);
+        int max_pts = 0;
+        for (std::size_t i = 0; i < nb; ++i) {
+            const Vec3 c = T.center(d, i);
+            cx[i] = c.x;
+            cy[i] = c.y;
+            cz[i] = c.z;
+            max_pts = std::max(max_pts, int(B.end[i] - B.begin[i]));
+        }
+        std::vector<std::int32_t> chunk_box, chunk_q0;
+        for (std::size_t i = 0; i < nb; ++i)
+            if (R.cousin[d - 1].count(i) > 0)
+                for (std::uint32_t q = 0; q < B.end[i] - B.begin[i]; q += kChunk) {
+                    chunk_box.push_back(std::int32_t(i));
+                    chunk_q0.push_back(std::int32_t(q));
+                }
+        b.cx.upload(cx);
+        b.cy.upload(cy);
+        b.cz.upload(cz);
+        b.beg.upload(B.begin);
+        b.end.upload(B.end);
+        b.cz_ptr.upload(R.cousin[d - 1].ptr);
+        b.cz_idx.upload(R.cousin[d - 1].idx);
+        b.cev_begin.upload(CL.cev_begin);
+        b.cev_seg.upload(CL.cev_seg);
+        b.seg_box.upload(CL.seg_box);
+        b.seg_gamma.upload(CL.seg_gamma);
+        b.box_seg_begin.upload(CL.box_seg_begin);
+        b.pev_begin.upload(CL.pev_begin);
+        b.pev_seg.upload(CL.pev_seg);
+        b.ch_ptr.upload(C.child_ptr[d - 1]);
+        b.ch_idx.upload(C.child_idx[d - 1]);
+        b.s_nodes.upload(CL.s_nodes);
+        b.th_nodes.upload(CL.th_nodes);
+        b.ph_nodes.upload(CL.ph_nodes);
+        b.chunk_box.upload(chunk_box);
+        b.chunk_q0.upload(chunk_q0);
+        L.d = d;
+        L.nb = int(nb);
+        L.nseg = int(CL.nseg());
+        L.ns = CL.ns;
+        L.nc = CL.nc;
+        L.ps = CL.ps;
+        L.pang = CL.pang;
+        L.ds = CL.ds;
+        L.dth = CL.dth;
+        L.dph = CL.dph;
+        L.h = T.half_diag(d);
+        L.cx = b.cx.as<double>();
+        L.cy = b.cy.as<double>();
+        L.cz = b.cz.as<double>();
+        L.beg = b.beg.as<std::uint32_t>();
+        L.end = b.end.as<std::uint32_t>();
+        L.cz_ptr = b.cz_ptr.as<std::int32_t>();
+        L.cz_idx = b.cz_idx.as<std::int32_t>();
+        L.cev_begin = b.cev_begin.as<std::int64_t>();
+        L.cev_seg = b.cev_seg.as<std::int32_t>();
+        L.seg_box = b.seg_box.as<std::int32_t>();
+        L.seg_gamma = b.seg_gamma.as<std::int32_t>();
+        L.box_seg_begin = b.box_seg_begin.as<std::int32_t>();
+        L.pev_begin = b.pev_begin.as<std::int64_t>();
+        L.pev_seg = b.pev_seg.as<std::int32_t>();
+        L.ch_ptr = b.ch_ptr.as<std::int32_t>();
+        L.ch_idx = b.ch_idx.as<std::int32_t>();
+        L.s_nodes = b.s_nodes.as<double>();
+        L.th_nodes = b.th_nodes.as<double>();
+        L.ph_nodes = b.ph_nodes.as<double>();
+        L.chunk_box = b.chunk_box.as<std::int32_t>();
+        L.chunk_q0 = b.chunk_q0.as<std::int32_t>();
+        L.nchunk = int(chunk_box.size());
+        L.max_pts = max_pts;
+        store = std::max(store, CL.nseg() * std::size_t(CL.nodes_per_seg()) * 3);
+    }
+    e.store_elems = store;
+    e.storeA.alloc(std::max<std::size_t>(store, 1) * sizeof(double2));
+    e.storeB.alloc(std::max<std::size_t>(store, 1) * sizeof(double2));
+    e.Ms.upload(cheb::transform(e.ps));
+    e.Ma.upload(cheb::transform(e.pang));
+
+    // ---- near field
+    {
+        const int D = T.depth;
+        const BoxLevel& B = T.level[D - 1];
+        std::vector<std::int32_t> chunk_box, chunk_q0;
+        for (std::size_t i = 0; i < B.size(); ++i)
+            for (std::uint32_t q = 0; q < B.end[i] - B.begin[i]; q += kChunk) {
+                chunk_box.push_back(std::int32_t(i));
+                chunk_q0.push_back(std::int32_t(q));
+            }
+        std::vector<std::uint32_t> fpos(PL.far_nodes.size());
+        std::vector<std::uint32_t> inv(n);
+        for (std::size_t t = 0; t < n; ++t) inv[T.perm[t]] = std::uint32_t(t);
+        for (std::size_t i = 0; i < fpos.size(); ++i) fpos[i] = inv[PL.far_nodes[i]];
+        if (D < 3) {
+            // leaf-level spans still needed for the near field
+            e.lb[D - 1].beg.upload(B.begin);
+            e.lb[D - 1].end.upload(B.end);
+        }
+        e.nb_ptr.upload(R.nbr[D - 1].ptr);
+        e.nb_idx.upload(R.nbr[D - 1].idx);
+        e.tpb.upload(PL.target_pair_begin);
+        e.pair_patch.upload(PL.patch);
+        e.far_begin.upload(PL.far_begin);
+        e.far_end.upload(PL.far_end);
+        e.far_pos.upload(fpos);
+        e.near_chunk_box.upload(chunk_box);
+        e.near_chunk_q0.upload(chunk_q0);
+        NearDev& N = e.near;
+        N.n = int(n);
+        N.nleaf = int(B.size());
+        N.perm = e.perm.as<std::uint32_t>();
+        N.beg = e.lb[D - 1].beg.as<std::uint32_t>();
+        N.end = e.lb[D - 1].end.as<std::uint32_t>();
+        N.nb_ptr = e.nb_ptr.as<std::int32_t>();
+        N.nb_idx = e.nb_idx.as<std::int32_t>();
+        N.patch_p = e.patch_p.as<std::int32_t>();
+        N.tpb = e.tpb.as<std::uint32_t>();
+        N.pair_patch = e.pair_patch.as<std::int32_t>();
+        N.far_begin = e.far_begin.as<std::uint32_t>();
+        N.far_end = e.far_end.as<std::uint32_t>();
+        N.far_pos = e.far_pos.as<std::uint32_t>();
+        N.chunk_box = e.near_chunk_box.as<std::int32_t>();
+        N.chunk_q0 = e.near_chunk_q0.as<std::int32_t>();
+        N.nchunk = int(chunk_box.size());
+    }
+
+    // ---- RP: patch transforms, pair lists; beta offsets
+    {
+        const std::size_t nq = S.patches.size();
+        std::vector<std::int32_t> nu(nq), nv(nq), du(nq), dv(nq), mat_off(2 * nq);
+        std::vector<std::int64_t> start(nq + 1), soff(nq + 1);
+        std::vector<double> mats, orient(nq), series, cutoff(nq);
+        std::vector<std::pair<int, std::int32_t>> cache;  // n -> offset
+        auto mat_for = [&](int m) {
+            for (auto& c : cache)
+                if (c.first == m) return c.second;
+            const auto M = cheb::transform(m);
+            const std::int32_t off = std::int32_t(mats.size());
+            mats.insert(mats.end(), M.begin(), M.end());
+            cache.push_back({m, off});
+            return off;
+        };
+        const std::vector<double> spacing = S.spacing();
+        int max_nn = 1;
+        for (std::size_t q = 0; q < nq; ++q) {
+            const Patch& p = S.patches[q];
+            nu[q] = p.nu;
+            nv[q] = p.nv;
+            du[q] = p.du;
+            dv[q] = p.dv;
+            orient[q] = p.orient;
+            start[q] = std::int64_t(S.patch_start[q]);
+            mat_off[2 * q] = mat_for(p.nu);
+            mat_off[2 * q + 1] = mat_for(p.nv);
+            max_nn = std::max(max_nn, p.nu * p.nv);
+            e.max_dudv = std::max({e.max_dudv, p.du, p.dv, p.nu, p.nv});
+            soff[q] = std::int64_t(series.size());
+            for (const auto* set : {&p.pos_c, &p.du_c, &p.dv_c})
+                for (int c = 0; c < 3; ++c) series.insert(series.end(), (*set)[c].begin(), (*set)[c].end());
+            cutoff[q] = std::max(1e-14, 1e-8 * spacing[q]);
+        }
+        start[nq] = std::int64_t(S.patch_start[nq]);
+        e.max_nunv = max_nn;
+        e.patch_nu.upload(nu);
+        e.patch_nv.upload(nv);
+        e.patch_start.upload(start);
+        e.mat_off.upload(mat_off);
+        e.mats.upload(mats);
+        std::vector<std::uint64_t> boff(PL.size() + 1, 0);
+        for (std::size_t i = 0; i < PL.size(); ++i) {
+            const Patch& p = S.patches[PL.patch[i]];
+            boff[i + 1] = boff[i] + std::uint64_t(p.nu) * p.nv;
+        }
+        e.beta_entries = boff.back();
+        e.beta_off.upload(boff);
+        e.beta_s.alloc(std::max<std::size_t>(e.beta_entries, 1) * sizeof(double2));
+        e.beta_d.alloc(std::max<std::size_t>(e.beta_entries, 1) * sizeof(double2));
+        e.coeffs.alloc(std::max<std::size_t>(n, 1) * sizeof(double2));
+        RpDev& rp = e.rp;
+        rp.n = int(n);
+        rp.npatch = int(nq);
+        rp.patch_nu = e.patch_nu.as<std::int32_t>();
+        rp.patch_nv = e.patch_nv.as<std::int32_t>();
+        rp.patch_start = e.patch_start.as<std::int64_t>();
+        rp.mat_off = e.mat_off.as<std::int32_t>();
+        rp.mats = e.mats.as<double>();
+        rp.tpb = e.tpb.as<std::uint32_t>();
+        rp.pair_patch = e.pair_patch.as<std::int32_t>();
+        rp.beta_off = e.beta_off.as<std::uint64_t>();
+        rp.beta_s = e.beta_s.as<double2>();
+        rp.beta_d = e.beta_d.as<double2>();
+        rp.pos = e.pos.as<std::uint32_t>();
+        rp.max_nn = max_nn;
+        // beta inputs
+        e.b_target.upload(PL.target);
+        e.b_ubar.upload(PL.ubar);
+        e.b_vbar.upload(PL.vbar);
+        e.b_du.upload(du);
+        e.b_dv.upload(dv);
+        e.b_orient.upload(orient);
+        e.b_series_off.upload(soff);
+        e.b_series.upload(series);
+        e.b_cutoff.upload(cutoff);
+        std::vector<double> rx, rw;
+        cheb::fejer(PL.cfg.n_beta, rx, rw);
+        e.b_rule_x.upload(rx);
+        e.b_rule_w.upload(rw);
+    }
+
+    // ---- direct-sum view and work vectors
+    e.direct = {int(n), e.ox.as<double>(), e.oy.as<double>(), e.oz.as<double>(), e.onx.as<double>(),
+                e.ony.as<double>(), e.onz.as<double>(), e.ojw.as<double>(), e.opatch.as<std::int32_t>(),
+                e.tpb.as<std::uint32_t>(), e.pair_patch.as<std::int32_t>()};
+    const std::size_t vb = std::max<std::size_t>(n, 1) * sizeof(double2);
+    for (DevBuf* b : {&e.d_phi, &e.d_out, &e.d_S, &e.d_D, &e.a_p, &e.Sp, &e.Dp, &e.scratch}) b->alloc(vb);
+    IFGF_CUDA(cudaDeviceSynchronize());
+}
+
+Engine::~Engine() {
+    if (d_) {
+        cudaSetDevice(d_->dev);
+        if (d_->graph) cudaGraphExecDestroy(d_->graph);
+        if (d_->st) cudaStreamDestroy(d_->st);
+    }
+}
+
+std::size_t Engine::size() const { return d_->n; }
+int Engine::device() const { return d_->dev; }
+
+void Engine::compute_beta() {
+    Impl& e = *d_;
+    std::lock_guard<std::mutex> g(e.mu);
+    IFGF_CUDA(cudaSetDevice(e.dev));
+    BetaDev B;
+    B.npairs = int(e.pairs->size());
+    B.n_beta = e.pairs->cfg.n_beta;
+    B.cov_d = e.pairs->cfg.cov_d;
+    B.k = e.k;
+    B.target = e.b_target.as<std::uint32_t>();
+    B.patch = e.pair_patch.as<std::int32_t>();
+    B.ubar = e.b_ubar.as<double>();
+    B.vbar = e.b_vbar.as<double>();
+    B.offset = e.beta_off.as<std::uint64_t>();
+    B.tx = e.ox.as<double>();
+    B.ty = e.oy.as<double>();
+    B.tz = e.oz.as<double>();
+    B.nu = e.patch_nu.as<std::int32_t>();
+    B.nv = e.patch_nv.as<std::int32_t>();
+    B.du = e.b_du.as<std::int32_t>();
+    B.dv = e.b_dv.as<std::int32_t>();
+    B.orient = e.b_orient.as<double>();
+    B.series_off = e.b_series_off.as<std::int64_t>();
+    B.series = e.b_series.as<double>();
+    B.cutoff = e.b_cutoff.as<double>();
+    B.rule_x = e.b_rule_x.as<double>();
+    B.rule_w = e.b_rule_w.as<double>();
+    launch_beta(B, e.beta_s.as<double2>(), e.beta_d.as<double2>(), e.max_dudv, e.max_nunv, e.st);
+    IFGF_CUDA(cudaStreamSynchronize(e.st));
+    e.beta_ready = true;
+}
+
+void Engine::upload_beta(const std::vector<std::uint64_t>& offset, const cplx* bs, const cplx* bd) {
+    Impl& e = *d_;
+    std::lock_guard<std::mutex> g(e.mu);
+    IFGF_CUDA(cudaSetDevice(e.dev));
+    if (offset.size() != e.pairs->size() + 1 || offset.back() != e.beta_entries)
+        throw InvalidArgument("upload_beta: table layout does not match the pair list");
+    IFGF_CUDA(cudaMemcpy(e.beta_s.as<void>(), bs, e.beta_entries * sizeof(double2), cudaMemcpyHostToDevice));
+    IFGF_CUDA(cudaMemcpy(e.beta_d.as<void>(), bd, e.beta_entries * sizeof(double2), cudaMemcpyHostToDevice));
+    e.beta_ready = true;
+}
+
+void Engine::download_beta(std::vector<std::uint64_t>& offset, std::vector<cplx>& bs,
+                           std::vector<cplx>& bd) {
+    Impl& e = *d_;
+    std::lock_guard<std::mutex> g(e.mu);
+    e.ensure_beta();
+    IFGF_CUDA(cudaSetDevice(e.dev));
+    offset.resize(e.pairs->size() + 1);
+    IFGF_CUDA(cudaMemcpy(offset.data(), e.beta_off.as<void>(), offset.size() * 8, cudaMemcpyDeviceToHost));
+    bs.resize(e.beta_entries);
+    bd.resize(e.beta_entries);
+    IFGF_CUDA(cudaMemcpy(bs.data(), e.beta_s.as<void>(), e.beta_entries * sizeof(double2), cudaMemcpyDeviceToHost));
+    IFGF_CUDA(cudaMemcpy(bd.data(), e.beta_d.as<void>(), e.beta_entries * sizeof(double2), cudaMemcpyDeviceToHost));
+}
+
+void Engine::apply(const cplx* phi, cplx* out, cplx* S, cplx* D) {
+    Impl& e = *d_;
+    std::lock_guard<std::mutex> g(e.mu);
+    e.ensure_beta();
+    IFGF_CUDA(cudaSetDevice(e.dev));
+    const std::size_t bytes = e.n * sizeof(double2);
+    IFGF_CUDA(cudaMemcpyAsync(e.d_phi.as<void>(), phi, bytes, cudaMemcpyHostToDevice, e.st));
+    e.apply_graph();
+    IFGF_CUDA(cudaMemcpyAsync(out, e.d_out.as<void>(), bytes, cudaMemcpyDeviceToHost, e.st));
+    if (S) IFGF_CUDA(cudaMemcpyAsync(S, e.d_S.as<void>(), bytes, cudaMemcpyDeviceToHost, e.st));
+    if (D) IFGF_CUDA(cudaMemcpyAsync(D, e.d_D.as<void>(), bytes, cudaMemcpyDeviceToHost, e.st));
+    IFGF_CUDA(cudaStreamSynchronize(e.st));
+}
+
+void Engine::apply_device(const void* phi, void* out, void* S, void* D) {
+    Impl& e = *d_;
+    std::lock_guard<std::mutex> g(e.mu);
+    e.ensure_beta();
+    IFGF_CUDA(cudaSetDevice(e.dev));
+    e.run_apply(static_cast<const double2*>(phi), static_cast<double2*>(out), static_cast<double2*>(S),
+                static_cast<double2*>(D));
+    IFGF_CUDA(cudaStreamSynchronize(e.st));
+}
+
+void Engine::ifgf_apply(const cplx* a, bool single, bool dbl, DlStrategy s, cplx* S, cplx* D) {
+    Impl& e = *d_;
+    std::lock_guard<std::mutex> g(e.mu);
+    IFGF_CUDA(cudaSetDevice(e.dev));
+    const std::size_t bytes = e.n * sizeof(double2);
+    IFGF_CUDA(cudaMemcpyAsync(e.d_phi.as<void>(), a, bytes, cudaMemcpyHostToDevice, e.st));
+    IFGF_CUDA(cudaMemsetAsync(e.Sp.as<void>(), 0, bytes, e.st));
+    IFGF_CUDA(cudaMemsetAsync(e.Dp.as<void>(), 0, bytes, e.st));
+    launch_weights(int(e.n), e.perm.as<std::uint32_t>(), e.d_phi.as<double2>(), e.ones_p.as<double>(),
+                   e.a_p.as<double2>(), e.st);
+    e.run_ifgf(single, dbl, s);
+    launch_unpermute(int(e.n), e.perm.as<std::uint32_t>(), e.Sp.as<double2>(), e.Dp.as<double2>(),
+                     e.d_S.as<double2>(), e.d_D.as<double2>(), e.st);
+    IFGF_CUDA(cudaMemcpyAsync(S, e.d_S.as<void>(), bytes, cudaMemcpyDeviceToHost, e.st));
+    IFGF_CUDA(cudaMemcpyAsync(D, e.d_D.as<void>(), bytes, cudaMemcpyDeviceToHost, e.st));
+    IFGF_CUDA(cudaStreamSynchronize(e.st));
+}
+
+void Engine::level_d_fill(const cplx* a_perm, const std::vector<int>& pipes, std::vector<cplx>& out) {
+    Impl& e = *d_;
+    std::lock_guard<std::mutex> g(e.mu);
+    IFGF_CUDA(cudaSetDevice(e.dev));
+    out.clear();
+    if (e.depth < 3) return;
+    if (pipes.empty() || pipes.size() > 3) throw InvalidArgument("level_d_fill: 1..3 pipelines");
+    const LevelDev& L = e.L[e.depth - 1];
+    const std::size_t total = std::size_t(L.nseg) * (L.ps * L.pang * L.pang) * pipes.size();
+    IFGF_CUDA(cudaMemcpyAsync(e.a_p.as<void>(), a_perm, e.n * sizeof(double2), cudaMemcpyHostToDevice, e.st));
+    launch_leaf_fill(L, e.P, e.a_p.as<double2>(), e.k, make_pipes(pipes), e.Ms.as<double>(),
+                     e.Ma.as<double>(), e.storeA.as<double2>(), e.st);
+    out.resize(total);
+    IFGF_CUDA(cudaMemcpyAsync(out.data(), e.storeA.as<void>(), total * sizeof(double2), cudaMemcpyDeviceToHost, e.st));
+    IFGF_CUDA(cudaStreamSynchronize(e.st));
+}
+
+void Engine::apply_direct(const cplx* phi, cplx* out) {
+    Impl& e = *d_;
+    std::lock_guard<std::mutex> g(e.mu);
+    e.ensure_beta();
+    IFGF_CUDA(cudaSetDevice(e.dev));
+    const std::size_t bytes = e.n * sizeof(double2);
+    IFGF_CUDA(cudaMemcpyAsync(e.d_phi.as<void>(), phi, bytes, cudaMemcpyHostToDevice, e.st));
+    launch_direct(e.direct, e.d_phi.as<double2>(), e.k, e.Sp.as<double2>(), e.Dp.as<double2>(), e.st);
+    RpDev rp = e.rp;
+    rp.pos = e.identity.as<std::uint32_t>();  // Sp/Dp are in original order here
+    launch_density_coeffs(rp, e.d_phi.as<double2>(), e.coeffs.as<double2>(), e.st);
+    launch_rp_combine(rp, e.coeffs.as<double2>(), e.d_phi.as<double2>(), e.Sp.as<double2>(),
+                      e.Dp.as<double2>(), e.gamma, e.scratch.as<double2>(), nullptr, nullptr, e.st);
+    IFGF_CUDA(cudaMemcpyAsync(out, e.scratch.as<void>(), bytes, cudaMemcpyDeviceToHost, e.st));
+    IFGF_CUDA(cudaStreamSynchronize(e.st));
+}
+
+void Engine::rp_apply(const cplx* phi, cplx* S, cplx* D) {
+    Impl& e = *d_;
+    std::lock_guard<std::mutex> g(e.mu);
+    e.ensure_beta();
+    IFGF_CUDA(cudaSetDevice(e.dev));
+    const std::size_t bytes = e.n * sizeof(double2);
+    IFGF_CUDA(cudaMemcpyAsync(e.d_phi.as<void>(), phi, bytes, cudaMemcpyHostToDevice, e.st));
+    IFGF_CUDA(cudaMemsetAsync(e.Sp.as<void>(), 0, bytes, e.st));
+    IFGF_CUDA(cudaMemsetAsync(e.Dp.as<void>(), 0, bytes, e.st));
+    launch_density_coeffs(e.rp, e.d_phi.as<double2>(), e.coeffs.as<double2>(), e.st);
+    launch_rp_combine(e.rp, e.coeffs.as<double2>(), e.d_phi.as<double2>(), e.Sp.as<double2>(),
+                      e.Dp.as<double2>(), 0.0, e.scratch.as<double2>(), e.d_S.as<double2>(),
+                      e.d_D.as<double2>(), e.st);
+    IFGF_CUDA(cudaMemcpyAsync(S, e.d_S.as<void>(), bytes, cudaMemcpyDeviceToHost, e.st));
+    IFGF_CUDA(cudaMemcpyAsync(D, e.d_D.as<void>(), bytes, cudaMemcpyDeviceToHost, e.st));
+    IFGF_CUDA(cudaStreamSynchronize(e.st));
+}
+
+void Engine::upload_density(const cplx* phi) {
+    Impl& e = *d_;
+    std::lock_guard<std::mutex> g(e.mu);
+    IFGF_CUDA(cudaSetDevice(e.dev));
+    IFGF_CUDA(cudaMemcpy(e.d_phi.as<void>(), phi, e.n * sizeof(double2), cudaMemcpyHostToDevice));
+}
+
+double Engine::time_device_applies(int iters, bool flush_l2) {
+    Impl& e = *d_;
+    std::lock_guard<std::mutex> g(e.mu);
+    e.ensure_beta();
+    IFGF_CUDA(cudaSetDevice(e.dev));
+    const std::size_t flush_bytes = std::size_t(256) << 20;  // 2x the 126 MB L2
+    if (flush_l2 && e.flush.bytes() < flush_bytes) e.flush.alloc(flush_bytes);
+    e.apply_graph();  // eager run + capture on first use
+    IFGF_CUDA(cudaStreamSynchronize(e.st));
+    cudaEvent_t a, b;
+    IFGF_CUDA(cudaEventCreate(&a));
+    IFGF_CUDA(cudaEventCreate(&b));
+    float total = 0.f;
+    for (int i = 0; i < iters; ++i) {
+        if (flush_l2) IFGF_CUDA(cudaMemsetAsync(e.flush.as<void>(), i & 0xff, flush_bytes, e.st));
+        IFGF_CUDA(cudaEventRecord(a, e.st));
+        e.apply_graph();
+        IFGF_CUDA(cudaEventRecord(b, e.st));
+        IFGF_CUDA(cudaEventSynchronize(b));
+        float ms = 0.f;
+        IFGF_CUDA(cudaEventElapsedTime(&ms, a, b));
+        total += ms;
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return iters > 0 ? double(total) / iters : 0.0;
+}
+
+PhaseTimes Engine::time_phases() {
+    Impl& e = *d_;
+    std::lock_guard<std::mutex> g(e.mu);
+    e.ensure_beta();
+    IFGF_CUDA(cudaSetDevice(e.dev));
+    PhaseTimes pt;
+    if (!e.eager_done) e.apply_graph();
+    IFGF_CUDA(cudaStreamSynchronize(e.st));
+    // events: start, weights, leaf, then per level (cousin, parent), near, rp
+    std::vector<cudaEvent_t> ev(4 + 2 * e.depth + 4);
+    for (auto& x : ev) IFGF_CUDA(cudaEventCreate(&x));
+    int ie = 0;
+    auto rec = [&] { IFGF_CUDA(cudaEventRecord(ev[ie++], e.st)); };
+    auto el = [&](int i0, int i1) {
+        float ms = 0.f;
+        IFGF_CUDA(cudaEventElapsedTime(&ms, ev[i0], ev[i1]));
+        return double(ms);
+    };
+    const double2* phi = e.d_phi.as<double2>();
+    rec();  // 0
+    IFGF_CUDA(cudaMemsetAsync(e.Sp.as<void>(), 0, e.n * sizeof(double2), e.st));
+    IFGF_CUDA(cudaMemsetAsync(e.Dp.as<void>(), 0, e.n * sizeof(double2), e.st));
+    launch_weights(int(e.n), e.perm.as<std::uint32_t>(), phi, e.jw_p.as<double>(), e.a_p.as<double2>(), e.st);
+    rec();  // 1
+    std::vector<std::pair<int, int>> cousin_ev, parent_ev;
+    if (e.depth >= 3) {
+        double2* cur = e.storeA.as<double2>();
+        double2* nxt = e.storeB.as<double2>();
+        launch_leaf_fill(e.L[e.depth - 1], e.P, e.a_p.as<double2>(), e.k,
+                         make_pipes(e.pipes_at(e.depth, true, true, e.strategy)), e.Ms.as<double>(),
+                         e.Ma.as<double>(), cur, e.st);
+        rec();  // 2
+        for (int d = e.depth; d >= 3; --d) {
+            const Pipes pc = make_pipes(e.pipes_at(d, true, true, e.strategy));
+            const int c0 = ie - 1;
+            launch_cousin_eval(e.L[d - 1], e.P, cur, e.k, pc, e.Sp.as<double2>(), e.Dp.as<double2>(), e.st);
+            rec();
+            cousin_ev.push_back({c0, ie - 1});
+            if (d > 3) {
+                const Pipes pp = make_pipes(e.pipes_at(d - 1, true, true, e.strategy));
+                const int p0 = ie - 1;
+                launch_parent_fill(e.L[d - 2], e.L[d - 1], cur, e.k, pp, pc, e.Ms.as<double>(),
+                                   e.Ma.as<double>(), nxt, e.st);
+                rec();
+                parent_ev.push_back({p0, ie - 1});
+                std::swap(cur, nxt);
+            }
+        }
+    } else {
+        rec();
+    }
+    const int n0 = ie - 1;
+    launch_near_field(e.near, e.P, e.a_p.as<double2>(), e.k, e.Sp.as<double2>(), e.Dp.as<double2>(), e.st);
+    rec();
+    const int r0 = ie - 1;
+    launch_density_coeffs(e.rp, phi, e.coeffs.as<double2>(), e.st);
+    launch_rp_combine(e.rp, e.coeffs.as<double2>(), phi, e.Sp.as<double2>(), e.Dp.as<double2>(), e.gamma,
+                      e.d_out.as<double2>(), e.d_S.as<double2>(), e.d_D.as<double2>(), e.st);
+    rec();
+    IFGF_CUDA(cudaEventSynchronize(ev[ie - 1]));
+    pt.weights = el(0, 1);
+    pt.leaf = el(1, 2);
+    for (auto& c : cousin_ev) pt.cousin += el(c.first, c.second);
+    for (auto& p : parent_ev) pt.parent += el(p.first, p.second);
+    pt.near = el(n0, n0 + 1);
+    pt.rp = el(r0, r0 + 1);
+    pt.total = el(0, ie - 1);
+    for (auto& x : ev) cudaEventDestroy(x);
+    return pt;
+}
+
+int Engine::kernels_per_apply() const {
+    const Impl& e = *d_;
+    // weights + leaf + cousin per level + parent per level>3 + near + coeffs + rp_combine
+    if (e.depth < 3) return 4;
+    return 1 + 1 + (e.depth - 2) + (e.depth - 3) + 1 + 2;
+}
+
+std::string Engine::describe() const {
+    const Impl& e = *d_;
+    std::ostringstream os;
+    os << "N=" << e.n << " depth=" << e.depth << " store_elems=" << e.store_elems
+       << " beta_entries=" << e.beta_entries << " pairs=" << e.pairs->size();
+    return os.str();
+}
+
+void* Engine::device_phi() { return d_->d_phi.as<void>(); }
+void* Engine::device_out() { return d_->d_out.as<void>(); }
+void Engine::sync() {
+    IFGF_CUDA(cudaSetDevice(d_->dev));
+    IFGF_CUDA(cudaStreamSynchronize(d_->st));
+}
+
+}  // namespace ifgfb200

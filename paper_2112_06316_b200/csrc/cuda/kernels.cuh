@@ -1,0 +1,103 @@
+// Launchers of the sm_100a kernels (one translation unit per kernel family).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "device_plan.cuh"
+
+namespace ifgfb200 {
+
+// index of each factor in a pipe set, -1 if absent
+struct PipeIndex {
+    int w1 = -1, w2 = -1, w3 = -1, w4 = -1;
+};
+
+// ---- IFGF far field (ifgf_kernels.cu) ----
+// level-D fill + block transform (ifgf.cpp:312-391), one CTA per leaf box
+void launch_leaf_fill(const LevelDev& L, const PointsDev& P, const double2* a_p, double k,
+                      const Pipes& pipes, const double* Ms, const double* Ma, double2* store,
+                      cudaStream_t st);
+// cousin interpolation into the targets (ifgf.cpp:396-450), one CTA per target chunk
+void launch_cousin_eval(const LevelDev& L, const PointsDev& P, const double2* store, double k,
+                        const Pipes& pipes, double2* Sp, double2* Dp, cudaStream_t st);
+// child -> parent re-centred interpolation + block transform (ifgf.cpp:452-568)
+void launch_parent_fill(const LevelDev& Lp, const LevelDev& Lc, const double2* child_store,
+                        double k, const Pipes& parent_pipes, const Pipes& child_pipes,
+                        const double* Ms, const double* Ma, double2* parent_store, cudaStream_t st);
+
+// ---- near field, RP, combine, direct (near_rp_kernels.cu) ----
+struct NearDev {
+    int n = 0;       // points
+    int nleaf = 0;
+    const std::uint32_t* perm = nullptr;      // Morton -> original
+    const std::uint32_t* beg = nullptr;       // leaf spans
+    const std::uint32_t* end = nullptr;
+    const std::int32_t *nb_ptr = nullptr, *nb_idx = nullptr;  // leaf neighbours
+    const std::int32_t* patch_p = nullptr;    // patch of each Morton point
+    const std::uint32_t* tpb = nullptr;       // pairs per ORIGINAL target (CSR, N+1)
+    const std::int32_t* pair_patch = nullptr;
+    const std::uint32_t *far_begin = nullptr, *far_end = nullptr;
+    const std::uint32_t* far_pos = nullptr;   // far nodes as Morton positions
+    const std::int32_t *chunk_box = nullptr, *chunk_q0 = nullptr;
+    int nchunk = 0;
+};
+void launch_weights(int n, const std::uint32_t* perm, const double2* phi, const double* jw_p,
+                    double2* a_p, cudaStream_t st);
+// S[perm[t]] = Sp[t], D[perm[t]] = Dp[t]
+void launch_unpermute(int n, const std::uint32_t* perm, const double2* Sp, const double2* Dp,
+                      double2* S, double2* D, cudaStream_t st);
+void launch_near_field(const NearDev& N, const PointsDev& P, const double2* a_p, double k,
+                       double2* Sp, double2* Dp, cudaStream_t st);
+
+struct RpDev {
+    int n = 0, npatch = 0;
+    const std::int32_t* patch_nu = nullptr;
+    const std::int32_t* patch_nv = nullptr;
+    const std::int64_t* patch_start = nullptr;   // node start (== coefficient start)
+    const std::int32_t* mat_off = nullptr;       // per patch: offsets of (Mu, Mv) in mats
+    const double* mats = nullptr;
+    const std::uint32_t* tpb = nullptr;          // pairs per original target
+    const std::int32_t* pair_patch = nullptr;
+    const std::uint64_t* beta_off = nullptr;     // per pair
+    const double2 *beta_s = nullptr, *beta_d = nullptr;
+    const std::uint32_t* pos = nullptr;          // original -> Morton
+    int max_nn = 0;
+};
+void launch_density_coeffs(const RpDev& R, const double2* phi, double2* coeffs, cudaStream_t st);
+// out[l] = 1/2 phi + (D_far+near+rp) - i gamma (S_far+near+rp); S/D written when non-null
+void launch_rp_combine(const RpDev& R, const double2* coeffs, const double2* phi,
+                       const double2* Sp, const double2* Dp, double gamma, double2* out,
+                       double2* S, double2* D, cudaStream_t st);
+
+// non-accelerated: every non-singular pair directly (rp.cpp:481-513), original order
+struct DirectDev {
+    int n = 0;
+    const double *x, *y, *z, *nx, *ny, *nz, *jw;
+    const std::int32_t* patch_of;
+    const std::uint32_t* tpb;
+    const std::int32_t* pair_patch;
+};
+void launch_direct(const DirectDev& Dd, const double2* phi, double k, double2* S, double2* D,
+                   cudaStream_t st);
+
+// ---- beta tables (beta_kernel.cu) ----
+struct BetaDev {
+    int npairs = 0, n_beta = 0, cov_d = 0;
+    double k = 0;
+    const std::uint32_t* target = nullptr;
+    const std::int32_t* patch = nullptr;
+    const double *ubar = nullptr, *vbar = nullptr;
+    const std::uint64_t* offset = nullptr;
+    const double *tx = nullptr, *ty = nullptr, *tz = nullptr;   // target positions (original order)
+    // per patch: dims and series (pos, d/du, d/dv; 3 comps each, du*dv, u fastest)
+    const std::int32_t *nu = nullptr, *nv = nullptr, *du = nullptr, *dv = nullptr;
+    const double* orient = nullptr;
+    const std::int64_t* series_off = nullptr;  // start of the 9 series of a patch
+    const double* series = nullptr;
+    const double* cutoff = nullptr;            // per patch: max(1e-14, 1e-8 spacing)
+    const double *rule_x = nullptr, *rule_w = nullptr;  // Fejér nodes/weights, n_beta
+};
+void launch_beta(const BetaDev& B, double2* bs, double2* bd, int max_dudv, int max_nunv,
+                 cudaStream_t st);
+
+}  // namespace ifgfb200

@@ -1,0 +1,280 @@
+// Near-field, RP singular correction, combine and direct-sum kernels for sm_100a.
+//
+//  * weights      : a_m = phi_m J_m w_m gathered into Morton order (solver.cpp:87-88,
+//                   ifgf.cpp:586-587)
+//  * near_field   : level-D neighbour sum minus singular-patch exclusions and far-node
+//                   corrections (solver.cpp:100-144); one thread per target, sources of the
+//                   <=27 neighbour leaves read by the whole warp in lock step (broadcast).
+//  * density_coeffs + rp_combine : per-patch 2-D Chebyshev coefficients of phi
+//                   (rp.cpp:400-417) and the per-(target, patch) beta dot products
+//                   (rp.cpp:421-451), one warp per target with coalesced beta streaming,
+//                   fused with 1/2 phi + D - i gamma S (solver.cpp:152-156) and the
+//                   Morton un-permute (ifgf.cpp:603-606).
+//  * direct       : layer_potential_direct's regular part (rp.cpp:481-513), O(N^2).
+#include "dev_common.cuh"
+#include "kernels.cuh"
+
+namespace ifgfb200 {
+namespace {
+
+using namespace dev;
+
+constexpr int kNearThreads = 128;
+constexpr int kMaxSing = 8;
+
+__global__ void weights_kernel(int n, const std::uint32_t* __restrict__ perm,
+                               const double2* __restrict__ phi, const double* __restrict__ jw_p,
+                               double2* __restrict__ a_p) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    a_p[t] = cscale(phi[perm[t]], jw_p[t]);
+}
+
+__global__ void unpermute_kernel(int n, const std::uint32_t* __restrict__ perm,
+                                 const double2* __restrict__ Sp, const double2* __restrict__ Dp,
+                                 double2* __restrict__ S, double2* __restrict__ D) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const std::uint32_t l = perm[t];
+    S[l] = Sp[t];
+    D[l] = Dp[t];
+}
+
+// G a and dG/dnu_y a for one pair, accumulated with sign sg
+__device__ __forceinline__ void pair_kernels(double x, double y, double z, double yx, double yy,
+                                             double yz, double nx, double ny, double nz, double2 a,
+                                             double k, double sg, double2& accS, double2& accD) {
+    const double dx = x - yx, dy = y - yy, dz = z - yz;
+    const double r = sqrt(fma(dx, dx, fma(dy, dy, dz * dz)));
+    const double inv = 1.0 / r;
+    double sn, cs;
+    sincos(k * r, &sn, &cs);
+    const double g = kInv4PiD * inv;
+    const double2 ga = cmul(make_double2(cs * g, sn * g), a);
+    accS.x = fma(sg, ga.x, accS.x);
+    accS.y = fma(sg, ga.y, accS.y);
+    const double dn = fma(dx, nx, fma(dy, ny, dz * nz));
+    const double kr = k * r;
+    const double f = dn * kInv4PiD * inv * inv * inv;
+    const double2 e = make_double2(fma(kr, sn, cs) * f, fma(-kr, cs, sn) * f);  // e^{ikr}(1-ikr) f
+    const double2 da = cmul(e, a);
+    accD.x = fma(sg, da.x, accD.x);
+    accD.y = fma(sg, da.y, accD.y);
+}
+
+__global__ void __launch_bounds__(kNearThreads)
+near_kernel(NearDev N, PointsDev P, const double2* __restrict__ a_p, double k,
+            double2* __restrict__ Sp, double2* __restrict__ Dp) {
+    const int c = blockIdx.x;
+    const int tb = N.chunk_box[c];
+    const int tbeg = int(N.beg[tb]);
+    const int n_t = int(N.end[tb]) - tbeg;
+    const int q = N.chunk_q0[c] + threadIdx.x;
+    const bool act = q < n_t;
+    const int t = act ? tbeg + q : tbeg;
+    const std::uint32_t l = N.perm[t];
+    const double x = P.x[t], y = P.y[t], z = P.z[t];
+    const int p0 = int(N.tpb[l]), p1 = int(N.tpb[l + 1]);
+    const int nsing = p1 - p0;
+    int sing[kMaxSing];
+#pragma unroll
+    for (int i = 0; i < kMaxSing; ++i) sing[i] = (i < nsing) ? N.pair_patch[p0 + i] : -1;
+    double2 accS = make_double2(0.0, 0.0), accD = make_double2(0.0, 0.0);
+    for (int j = N.nb_ptr[tb]; j < N.nb_ptr[tb + 1]; ++j) {
+        const int nb = N.nb_idx[j];
+        const int u1 = int(N.end[nb]);
+        for (int u = int(N.beg[nb]); u < u1; ++u) {
+            if (!act || u == t) continue;
+            const int pq = N.patch_p[u];
+            bool skip = false;
+#pragma unroll
+            for (int i = 0; i < kMaxSing; ++i) skip |= (sing[i] == pq);
+            if (nsing > kMaxSing)
+                for (int i = kMaxSing; i < nsing; ++i) skip |= (N.pair_patch[p0 + i] == pq);
+            if (skip) continue;
+            pair_kernels(x, y, z, P.x[u], P.y[u], P.z[u], P.nx[u], P.ny[u], P.nz[u], a_p[u], k, 1.0,
+                         accS, accD);
+        }
+    }
+    if (!act) return;
+    // far-node corrections of the singular patches (solver.cpp:131-139)
+    for (int p = p0; p < p1; ++p)
+        for (std::uint32_t f = N.far_begin[p]; f < N.far_end[p]; ++f) {
+            const int u = int(N.far_pos[f]);
+            pair_kernels(x, y, z, P.x[u], P.y[u], P.z[u], P.nx[u], P.ny[u], P.nz[u], a_p[u], k, -1.0,
+                         accS, accD);
+        }
+    Sp[t] = cadd(Sp[t], accS);
+    Dp[t] = cadd(Dp[t], accD);
+}
+
+// one CTA per patch: a^q = Mv (Mu phi_q) along u then v (chebyshev.cpp:43-61)
+__global__ void density_coeffs_kernel(RpDev R, const double2* __restrict__ phi,
+                                      double2* __restrict__ coeffs) {
+    extern __shared__ double2 tmp[];
+    const int q = blockIdx.x;
+    const int nu = R.patch_nu[q], nv = R.patch_nv[q];
+    const std::int64_t st = R.patch_start[q];
+    const double* Mu = R.mats + R.mat_off[2 * q];
+    const double* Mv = R.mats + R.mat_off[2 * q + 1];
+    const int nn = nu * nv;
+    for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+        const int i = e % nu, j = e / nu;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int kk = 0; kk < nu; ++kk) cfma_r(acc, phi[st + kk + std::int64_t(nu) * j], Mu[i * nu + kk]);
+        tmp[e] = acc;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+        const int i = e % nu, j = e / nu;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int kk = 0; kk < nv; ++kk) cfma_r(acc, tmp[i + nu * kk], Mv[j * nv + kk]);
+        coeffs[st + e] = acc;
+    }
+}
+
+__global__ void rp_combine_kernel(RpDev R, const double2* __restrict__ coeffs,
+                                  const double2* __restrict__ phi, const double2* __restrict__ Sp,
+                                  const double2* __restrict__ Dp, double gamma,
+                                  double2* __restrict__ out, double2* __restrict__ S,
+                                  double2* __restrict__ D) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= R.n) return;
+    const int l = warp;
+    double2 as = make_double2(0.0, 0.0), ad = make_double2(0.0, 0.0);
+    for (std::uint32_t p = R.tpb[l]; p < R.tpb[l + 1]; ++p) {
+        const int q = R.pair_patch[p];
+        const int nn = R.patch_nu[q] * R.patch_nv[q];
+        const double2* a = coeffs + R.patch_start[q];
+        const double2* bs = R.beta_s + R.beta_off[p];
+        const double2* bd = R.beta_d + R.beta_off[p];
+        for (int i = lane; i < nn; i += 32) {
+            const double2 ai = a[i];
+            cfma(as, ai, __ldcs(bs + i));
+            cfma(ad, ai, __ldcs(bd + i));
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        as.x += __shfl_xor_sync(0xffffffffu, as.x, o);
+        as.y += __shfl_xor_sync(0xffffffffu, as.y, o);
+        ad.x += __shfl_xor_sync(0xffffffffu, ad.x, o);
+        ad.y += __shfl_xor_sync(0xffffffffu, ad.y, o);
+    }
+    if (lane != 0) return;
+    const int t = int(R.pos[l]);
+    const double2 s = cadd(Sp[t], as);
+    const double2 d = cadd(Dp[t], ad);
+    const double2 f = phi[l];
+    out[l] = make_double2(0.5 * f.x + d.x + gamma * s.y, 0.5 * f.y + d.y - gamma * s.x);
+    if (S) S[l] = s;
+    if (D) D[l] = d;
+}
+
+constexpr int kDirectThreads = 256;
+
+__global__ void __launch_bounds__(kDirectThreads)
+direct_kernel(DirectDev Dd, const double2* __restrict__ phi, double k, double2* __restrict__ S,
+              double2* __restrict__ D) {
+    __shared__ double sx[kDirectThreads], sy[kDirectThreads], sz[kDirectThreads];
+    __shared__ double snx[kDirectThreads], sny[kDirectThreads], snz[kDirectThreads];
+    __shared__ double2 sa[kDirectThreads];
+    __shared__ int spq[kDirectThreads];
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool act = l < Dd.n;
+    double x = 0, y = 0, z = 0;
+    int sing[kMaxSing];
+    int p0 = 0, nsing = 0;
+    if (act) {
+        x = Dd.x[l];
+        y = Dd.y[l];
+        z = Dd.z[l];
+        p0 = int(Dd.tpb[l]);
+        nsing = int(Dd.tpb[l + 1]) - p0;
+    }
+#pragma unroll
+    for (int i = 0; i < kMaxSing; ++i) sing[i] = (i < nsing) ? Dd.pair_patch[p0 + i] : -1;
+    double2 accS = make_double2(0.0, 0.0), accD = make_double2(0.0, 0.0);
+    for (int m0 = 0; m0 < Dd.n; m0 += kDirectThreads) {
+        __syncthreads();
+        const int m = m0 + threadIdx.x;
+        if (m < Dd.n) {
+            sx[threadIdx.x] = Dd.x[m];
+            sy[threadIdx.x] = Dd.y[m];
+            sz[threadIdx.x] = Dd.z[m];
+            snx[threadIdx.x] = Dd.nx[m];
+            sny[threadIdx.x] = Dd.ny[m];
+            snz[threadIdx.x] = Dd.nz[m];
+            sa[threadIdx.x] = cscale(phi[m], Dd.jw[m]);
+            spq[threadIdx.x] = Dd.patch_of[m];
+        }
+        __syncthreads();
+        if (!act) continue;
+        const int cnt = min(kDirectThreads, Dd.n - m0);
+        for (int j = 0; j < cnt; ++j) {
+            if (m0 + j == l) continue;
+            const int pq = spq[j];
+            bool skip = false;
+#pragma unroll
+            for (int i = 0; i < kMaxSing; ++i) skip |= (sing[i] == pq);
+            if (nsing > kMaxSing)
+                for (int i = kMaxSing; i < nsing; ++i) skip |= (Dd.pair_patch[p0 + i] == pq);
+            if (skip) continue;
+            pair_kernels(x, y, z, sx[j], sy[j], sz[j], snx[j], sny[j], snz[j], sa[j], k, 1.0, accS, accD);
+        }
+    }
+    if (!act) return;
+    S[l] = accS;
+    D[l] = accD;
+}
+
+}  // namespace
+
+void launch_weights(int n, const std::uint32_t* perm, const double2* phi, const double* jw_p,
+                    double2* a_p, cudaStream_t st) {
+    if (n == 0) return;
+    weights_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, perm, phi, jw_p, a_p);
+    IFGF_CUDA(cudaGetLastError());
+}
+
+void launch_unpermute(int n, const std::uint32_t* perm, const double2* Sp, const double2* Dp,
+                      double2* S, double2* D, cudaStream_t st) {
+    if (n == 0) return;
+    unpermute_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, perm, Sp, Dp, S, D);
+    IFGF_CUDA(cudaGetLastError());
+}
+
+void launch_near_field(const NearDev& N, const PointsDev& P, const double2* a_p, double k,
+                       double2* Sp, double2* Dp, cudaStream_t st) {
+    if (N.nchunk == 0) return;
+    near_kernel<<<N.nchunk, kNearThreads, 0, st>>>(N, P, a_p, k, Sp, Dp);
+    IFGF_CUDA(cudaGetLastError());
+}
+
+void launch_density_coeffs(const RpDev& R, const double2* phi, double2* coeffs, cudaStream_t st) {
+    if (R.npatch == 0) return;
+    const int threads = R.max_nn >= 256 ? 256 : ((R.max_nn + 31) / 32) * 32;
+    density_coeffs_kernel<<<R.npatch, threads, std::size_t(R.max_nn) * sizeof(double2), st>>>(R, phi, coeffs);
+    IFGF_CUDA(cudaGetLastError());
+}
+
+void launch_rp_combine(const RpDev& R, const double2* coeffs, const double2* phi,
+                       const double2* Sp, const double2* Dp, double gamma, double2* out,
+                       double2* S, double2* D, cudaStream_t st) {
+    if (R.n == 0) return;
+    const int threads = 256;
+    const long warps = R.n;
+    const int grid = int((warps * 32 + threads - 1) / threads);
+    rp_combine_kernel<<<grid, threads, 0, st>>>(R, coeffs, phi, Sp, Dp, gamma, out, S, D);
+    IFGF_CUDA(cudaGetLastError());
+}
+
+void launch_direct(const DirectDev& Dd, const double2* phi, double k, double2* S, double2* D,
+                   cudaStream_t st) {
+    if (Dd.n == 0) return;
+    direct_kernel<<<(Dd.n + kDirectThreads - 1) / kDirectThreads, kDirectThreads, 0, st>>>(Dd, phi, k, S, D);
+    IFGF_CUDA(cudaGetLastError());
+}
+
+}  // namespace ifgfb200

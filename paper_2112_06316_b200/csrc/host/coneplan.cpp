@@ -1,0 +1,297 @@
+#include "coneplan.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <exception>
+#include <mutex>
+#include <sstream>
+
+#include "chebyshev.hpp"
+
+namespace ifgfb200 {
+
+namespace {
+
+constexpr double kTwoPiC = 2.0 * kPi;
+constexpr int kMaxOrder = 12;
+
+struct Cone {
+    double s, th, ph;
+};
+
+// kernels.cpp:34-48
+inline Cone to_cone(const Vec3& x, const Vec3& c, double h) {
+    const Vec3 v = x - c;
+    const double r = len(v);
+    if (r < 1e-300) throw InvalidArgument("cone coordinates: point at box center");
+    Cone o;
+    o.s = h / r;
+    double ct = v.z / r;
+    ct = std::min(1.0, std::max(-1.0, ct));
+    o.th = std::acos(ct);
+    double ph = std::atan2(v.y, v.x);
+    if (ph < 0.0) ph += kTwoPiC;
+    if (ph >= kTwoPiC) ph = 0.0;
+    o.ph = ph;
+    return o;
+}
+
+// kernels.cpp:27-32
+inline Vec3 from_cone(double s, double th, double ph, const Vec3& c, double h) {
+    if (s <= 0.0) throw InvalidArgument("cone point: s must be positive");
+    const double r = h / s;
+    const double st = std::sin(th), ct = std::cos(th);
+    return c + Vec3{r * st * std::cos(ph), r * st * std::sin(ph), r * ct};
+}
+
+// LevelCones::segment_of (ifgf.cpp:161-176), returned as the gamma index of ifgf.hpp:34-36
+inline int segment_gamma(const ConeLevel& L, const Cone& c) {
+    if (c.s > kConeEtaC + 1e-12)
+        throw InternalError("cone segment query with s > sqrt(3)/3: s=" + std::to_string(c.s));
+    int g1 = int(std::floor(c.s / L.ds)) + 1;
+    if (g1 > L.ns) g1 = L.ns;
+    if (g1 < 1) g1 = 1;
+    int g2, g3;
+    if (c.th >= kPi) {
+        g2 = L.nc;
+        g3 = 2 * L.nc;
+    } else {
+        g2 = std::min(L.nc, int(std::floor(c.th / L.dth)) + 1);
+        if (g2 < 1) g2 = 1;
+        g3 = std::min(2 * L.nc, int(std::floor(c.ph / L.dph)) + 1);
+        if (g3 < 1) g3 = 1;
+    }
+    return (g1 - 1) + L.ns * ((g2 - 1) + L.nc * (g3 - 1));
+}
+
+ConeLevel make_level(int d, double side, double lambda, const ConeParams& p) {
+    ConeLevel L;
+    L.d = d;
+    const int m = cone_doublings(side, lambda);
+    L.ns = p.n_s0 << m;
+    L.nc = p.n_c0 << m;
+    L.ps = p.ps;
+    L.pang = p.pang;
+    L.ds = kConeEtaC / L.ns;
+    L.dth = kPi / L.nc;
+    L.dph = kPi / L.nc;
+    const auto xs = cheb::gauss_nodes(p.ps);
+    const auto xa = cheb::gauss_nodes(p.pang);
+    auto table = [](int cells, double width, const std::vector<double>& x) {
+        std::vector<double> t(std::size_t(cells) * x.size());
+        for (int g = 0; g < cells; ++g)
+            for (std::size_t i = 0; i < x.size(); ++i)
+                t[std::size_t(g) * x.size() + i] = g * width + (x[i] + 1.0) * 0.5 * width;
+        return t;
+    };
+    L.s_nodes = table(L.ns, L.ds, xs);
+    L.th_nodes = table(L.nc, L.dth, xa);
+    L.ph_nodes = table(2 * L.nc, L.dph, xa);
+    return L;
+}
+
+// Runs body(i) for i in [0, n) on the OpenMP team; the first exception is rethrown after
+// the region (the reference's ParallelErrors, common.hpp:71-92).
+template <class F>
+void parallel_for(std::int64_t n, int workers, F&& body) {
+    std::exception_ptr err;
+    std::atomic<bool> failed{false};
+    std::mutex mu;
+#pragma omp parallel for schedule(dynamic, 4) num_threads(workers)
+    for (std::int64_t i = 0; i < n; ++i) {
+        if (failed.load(std::memory_order_relaxed)) continue;
+        try {
+            body(i);
+        } catch (...) {
+            std::lock_guard<std::mutex> g(mu);
+            if (!failed) {
+                err = std::current_exception();
+                failed = true;
+            }
+        }
+    }
+    if (err) std::rethrow_exception(err);
+}
+
+inline void mark(std::vector<std::uint8_t>& m, std::size_t at) {
+    __atomic_store_n(&m[at], std::uint8_t(1), __ATOMIC_RELAXED);
+}
+
+}  // namespace
+
+int cone_doublings(double side, double lambda) {
+    const double ratio = side / (0.3 * lambda);
+    return std::max(0, int(std::floor(std::log2(ratio * (1.0 + 1e-9)))) + 1);
+}
+
+std::vector<int> dl_pipes(const BoxTree& t, int level, DlStrategy s) {
+    switch (s) {
+        case DlStrategy::W4:
+            return {W4};
+        case DlStrategy::W2W3:
+            return {W2, W3};
+        case DlStrategy::Hybrid: {
+            const double lambda = 2.0 * kPi / t.k;
+            if (t.side(level) / lambda < 0.5 - 1e-12) return {W2, W3};
+            return {W4};
+        }
+    }
+    return {W4};
+}
+
+ConePlanHost build_cone_plan(const BoxTree& t, const BoxRelations& rel,
+                             const std::vector<Vec3>& pts, const ConeParams& p, int workers) {
+    if (p.ps < 1 || p.ps > kMaxOrder || p.pang < 1 || p.pang > kMaxOrder)
+        throw InvalidArgument("plan_cones: interpolation orders must lie in [1,12]");
+    if (p.n_s0 < 1 || p.n_c0 < 1) throw InvalidArgument("plan_cones: interval counts must be positive");
+    const int w = worker_count(workers);
+    ConePlanHost plan;
+    plan.params = p;
+    plan.k = t.k;
+    const double lambda = 2.0 * kPi / t.k;
+    const int D = t.depth;
+    plan.level.resize(D);
+    plan.child_ptr.resize(D);
+    plan.child_idx.resize(D);
+    for (int d = 1; d <= D; ++d) {
+        const BoxLevel& B = t.level[d - 1];
+        auto& cp = plan.child_ptr[d - 1];
+        auto& ci = plan.child_idx[d - 1];
+        cp.assign(B.size() + 1, 0);
+        for (std::size_t b = 0; b < B.size(); ++b) {
+            for (std::int32_t ch : B.child[b])
+                if (ch >= 0) ci.push_back(ch);
+            cp[b + 1] = std::int32_t(ci.size());
+        }
+    }
+
+    for (int d = 3; d <= D; ++d) {
+        ConeLevel& L = plan.level[d - 1];
+        L = make_level(d, t.side(d), lambda, p);
+        const BoxLevel& B = t.level[d - 1];
+        const std::size_t nb = B.size();
+        const std::size_t spb = std::size_t(L.segs_per_box());
+        const double h = t.half_diag(d);
+        std::vector<Vec3> ctr(nb);
+        for (std::size_t b = 0; b < nb; ++b) ctr[b] = t.center(d, b);
+        std::vector<std::uint8_t> marks(nb * spb, 0);
+
+        // (1) cousin target points, evaluated in the frame of each cousin source box
+        const Adjacency& cz = rel.cousin[d - 1];
+        L.cev_begin.assign(nb + 1, 0);
+        for (std::size_t b = 0; b < nb; ++b)
+            L.cev_begin[b + 1] = L.cev_begin[b] + std::int64_t(cz.count(b)) * (B.end[b] - B.begin[b]);
+        L.cev_seg.assign(std::size_t(L.cev_begin[nb]), 0);
+        parallel_for(std::int64_t(nb), w, [&](std::int64_t tb) {
+            const std::uint32_t n_t = B.end[tb] - B.begin[tb];
+            std::int64_t at = L.cev_begin[tb];
+            for (std::int32_t j = cz.ptr[tb]; j < cz.ptr[tb + 1]; ++j) {
+                const std::int32_t sb = cz.idx[j];
+                for (std::uint32_t q = 0; q < n_t; ++q) {
+                    const int g = segment_gamma(L, to_cone(pts[B.begin[tb] + q], ctr[sb], h));
+                    L.cev_seg[at++] = g;
+                    mark(marks, std::size_t(sb) * spb + g);
+                }
+            }
+        });
+
+        // (2) interpolation nodes of every relevant parent segment, in each child's frame
+        if (d > 3) {
+            const ConeLevel& PL = plan.level[d - 2];
+            const double ph = t.half_diag(d - 1);
+            const auto& cptr = plan.child_ptr[d - 2];
+            const auto& cidx = plan.child_idx[d - 2];
+            const int P = PL.nodes_per_seg();
+            const std::size_t pseg = PL.nseg();
+            L.pev_begin.assign(pseg + 1, 0);
+            for (std::size_t so = 0; so < pseg; ++so) {
+                const std::int32_t pb = PL.seg_box[so];
+                L.pev_begin[so + 1] = L.pev_begin[so] + std::int64_t(P) * (cptr[pb + 1] - cptr[pb]);
+            }
+            L.pev_seg.assign(std::size_t(L.pev_begin[pseg]), 0);
+            parallel_for(std::int64_t(pseg), w, [&](std::int64_t so) {
+                const std::int32_t pb = PL.seg_box[so];
+                const int gam = PL.seg_gamma[so];
+                const int g1 = gam % PL.ns, g2 = (gam / PL.ns) % PL.nc, g3 = gam / PL.ns / PL.nc;
+                const Vec3 pc = t.center(d - 1, std::size_t(pb));
+                const int nch = cptr[pb + 1] - cptr[pb];
+                for (int ip = 0; ip < PL.pang; ++ip)
+                    for (int it = 0; it < PL.pang; ++it)
+                        for (int is = 0; is < PL.ps; ++is) {
+                            const Vec3 x = from_cone(PL.s_nodes[std::size_t(g1) * PL.ps + is],
+                                                     PL.th_nodes[std::size_t(g2) * PL.pang + it],
+                                                     PL.ph_nodes[std::size_t(g3) * PL.pang + ip], pc, ph);
+                            const int node = is + PL.ps * (it + PL.pang * ip);
+                            std::int64_t at = L.pev_begin[so] + std::int64_t(node) * nch;
+                            for (int c = 0; c < nch; ++c) {
+                                const std::int32_t ch = cidx[cptr[pb] + c];
+                                const int g = segment_gamma(L, to_cone(x, ctr[ch], h));
+                                L.pev_seg[at++] = g;
+                                mark(marks, std::size_t(ch) * spb + g);
+                            }
+                        }
+            });
+        }
+
+        // relevant segments in (box, gamma) order
+        L.box_seg_begin.assign(nb + 1, 0);
+        for (std::size_t b = 0; b < nb; ++b) {
+            L.box_seg_begin[b] = std::int32_t(L.seg_box.size());
+            const std::uint8_t* mb = marks.data() + b * spb;
+            for (std::size_t g = 0; g < spb; ++g)
+                if (mb[g]) {
+                    L.seg_box.push_back(std::int32_t(b));
+                    L.seg_gamma.push_back(std::int32_t(g));
+                }
+        }
+        L.box_seg_begin[nb] = std::int32_t(L.seg_box.size());
+        marks.clear();
+        marks.shrink_to_fit();
+
+        // gamma -> ordinal of (box, gamma) among the relevant segments
+        auto ordinal = [&](std::int32_t box, int g) {
+            const auto b0 = L.seg_gamma.begin() + L.box_seg_begin[box];
+            const auto b1 = L.seg_gamma.begin() + L.box_seg_begin[box + 1];
+            const auto it = std::lower_bound(b0, b1, g);
+            if (it == b1 || *it != g) throw InternalError("cone plan: unmarked segment");
+            return std::int32_t(it - L.seg_gamma.begin());
+        };
+        parallel_for(std::int64_t(nb), w, [&](std::int64_t tb) {
+            const std::uint32_t n_t = B.end[tb] - B.begin[tb];
+            std::int64_t at = L.cev_begin[tb];
+            for (std::int32_t j = cz.ptr[tb]; j < cz.ptr[tb + 1]; ++j) {
+                const std::int32_t sb = cz.idx[j];
+                for (std::uint32_t q = 0; q < n_t; ++q, ++at) L.cev_seg[at] = ordinal(sb, L.cev_seg[at]);
+            }
+        });
+        if (d > 3) {
+            const ConeLevel& PL = plan.level[d - 2];
+            const auto& cptr = plan.child_ptr[d - 2];
+            const auto& cidx = plan.child_idx[d - 2];
+            const int P = PL.nodes_per_seg();
+            parallel_for(std::int64_t(PL.nseg()), w, [&](std::int64_t so) {
+                const std::int32_t pb = PL.seg_box[so];
+                const int nch = cptr[pb + 1] - cptr[pb];
+                std::int64_t at = L.pev_begin[so];
+                for (int node = 0; node < P; ++node)
+                    for (int c = 0; c < nch; ++c, ++at)
+                        L.pev_seg[at] = ordinal(cidx[cptr[pb] + c], L.pev_seg[at]);
+            });
+        }
+    }
+    return plan;
+}
+
+std::string plan_diagnostics(const BoxTree& t, const ConePlanHost& plan) {
+    std::ostringstream os;
+    os << "levels " << t.depth << "\n";
+    for (int d = 3; d <= t.depth; ++d) {
+        const ConeLevel& L = plan.level[d - 1];
+        os << "level " << d << ": boxes=" << t.level[d - 1].size() << " segments=" << L.nseg()
+           << " interp_points=" << L.nseg() * std::size_t(L.nodes_per_seg()) << " ns=" << L.ns
+           << " nc=" << L.nc << "\n";
+    }
+    return os.str();
+}
+
+}  // namespace ifgfb200

@@ -1,0 +1,68 @@
+// Cone-segment plan of the IFGF far field, precompiled into device work lists.
+//
+// The reference decides, during every apply, which cone segment each cousin target point
+// and each parent interpolation node falls into (ifgf.cpp:161-176 via cartesian_to_cone,
+// kernels.cpp:34-48). Those decisions hinge on the last ulp of glibc acos/atan2 (3,168
+// exact ties at cfg1), so they are taken ONCE here, on the host, with
+// the reference's own expressions, and shipped to HBM as per-evaluation segment ordinals.
+// The B200 kernels then only recompute the continuous local coordinates. The relevance
+// marking is the reference's plan_cones (ifgf.cpp:209-296); the cone geometry is
+// make_level_cones / doublings_for_side (ifgf.cpp:18-55).
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "boxtree.hpp"
+
+namespace ifgfb200 {
+
+struct ConeParams {
+    int n_c0 = 2, n_s0 = 1, ps = 3, pang = 5;  // ifgf.hpp:12-17 defaults
+};
+
+enum Factor : int { W1 = 1, W2 = 2, W3 = 3, W4 = 4 };
+enum class DlStrategy : int { W4 = 0, W2W3 = 1, Hybrid = 2 };
+
+struct ConeLevel {
+    int d = 0;
+    int ns = 0, nc = 0, ps = 0, pang = 0;
+    double ds = 0, dth = 0, dph = 0;
+    std::vector<double> s_nodes, th_nodes, ph_nodes;  // ns*ps, nc*pang, 2nc*pang
+
+    std::vector<std::int32_t> seg_box, seg_gamma;  // relevant segments, (box, gamma) order
+    std::vector<std::int32_t> box_seg_begin;       // nboxes + 1
+
+    // cousin evaluations, target-box major: for box tb, cousin j (ascending cousin list),
+    // point t of tb -> segment ordinal of the cousin box at this level
+    std::vector<std::int64_t> cev_begin;  // nboxes + 1
+    std::vector<std::int32_t> cev_seg;
+    // parent-node evaluations of level d-1 segments into this level's segments:
+    // parent segment so, node (is + ps*(it + pang*ip)), child slot c -> child segment ordinal
+    std::vector<std::int64_t> pev_begin;  // nseg(d-1) + 1 (empty at d = 3)
+    std::vector<std::int32_t> pev_seg;
+
+    int segs_per_box() const { return ns * nc * 2 * nc; }
+    int nodes_per_seg() const { return ps * pang * pang; }
+    std::size_t nseg() const { return seg_box.size(); }
+};
+
+struct ConePlanHost {
+    ConeParams params;
+    double k = 0;
+    std::vector<ConeLevel> level;  // level[d-1], valid for 3 <= d <= depth
+    // per leaf/coarse level: children lists compacted in slot order (nch <= 8)
+    std::vector<std::vector<std::int32_t>> child_ptr, child_idx;  // [d-1] over boxes of level d
+};
+
+int cone_doublings(double side, double lambda);  // ifgf.cpp:18-25
+std::vector<int> dl_pipes(const BoxTree& t, int level, DlStrategy s);  // ifgf.cpp:193-207
+
+ConePlanHost build_cone_plan(const BoxTree& t, const BoxRelations& rel,
+                             const std::vector<Vec3>& pts_morton, const ConeParams& p,
+                             int workers);
+
+// textual per-level counts, the reference's ConePlan::diagnostics (ifgf.cpp:298-310)
+std::string plan_diagnostics(const BoxTree& t, const ConePlanHost& plan);
+
+}  // namespace ifgfb200

@@ -1,0 +1,52 @@
+// Singular / near-singular (target, patch) pairs for the RP correction and the near-field
+// exclusion lists. Restates classify_targets (/root/reference/proj/src/rp.cpp:194-289) and
+// its golden-section closest_point (rp.cpp:22-43, 122-137) with identical decisions; the
+// pair set, (ubar, vbar) and the far-node correction lists feed the hot path.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "boxtree.hpp"
+#include "surface.hpp"
+
+namespace ifgfb200 {
+
+struct RpParams {
+    double delta_rel = 1.0;
+    double delta_abs = -1.0;
+    int n_beta = 96;
+    int cov_d = 6;
+};
+
+struct PairList {
+    RpParams cfg;
+    std::vector<double> delta;                   // per patch
+    std::vector<std::uint32_t> target;           // per pair (original node index)
+    std::vector<std::int32_t> patch;
+    std::vector<double> ubar, vbar;
+    std::vector<std::uint32_t> far_begin, far_end;
+    std::vector<std::uint32_t> target_pair_begin;  // N + 1
+    std::vector<std::uint32_t> far_nodes;          // original node indices
+    std::size_t size() const { return target.size(); }
+};
+
+struct ClosestPoint {
+    double u = 0, v = 0, dist = 0;
+};
+ClosestPoint closest_point_on(const Patch& p, const Vec3& x, double u0, double v0);
+
+PairList classify_pairs(const Surface& s, const BoxTree& t, const BoxRelations& rel,
+                        const RpParams& cfg, int workers);
+
+// graded change of variables (rp.cpp:139-192)
+double grade_w(double tau, int d);
+double grade_w_deriv(double tau, int d);
+double grade_xi(double alpha, double tau, int d);
+double grade_xi_deriv(double alpha, double tau, int d);
+
+// FNV-1a fingerprint of everything the beta tables depend on (rp.cpp:291-307), so beta
+// caches written here and by the reference are interchangeable.
+std::uint64_t beta_key(const Surface& s, const PairList& pl, double k);
+
+}  // namespace ifgfb200

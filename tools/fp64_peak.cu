@@ -1,0 +1,34 @@
+// DFMA-chain FP64 peak microbenchmark (roofline denominator for the FP64-bound kernels).
+#include <cstdio>
+#include <cuda_runtime.h>
+__global__ void dfma_chain(double* out, int iters, double a, double b) {
+    double x0 = threadIdx.x * 1e-9, x1 = x0 + 1e-3, x2 = x0 + 2e-3, x3 = x0 + 3e-3;
+    double x4 = x0 + 4e-3, x5 = x0 + 5e-3, x6 = x0 + 6e-3, x7 = x0 + 7e-3;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+            x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+        }
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+}
+int main() {
+    int dev = 0; cudaDeviceProp p; cudaGetDeviceProperties(&p, dev);
+    int sms = p.multiProcessorCount;
+    int blocks = sms * 8, threads = 256, iters = 4096;
+    double* out; cudaMalloc(&out, sizeof(double) * blocks * threads);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    dfma_chain<<<blocks, threads>>>(out, 16, 0.999999, 1e-7);
+    cudaDeviceSynchronize();
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(e0);
+        dfma_chain<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
+        cudaEventRecord(e1); cudaEventSynchronize(e1);
+        float ms; cudaEventElapsedTime(&ms, e0, e1); if (ms < best) best = ms;
+    }
+    double flops = 2.0 * 8 * 16 * double(iters) * blocks * threads;
+    printf("{\"gpu\": \"%s\", \"sms\": %d, \"fp64_dfma_tflops\": %.3f, \"ms\": %.3f}\n", p.name, sms, flops / best / 1e9, best);
+    return 0;
+}
