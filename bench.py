@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""CF-operator apply benchmark (BASELINE.json metric: applies/s and points/s).
+
+One step = one combined-field operator apply out = 1/2 phi + D[phi] - i gamma S[phi]
+(CombinedOperator::apply, solver.cpp:149-157) over the cfg2 sphere (16 wavelengths,
+N = 393,216; SURVEY.md Appendix A maps BASELINE's 6 x 256^2 layout to the reference-
+constructible 1,536 x 16^2 patches with the same N).
+
+  value : points/s with phi resident in HBM (CUDA-graph replays timed with CUDA events on
+          the engine stream), whole job (sum over ranks, max time over ranks)
+  e2e   : the same through the public API with host buffers — pinned phi copied in and the
+          result read back every step (CombinedOperator.apply)
+  roofline / rooflines : per-phase device time (CUDA events) against the algorithmic work
+  cpu_baseline : the reference's own CombinedOperator::apply (oracle/_ref, built from the
+          untouched /root/reference sources) on the host's cores, one full apply
+
+--impl reference runs the reference CPU implementation alone (rank 0), same metric/config.
+Multi-GPU (torchrun): each rank runs an independent replica of the apply (DESIGN.md §7:
+the Morton-partitioned NCCL path is not built yet), scaling "weak".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (splits, nodes per patch side, k, gamma, description)
+    "cfg1": (2, 16, 4 * np.pi, 4 * np.pi, "sphere r=1, 4 wavelengths, 96 patches x 16^2, k=4pi, gamma=k"),
+    "cfg2": (4, 16, 16 * np.pi, -1.0, "sphere r=1, 16 wavelengths, 1536 patches x 16^2, k=16pi"),
+    "cfg3": (6, 16, 64 * np.pi, -1.0, "sphere r=1, 64 wavelengths, 24576 patches x 16^2, k=64pi"),
+}
+
+
+def peaks():
+    p = {"hbm_gbs": 6551.4, "fp64_tflops": 34.2, "source_fp64": "tools/fp64_peak.cu DFMA chain on this pool's B200 (profiles/r01_box_probe.txt)"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p["hbm_gbs"] = float(m.get("hbm_gbs", p["hbm_gbs"]))
+        p["source_hbm"] = "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"
+    except Exception:
+        p["hbm_gbs"] = 6650.0
+        p["source_hbm"] = "fallback 6.65 TB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
+    return p
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 7:
+                    continue
+                try:
+                    sm.append(float(f[0]))
+                    mx = float(f[1])
+                except ValueError:
+                    continue
+                names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+                for nm, v in zip(names, f[3:7]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        except Exception:
+            pass
+        finally:
+            if self.path and os.path.exists(self.path):
+                os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def barrier_max(value, ws):
+    if ws == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def reference_apply_time(cfg_name, phi, beta_cache=None, applies=1, warmup=0):
+    """Times the reference's own CombinedOperator::apply; returns (seconds list, out, setup_s)."""
+    from oracle import ref as R
+
+    splits, nu, k, gamma, _ = CONFIGS[cfg_name]
+    rm = R.RefMesh.sphere(1.0, splits, nu, nu)
+    t0 = time.perf_counter()
+    ro = R.RefOperator(rm, k, gamma=gamma, beta_cache=beta_cache or "")
+    setup = time.perf_counter() - t0
+    for _ in range(warmup):
+        ro.apply(phi)
+    times = []
+    out = None
+    for _ in range(applies):
+        t0 = time.perf_counter()
+        out = ro.apply(phi)
+        times.append(time.perf_counter() - t0)
+    return times, out, setup, R.lib().ref_op_beta_cache_hit(ro.h) == 1
+
+
+def run_reference(args, ws, rank):
+    cfg_name = args.config
+    splits, nu, k, gamma, desc = CONFIGS[cfg_name]
+    if rank != 0:
+        return
+    n = 6 * 4 ** splits * nu * nu
+    from oracle import ref as R
+
+    if not R.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libifgf_ref.so not built"}))
+        return
+    phi = R.random_density(n, 1)
+    steps = max(1, min(args.steps, args.ref_steps))
+    warm = min(args.warmup, 1)
+    times, _, setup, _ = reference_apply_time(cfg_name, phi, applies=steps, warmup=warm)
+    total = sum(times)
+    value = n * steps / total
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": "cf_operator_points_per_s", "value": value, "unit": "points/s",
+        "applies_per_s": steps / total, "n_gpus": args.gpus, "steps": steps, "warmup": warm,
+        "steps_requested": args.steps, "ms_per_step": 1e3 * total / steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": f"{cfg_name}: {desc}", "N": n, "k": k, "parallelism": "cpu-openmp"},
+        "setup_s": setup,
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "reference",
+                         "sample": f"{steps} full CombinedOperator::apply at {cfg_name} after {warm} warm-up"
+                                   f" (reference built from /root/reference sources, OpenMP {cores} threads);"
+                                   f" steps capped at {args.ref_steps} to bound the run"},
+        "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def roofline_for(phases, work, pk):
+    """per-phase achieved rates; fp64 roof for leaf/near, HBM for cousin/parent/rp (north_star)"""
+    m = {
+        "leaf": ("leaf_flops", "leaf_bytes", "fp64"),
+        "cousin": ("cousin_flops", "cousin_bytes", "hbm"),
+        "parent": ("parent_flops", "parent_bytes", "hbm"),
+        "near": ("near_flops", "near_bytes", "fp64"),
+        "rp": ("rp_flops", "rp_bytes", "hbm"),
+    }
+    out = {}
+    for ph, (fk, bk, bound) in m.items():
+        ms = phases.get(ph, 0.0)
+        if ms <= 0:
+            continue
+        tf = work[fk] / (ms * 1e-3) / 1e12
+        gbs = work[bk] / (ms * 1e-3) / 1e9
+        out[ph] = {"ms": ms, "fp64_tflops": tf, "fp64_frac": tf / pk["fp64_tflops"], "hbm_gbs": gbs,
+                   "hbm_frac": gbs / pk["hbm_gbs"], "stated_bound": bound,
+                   "flops": work[fk], "bytes": work[bk]}
+    return out
+
+
+def run_b200(args, ws, rank, local):
+    import torch
+
+    import paper_2112_06316_b200 as P
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    splits, nu, k, gamma, desc = CONFIGS[args.config]
+    t0 = time.perf_counter()
+    mesh = P.SurfaceMesh.sphere(1.0, splits, nu, nu)
+    cfg = P.SolveConfig(k=k, gamma=gamma, device=local)
+    op = P.CombinedOperator(mesh, cfg)
+    setup_s = time.perf_counter() - t0
+    n = mesh.size()
+    phi = P.random_density(n, 1)
+
+    # --- device-resident throughput
+    op.upload_density(phi)
+    op.time_applies(max(args.warmup, 3), flush_l2=False)  # warm-up (eager run + graph capture)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as cs:
+        t_wall = time.perf_counter()
+        ms_per = op.time_applies(args.steps, flush_l2=False)
+        t_wall = time.perf_counter() - t_wall
+    torch.cuda.synchronize()
+    clocks = cs.summary()
+    ms_per = barrier_max(ms_per, ws)
+    value = ws * n / (ms_per * 1e-3)
+
+    # --- end to end through the public API with pinned host buffers
+    pin_in = torch.empty(2 * n, dtype=torch.float64, pin_memory=True)
+    pin_out = torch.empty(2 * n, dtype=torch.float64, pin_memory=True)
+    phi_h = pin_in.numpy().view(np.complex128)
+    phi_h[:] = phi
+    out_h = pin_out.numpy().view(np.complex128)
+    for _ in range(max(args.warmup, 3)):
+        op.apply_into(phi_h, out_h)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t_e2e = time.perf_counter()
+    for _ in range(args.steps):
+        op.apply_into(phi_h, out_h)
+    t_e2e = time.perf_counter() - t_e2e
+    t_e2e = barrier_max(t_e2e, ws)
+    e2e_value = ws * n * args.steps / t_e2e
+    out_gpu = out_h.copy()
+
+    # --- phases, work, roofline
+    phases = op.time_phases()
+    work = op.work()
+    pk = peaks()
+    roofs = roofline_for(phases, work, pk)
+    dom = max(roofs, key=lambda p: roofs[p]["ms"])
+    r = roofs[dom]
+    if r["stated_bound"] == "fp64":
+        roof = {"bound": "fp64", "kernel": dom, "achieved": r["fp64_tflops"], "peak": pk["fp64_tflops"],
+                "unit": "TFLOP/s", "frac": r["fp64_frac"], "traffic": None,
+                "peak_source": pk["source_fp64"]}
+    else:
+        roof = {"bound": "hbm", "kernel": dom, "achieved": r["hbm_gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": r["hbm_frac"], "traffic": None, "peak_source": pk["source_hbm"],
+                "fp64_frac": r["fp64_frac"]}
+
+    line = {
+        "metric": "cf_operator_points_per_s", "value": value, "unit": "points/s",
+        "applies_per_s": ws / (ms_per * 1e-3), "n_gpus": ws, "steps": args.steps, "warmup": max(args.warmup, 3),
+        "ms_per_step": ms_per, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c128", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {desc}", "N": n, "k": k, "gamma": op.gamma,
+                   "density": "U(-1,1)+iU(-1,1), mt19937_64 seed 1",
+                   "parallelism": "replicas" if ws > 1 else "single",
+                   "l2": "no flush: each apply streams the plan + beta tables (>> 126 MB L2)"},
+        "setup_s": setup_s, "wall_s_timed": t_wall, "clocks": clocks,
+        "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": 16 * n,
+                "d2h_bytes_per_step": 16 * n, "ms_per_step": 1e3 * t_e2e / args.steps},
+        "gpu_launches": args.steps * op.kernels_per_apply(), "kernels_per_apply": op.kernels_per_apply(),
+        "phases_ms": phases, "work": work, "roofline": roof, "rooflines": roofs,
+    }
+
+    # --- CPU baseline + parity at the bench config (rank 0, N=1)
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import ref as R
+
+            if R.available():
+                cache = os.path.join(tempfile.gettempdir(), f"ifgf_b200_beta_{args.config}.bin")
+                op.save_beta_cache(cache)
+                times, out_ref, ref_setup, hit = reference_apply_time(args.config, phi, beta_cache=cache,
+                                                                      applies=1)
+                os.unlink(cache)
+                cores = os.cpu_count()
+                line["cpu_baseline"] = {
+                    "value": n / times[0], "unit": "points/s", "cores": cores, "kind": "reference",
+                    "sample": f"one full CombinedOperator::apply at {args.config} (N={n}), reference built from "
+                              f"/root/reference sources, OpenMP {cores} threads; its setup ({ref_setup:.1f} s) "
+                              f"loaded the beta tables from an rpbeta v1 cache (hit={hit})",
+                    "seconds": times[0]}
+                rel = float(np.linalg.norm(out_gpu - out_ref) / np.linalg.norm(out_ref))
+                line["rel_l2_vs_reference"] = rel
+        except Exception as e:  # report, never hide
+            line["cpu_baseline"] = {"error": repr(e)}
+    if rank == 0:
+        print(json.dumps(line))
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", choices=list(CONFIGS), default="cfg2")
+    ap.add_argument("--ref-steps", type=int, default=3, help="cap on timed reference applies")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_b200(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()

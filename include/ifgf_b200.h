@@ -112,6 +112,13 @@ int ifgf_plan_pairs(const ifgf_plan* p, uint32_t* target, int32_t* patch, double
                     uint32_t* target_pair_begin, uint32_t* far_nodes);
 uint64_t ifgf_plan_beta_fingerprint(const ifgf_plan* p);
 int ifgf_plan_diagnostics(const ifgf_plan* p, char* buf, size_t cap);
+/* algorithmic work of one apply, 16 doubles:
+ * [0] leaf interactions  [1] cousin evaluations  [2] parent evaluations
+ * [3] near pairs (evaluated + corrections)  [4] RP pairs
+ * [5..9]  flops of leaf, cousin, parent, near, RP (SURVEY.md §8(d) counting)
+ * [10..14] algorithmic HBM bytes of leaf, cousin, parent, near, RP  [15] total flops */
+int ifgf_plan_work(const ifgf_plan* p, double* work16);
+int ifgf_operator_work(const ifgf_operator* op, double* work16);
 
 /* ---- device operator ---- */
 /* host setup + HBM upload + beta tables on the GPU */

@@ -74,6 +74,8 @@ _SIGS = {
     "ifgf_plan_pairs": (C.c_int, [vp, u32_p, i32_p, d_p, d_p, u32_p, u32_p, u32_p, u32_p]),
     "ifgf_plan_beta_fingerprint": (C.c_uint64, [vp]),
     "ifgf_plan_diagnostics": (C.c_int, [vp, C.c_char_p, C.c_size_t]),
+    "ifgf_plan_work": (C.c_int, [vp, d_p]),
+    "ifgf_operator_work": (C.c_int, [vp, d_p]),
     "ifgf_operator_create": (C.c_int, [vp, C.POINTER(IfgfConfig), C.POINTER(vp)]),
     "ifgf_operator_from_plan": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(vp)]),
     "ifgf_operator_free": (None, [vp]),

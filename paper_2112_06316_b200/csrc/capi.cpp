@@ -461,6 +461,100 @@ int ifgf_plan_diagnostics(const ifgf_plan* p, char* buf, size_t cap) {
     });
 }
 
+static void plan_work(const ifgf_plan& p, double* w) {
+    for (int i = 0; i < 16; ++i) w[i] = 0;
+    const BoxTree& T = p.tree;
+    const int D = T.depth;
+    const Surface& S = *p.surf;
+    auto npipes = [&](int d) {
+        int n = 1;  // W1
+        n += int(dl_pipes(T, d, p.strategy).size());
+        return n;
+    };
+    const double P = double(p.cfg.ps) * p.cfg.pang * p.cfg.pang;
+    constexpr double kTransform = 3900.0;  // block transform flops per block per pipe
+    if (D >= 3) {
+        const ConeLevel& L = p.cones.level[D - 1];
+        const BoxLevel& B = T.level[D - 1];
+        double inter = 0;
+        for (std::size_t so = 0; so < L.nseg(); ++so) {
+            const int b = L.seg_box[so];
+            inter += P * double(B.end[b] - B.begin[b]);
+        }
+        w[0] = inter;
+        w[5] = 47.0 * inter + kTransform * double(L.nseg()) * npipes(D);
+        w[10] = 64.0 * double(S.size()) + 16.0 * P * double(L.nseg()) * npipes(D);
+        for (int d = D; d >= 3; --d) {
+            const ConeLevel& C = p.cones.level[d - 1];
+            const double ev = double(C.cev_seg.size());
+            const int pc = npipes(d);
+            w[1] += ev;
+            w[6] += ev * (26.0 + pc * 434.0 + 6.0 + 8.0 * pc);
+            w[11] += 16.0 * P * double(C.nseg()) * pc + 4.0 * ev + 88.0 * double(S.size());
+            if (d > 3) {
+                const ConeLevel& PL = p.cones.level[d - 2];
+                const double pev = double(C.pev_seg.size());
+                const int pp = npipes(d - 1);
+                const bool conv = dl_pipes(T, d, p.strategy).size() == 2 && dl_pipes(T, d - 1, p.strategy).size() == 1;
+                w[2] += pev;
+                w[7] += pev * (26.0 + pc * 434.0 + 27.0 + 8.0 * pp + (conv ? 19.0 : 0.0)) +
+                        kTransform * double(PL.nseg()) * pp;
+                w[12] += 16.0 * P * (double(C.nseg()) * pc + double(PL.nseg()) * pp) + 4.0 * pev;
+            }
+        }
+    }
+    // near field: evaluated neighbour pairs + far-node corrections (solver.cpp:100-144)
+    const BoxLevel& leaves = T.level[D - 1];
+    const Adjacency& nb = p.rel.nbr[D - 1];
+    double pairs = 0;
+#pragma omp parallel for reduction(+ : pairs) schedule(dynamic, 256)
+    for (std::int64_t l = 0; l < std::int64_t(S.size()); ++l) {
+        const int tb = T.leaf_of[l];
+        const std::uint32_t p0 = p.pairs.target_pair_begin[l], p1 = p.pairs.target_pair_begin[l + 1];
+        double cnt = 0;
+        for (int j = nb.ptr[tb]; j < nb.ptr[tb + 1]; ++j) {
+            const int b = nb.idx[j];
+            for (std::uint32_t t = leaves.begin[b]; t < leaves.end[b]; ++t) {
+                const std::uint32_t m = T.perm[t];
+                if (m == std::uint32_t(l)) continue;
+                bool sing = false;
+                for (std::uint32_t q = p0; q < p1; ++q) sing |= (p.pairs.patch[q] == S.patch_of[m]);
+                if (!sing) cnt += 1;
+            }
+        }
+        for (std::uint32_t q = p0; q < p1; ++q) cnt += double(p.pairs.far_end[q] - p.pairs.far_begin[q]);
+        pairs += cnt;
+    }
+    w[3] = pairs;
+    w[8] = 47.0 * pairs;
+    w[13] = 64.0 * double(S.size()) + 64.0 * double(S.size()) + 4.0 * double(p.pairs.far_nodes.size());
+    double entries = 0;
+    for (std::size_t i = 0; i < p.pairs.size(); ++i) {
+        const Patch& q = S.patches[p.pairs.patch[i]];
+        entries += double(q.nu) * q.nv;
+    }
+    w[4] = double(p.pairs.size());
+    w[9] = 16.0 * entries;
+    w[14] = 32.0 * entries + 8.0 * double(p.pairs.size());
+    w[15] = w[5] + w[6] + w[7] + w[8] + w[9];
+}
+
+int ifgf_plan_work(const ifgf_plan* p, double* w) {
+    return guarded([&] {
+        need(p, "plan");
+        need(w, "work");
+        plan_work(*p, w);
+    });
+}
+
+int ifgf_operator_work(const ifgf_operator* op, double* w) {
+    return guarded([&] {
+        need(op, "operator");
+        need(w, "work");
+        plan_work(*op->plan, w);
+    });
+}
+
 // ------------------------------------------------------------------ operator
 int ifgf_operator_create(const ifgf_surface* s, const ifgf_config* cfg, ifgf_operator** out) {
     return guarded([&] {

@@ -105,8 +105,9 @@ struct Engine::Impl {
     bool beta_ready = false;
     // beta inputs
     DevBuf b_target, b_ubar, b_vbar, b_du, b_dv, b_orient, b_series_off, b_series, b_cutoff,
-        b_rule_x, b_rule_w;
-    int max_dudv = 1, max_nunv = 1;
+        b_gu, b_gwu, b_gv, b_gwv;
+    std::vector<double> rule_x, rule_w;
+    int max_dudv = 1, max_nunv = 1, max_dv = 1, max_nu = 1;
     // work vectors
     DevBuf d_phi, d_out, d_S, d_D, a_p, Sp, Dp, scratch, flush;
     PointsDev P;
@@ -430,6 +431,8 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
             mat_off[2 * q + 1] = mat_for(p.nv);
             max_nn = std::max(max_nn, p.nu * p.nv);
             e.max_dudv = std::max({e.max_dudv, p.du, p.dv, p.nu, p.nv});
+            e.max_dv = std::max(e.max_dv, p.dv);
+            e.max_nu = std::max(e.max_nu, p.nu);
             soff[q] = std::int64_t(series.size());
             for (const auto* set : {&p.pos_c, &p.du_c, &p.dv_c})
                 for (int c = 0; c < 3; ++c) series.insert(series.end(), (*set)[c].begin(), (*set)[c].end());
@@ -477,10 +480,7 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         e.b_series_off.upload(soff);
         e.b_series.upload(series);
         e.b_cutoff.upload(cutoff);
-        std::vector<double> rx, rw;
-        cheb::fejer(PL.cfg.n_beta, rx, rw);
-        e.b_rule_x.upload(rx);
-        e.b_rule_w.upload(rw);
+        cheb::fejer(PL.cfg.n_beta, e.rule_x, e.rule_w);
     }
 
     // ---- direct-sum view and work vectors
@@ -528,10 +528,30 @@ void Engine::compute_beta() {
     B.series_off = e.b_series_off.as<std::int64_t>();
     B.series = e.b_series.as<double>();
     B.cutoff = e.b_cutoff.as<double>();
-    B.rule_x = e.b_rule_x.as<double>();
-    B.rule_w = e.b_rule_w.as<double>();
-    launch_beta(B, e.beta_s.as<double2>(), e.beta_d.as<double2>(), e.max_dudv, e.max_nunv, e.st);
+    // graded rules on the host (glibc pow, bit-identical to the reference), in batches
+    const std::size_t np = e.pairs->size();
+    const int nb = B.n_beta;
+    const std::size_t batch = std::min<std::size_t>(np, std::size_t(1) << 17);
+    std::vector<double> hu(batch * nb), hwu(batch * nb), hv(batch * nb), hwv(batch * nb);
+    for (DevBuf* b : {&e.b_gu, &e.b_gwu, &e.b_gv, &e.b_gwv}) b->alloc(std::max<std::size_t>(batch * nb, 1) * sizeof(double));
+    B.grid_u = e.b_gu.as<double>();
+    B.grid_wu = e.b_gwu.as<double>();
+    B.grid_v = e.b_gv.as<double>();
+    B.grid_wv = e.b_gwv.as<double>();
+    for (std::size_t p0 = 0; p0 < np; p0 += batch) {
+        const std::size_t cnt = std::min(batch, np - p0);
+        graded_rules(*e.pairs, p0, p0 + cnt, e.rule_x, e.rule_w, hu.data(), hwu.data(), hv.data(), hwv.data(), 0);
+        IFGF_CUDA(cudaStreamSynchronize(e.st));  // previous batch done with the device buffers
+        const std::size_t bytes = cnt * nb * sizeof(double);
+        IFGF_CUDA(cudaMemcpyAsync(e.b_gu.as<void>(), hu.data(), bytes, cudaMemcpyHostToDevice, e.st));
+        IFGF_CUDA(cudaMemcpyAsync(e.b_gwu.as<void>(), hwu.data(), bytes, cudaMemcpyHostToDevice, e.st));
+        IFGF_CUDA(cudaMemcpyAsync(e.b_gv.as<void>(), hv.data(), bytes, cudaMemcpyHostToDevice, e.st));
+        IFGF_CUDA(cudaMemcpyAsync(e.b_gwv.as<void>(), hwv.data(), bytes, cudaMemcpyHostToDevice, e.st));
+        launch_beta_batch(B, int(p0), int(cnt), e.beta_s.as<double2>(), e.beta_d.as<double2>(), e.max_dudv,
+                          e.max_dv, e.max_nu, e.max_nunv, e.st);
+    }
     IFGF_CUDA(cudaStreamSynchronize(e.st));
+    for (DevBuf* b : {&e.b_gu, &e.b_gwu, &e.b_gv, &e.b_gwv}) b->alloc(0);
     e.beta_ready = true;
 }
 

@@ -95,9 +95,12 @@ struct BetaDev {
     const std::int64_t* series_off = nullptr;  // start of the 9 series of a patch
     const double* series = nullptr;
     const double* cutoff = nullptr;            // per patch: max(1e-14, 1e-8 spacing)
-    const double *rule_x = nullptr, *rule_w = nullptr;  // Fejér nodes/weights, n_beta
+    // graded nodes/weights of the current batch (host-computed, glibc pow): batch x n_beta
+    const double *grid_u = nullptr, *grid_wu = nullptr, *grid_v = nullptr, *grid_wv = nullptr;
 };
-void launch_beta(const BetaDev& B, double2* bs, double2* bd, int max_dudv, int max_nunv,
-                 cudaStream_t st);
+std::size_t beta_smem_bytes(int nb, int TT, int max_dv, int max_nu, int max_nunv);
+// pairs [p_base, p_base + count) of the batch whose graded rules are in B.grid_*
+void launch_beta_batch(const BetaDev& B, int p_base, int count, double2* bs, double2* bd, int TT,
+                       int max_dv, int max_nu, int max_nunv, cudaStream_t st);
 
 }  // namespace ifgfb200

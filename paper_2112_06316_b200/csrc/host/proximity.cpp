@@ -225,6 +225,24 @@ PairList classify_pairs(const Surface& s, const BoxTree& t, const BoxRelations& 
     return out;
 }
 
+void graded_rules(const PairList& pl, std::size_t p0, std::size_t p1, const std::vector<double>& rx,
+                  const std::vector<double>& rw, double* u, double* wu, double* v, double* wv,
+                  int workers) {
+    const int nb = int(rx.size());
+    const int d = pl.cfg.cov_d;
+    const int w = worker_count(workers);
+#pragma omp parallel for schedule(static) num_threads(w)
+    for (std::int64_t p = std::int64_t(p0); p < std::int64_t(p1); ++p) {
+        const std::size_t o = std::size_t(p - std::int64_t(p0)) * nb;
+        for (int i = 0; i < nb; ++i) {
+            u[o + i] = grade_xi(pl.ubar[p], rx[i], d);
+            wu[o + i] = grade_xi_deriv(pl.ubar[p], rx[i], d) * rw[i];
+            v[o + i] = grade_xi(pl.vbar[p], rx[i], d);
+            wv[o + i] = grade_xi_deriv(pl.vbar[p], rx[i], d) * rw[i];
+        }
+    }
+}
+
 std::uint64_t beta_key(const Surface& s, const PairList& pl, double k) {
     std::uint64_t h = 14695981039346656037ULL;
     h = fnv(&k, sizeof k, h);

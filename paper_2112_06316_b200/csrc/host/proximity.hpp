@@ -45,6 +45,12 @@ double grade_w_deriv(double tau, int d);
 double grade_xi(double alpha, double tau, int d);
 double grade_xi_deriv(double alpha, double tau, int d);
 
+// graded Fejér nodes/weights of pairs [p0, p1) (rp.cpp:345-351): out arrays are
+// (p1-p0) x n_beta, pair-major; computed with glibc pow exactly as the reference does
+void graded_rules(const PairList& pl, std::size_t p0, std::size_t p1, const std::vector<double>& rx,
+                  const std::vector<double>& rw, double* u, double* wu, double* v, double* wv,
+                  int workers);
+
 // FNV-1a fingerprint of everything the beta tables depend on (rp.cpp:291-307), so beta
 // caches written here and by the reference are interchangeable.
 std::uint64_t beta_key(const Surface& s, const PairList& pl, double k);

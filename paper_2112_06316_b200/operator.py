@@ -398,6 +398,21 @@ class CombinedOperator:
     def kernels_per_apply(self) -> int:
         return int(lib().ifgf_operator_kernels_per_apply(self._h))
 
+    def work(self) -> dict:
+        """Algorithmic work of one apply (counts, flops, HBM bytes per phase)."""
+        w = np.zeros(16)
+        check(lib().ifgf_operator_work(self._h, _ptr(w)), "work")
+        return _work_dict(w)
+
+
+WORK_KEYS = ["leaf_interactions", "cousin_evals", "parent_evals", "near_pairs", "rp_pairs",
+             "leaf_flops", "cousin_flops", "parent_flops", "near_flops", "rp_flops",
+             "leaf_bytes", "cousin_bytes", "parent_bytes", "near_bytes", "rp_bytes", "total_flops"]
+
+
+def _work_dict(w):
+    return dict(zip(WORK_KEYS, [float(x) for x in w]))
+
 
 @dataclass
 class GmresResult:  # solver.hpp:86-91
