@@ -17,6 +17,7 @@ struct LevelDev {
     int nseg = 0;    // relevant segments
     int ns = 0, nc = 0, ps = 0, pang = 0;
     double ds = 0, dth = 0, dph = 0;
+    double inv_ds = 0, inv_dth = 0, inv_dph = 0;
     double h = 0;    // half diagonal of this level's boxes
     const double *cx = nullptr, *cy = nullptr, *cz = nullptr;  // box centres
     const std::uint32_t *beg = nullptr, *end = nullptr;       // Morton spans

@@ -322,6 +322,9 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         L.ds = CL.ds;
         L.dth = CL.dth;
         L.dph = CL.dph;
+        L.inv_ds = 1.0 / CL.ds;
+        L.inv_dth = 1.0 / CL.dth;
+        L.inv_dph = 1.0 / CL.dph;
         L.h = T.half_diag(d);
         L.cx = b.cx.as<double>();
         L.cy = b.cy.as<double>();

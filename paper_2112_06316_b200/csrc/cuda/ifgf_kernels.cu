@@ -31,11 +31,12 @@ struct LocalCoords {
     double ls, lt, lp;
 };
 
-// Cone coordinates of v = x - centre relative to the (host-decided) segment gamma.
-__device__ __forceinline__ LocalCoords local_coords(double vx, double vy, double vz, double r,
+// Cone coordinates of v = x - centre (inv_r = 1/|v|) relative to the host-decided segment
+// gamma, mapped to [-1,1]^3 (LevelCones::local_coords, ifgf.cpp:178-183).
+__device__ __forceinline__ LocalCoords local_coords(double vx, double vy, double vz, double inv_r,
                                                     double h, int gamma, const LevelDev& L) {
-    const double s = h / r;
-    double ct = vz / r;
+    const double s = h * inv_r;
+    double ct = vz * inv_r;
     ct = fmin(1.0, fmax(-1.0, ct));
     const double th = acos(ct);
     double ph = atan2(vy, vx);
@@ -48,9 +49,9 @@ __device__ __forceinline__ LocalCoords local_coords(double vx, double vy, double
     if (g3 == 0 && ph > kPiD) ph -= kTwoPiD;
     if (g3 == 2 * L.nc - 1 && ph < kPiD) ph += kTwoPiD;
     LocalCoords o;
-    o.ls = 2.0 * (s - g1 * L.ds) / L.ds - 1.0;
-    o.lt = 2.0 * (th - g2 * L.dth) / L.dth - 1.0;
-    o.lp = 2.0 * (ph - g3 * L.dph) / L.dph - 1.0;
+    o.ls = fma(s, 2.0 * L.inv_ds, -(2 * g1 + 1.0));
+    o.lt = fma(th, 2.0 * L.inv_dth, -(2 * g2 + 1.0));
+    o.lp = fma(ph, 2.0 * L.inv_dph, -(2 * g3 + 1.0));
     return o;
 }
 
@@ -237,7 +238,7 @@ leaf_fill_kernel(LevelDev L, PointsDev P, const double2* __restrict__ a_p, doubl
                     const double nv2 = fma(vx, vx, fma(vy, vy, vz * vz));
                     const double inv = rsqrt(nv2);
                     const double nv = nv2 * inv;
-                    const double arg = khos * ((nv2 - 1.0) / (nv + 1.0));
+                    const double arg = khos * (nv2 - 1.0) * fast_rcp(nv + 1.0);
                     double sn, cs;
                     sincos(arg, &sn, &cs);
                     const double ar = sar[q], ai = sai[q];
@@ -299,12 +300,14 @@ cousin_kernel(LevelDev L, PointsDev P, const double2* __restrict__ store, double
         const int sb = L.cz_idx[j];
         const int so = L.cev_seg[ev0 + std::int64_t(j - j0) * n_t];
         const double vx = x - L.cx[sb], vy = y - L.cy[sb], vz = z - L.cz[sb];
-        const double r = sqrt(fma(vx, vx, fma(vy, vy, vz * vz)));
-        const LocalCoords lc = local_coords(vx, vy, vz, r, h, L.seg_gamma[so], L);
+        const double r2 = fma(vx, vx, fma(vy, vy, vz * vz));
+        const double inv_r = rsqrt(r2);
+        const double r = r2 * inv_r;
+        const LocalCoords lc = local_coords(vx, vy, vz, inv_r, h, L.seg_gamma[so], L);
         basis3<PS, PA>(lc, ts, tt, tp, ps, pa);
         double sn, cs;
         sincos(k * r, &sn, &cs);
-        const double f1 = kInv4PiD / r;
+        const double f1 = kInv4PiD * inv_r;
         const double2 e1 = make_double2(cs * f1, sn * f1);  // e^{ikr}/(4 pi r)
         const double2* blk = store + std::size_t(so) * NP * NPTS;
 #pragma unroll
@@ -316,7 +319,7 @@ cousin_kernel(LevelDev L, PointsDev P, const double2* __restrict__ store, double
                     accS = cadd(accS, w);
                     break;
                 case 2:
-                    cfma_r(accD, w, 1.0 / r);
+                    cfma_r(accD, w, inv_r);
                     break;
                 case 3:  // -ik e^{ikr}/(4 pi r) val
                     accD.x = fma(k, w.y, accD.x);
@@ -337,7 +340,7 @@ struct ChildMap {
 };
 
 template <int NPP, int NPC, int PS, int PA>
-__global__ void __launch_bounds__(kParentThreads)
+__global__ void __launch_bounds__(kParentThreads, 2)
 parent_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, double k, Pipes ppar,
               ChildMap cm, const double* __restrict__ Ms, const double* __restrict__ Ma,
               double2* __restrict__ pstore) {
@@ -384,15 +387,17 @@ parent_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, doub
             const int cso = Lc.pev_seg[ev + c];
             const double ccx = Lc.cx[ch], ccy = Lc.cy[ch], ccz = Lc.cz[ch];
             const double vx = x - ccx, vy = y - ccy, vz = z - ccz;
-            const double rc = sqrt(fma(vx, vx, fma(vy, vy, vz * vz)));
-            const LocalCoords lc = local_coords(vx, vy, vz, rc, hc, Lc.seg_gamma[cso], Lc);
+            const double rc2 = fma(vx, vx, fma(vy, vy, vz * vz));
+            const double inv_rc = rsqrt(rc2);
+            const double rc = rc2 * inv_rc;
+            const LocalCoords lc = local_coords(vx, vy, vz, inv_rc, hc, Lc.seg_gamma[cso], Lc);
             basis3<PS, PA>(lc, ts, tt, tp, cps, cpa);
             // stable r_c - r_p (ifgf.cpp:149-153)
             const double sx = ccx + pcx - 2.0 * x, sy = ccy + pcy - 2.0 * y, sz = ccz + pcz - 2.0 * z;
             const double dr = fma(sx, ccx - pcx, fma(sy, ccy - pcy, sz * (ccz - pcz))) / (rc + rp);
             double sn, cs;
             sincos(k * dr, &sn, &cs);
-            const double q1 = rp / rc;
+            const double q1 = rp * inv_rc;
             const double2 ratio1 = make_double2(cs * q1, sn * q1);
             const double2* blk = cstore + std::size_t(cso) * NPC * CPTS;
             double2 val[NPC];
@@ -408,7 +413,7 @@ parent_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, doub
                         if (cm.w4 >= 0) {
                             cfma(acc[i], ratio1, val[cm.w4]);
                         } else {  // child carries W2/W3: re-centre into W4
-                            const double q2 = rp / (rc * rc);
+                            const double q2 = q1 * inv_rc;
                             cfma(acc[i], make_double2(cs * q2, sn * q2), val[cm.w2]);
                             const double2 r3 = cmul(ratio1, val[cm.w3]);
                             acc[i].x = fma(k, r3.y, acc[i].x);
@@ -416,7 +421,7 @@ parent_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, doub
                         }
                         break;
                     case 2: {
-                        const double q3 = (rp * rp) / (rc * rc);
+                        const double q3 = q1 * q1;
                         cfma(acc[i], make_double2(cs * q3, sn * q3), val[cm.w2]);
                         break;
                     }

@@ -45,8 +45,9 @@ __device__ __forceinline__ void pair_kernels(double x, double y, double z, doubl
                                              double yz, double nx, double ny, double nz, double2 a,
                                              double k, double sg, double2& accS, double2& accD) {
     const double dx = x - yx, dy = y - yy, dz = z - yz;
-    const double r = sqrt(fma(dx, dx, fma(dy, dy, dz * dz)));
-    const double inv = 1.0 / r;
+    const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+    const double inv = rsqrt(r2);
+    const double r = r2 * inv;
     double sn, cs;
     sincos(k * r, &sn, &cs);
     const double g = kInv4PiD * inv;
