@@ -106,6 +106,8 @@ int64_t ifgf_plan_level(const ifgf_plan* p, int level, int32_t* params4, double*
 /* number of cousin / parent-node evaluations planned at a level */
 int64_t ifgf_plan_evaluations(const ifgf_plan* p, int level, int which);
 int64_t ifgf_plan_npairs(const ifgf_plan* p);
+/* {groups, evaluations, 8-row tensor-core tiles} of the parent-node evaluations into level */
+int ifgf_plan_tile_stats(const ifgf_plan* p, int level, int64_t* out3);
 int64_t ifgf_plan_nfar(const ifgf_plan* p);
 int ifgf_plan_pairs(const ifgf_plan* p, uint32_t* target, int32_t* patch, double* ubar,
                     double* vbar, uint32_t* far_begin, uint32_t* far_end,

@@ -427,6 +427,20 @@ int64_t ifgf_plan_evaluations(const ifgf_plan* p, int level, int which) {
     return int64_t(which == 0 ? L.cev_seg.size() : L.pev_seg.size());
 }
 
+// {groups, evaluations, 8-row tensor-core tiles} of the parent-node evaluations into level
+int ifgf_plan_tile_stats(const ifgf_plan* p, int level, int64_t* out3) {
+    return guarded([&] {
+        need(p, "plan");
+        if (level < 4 || level > p->tree.depth) throw InvalidArgument("tile stats: level out of range");
+        const ConeLevel& L = p->cones.level[level - 1];
+        int64_t tiles = 0;
+        for (std::size_t g = 0; g < L.pgrp_count.size(); ++g) tiles += (L.pgrp_count[g] + 7) / 8;
+        out3[0] = int64_t(L.pgrp_seg.size());
+        out3[1] = int64_t(L.pev_seg.size());
+        out3[2] = tiles;
+    });
+}
+
 int64_t ifgf_plan_npairs(const ifgf_plan* p) { return p ? int64_t(p->pairs.size()) : -1; }
 int64_t ifgf_plan_nfar(const ifgf_plan* p) { return p ? int64_t(p->pairs.far_nodes.size()) : -1; }
 

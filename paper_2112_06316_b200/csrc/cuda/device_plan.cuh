@@ -27,8 +27,13 @@ struct LevelDev {
     const std::int32_t *seg_box = nullptr, *seg_gamma = nullptr, *box_seg_begin = nullptr;
     const std::int64_t* pev_begin = nullptr;  // per parent (level d-1) segment
     const std::int32_t* pev_seg = nullptr;    // per parent-node evaluation into this level
+    const std::uint16_t* pev_perm = nullptr;  // evaluations grouped by child segment
+    const std::int32_t *pgrp_begin = nullptr, *pgrp_seg = nullptr;
+    const std::uint16_t *pgrp_start = nullptr, *pgrp_count = nullptr;
     const std::int32_t *ch_ptr = nullptr, *ch_idx = nullptr;  // children (level d+1) of this level's boxes
     const double *s_nodes = nullptr, *th_nodes = nullptr, *ph_nodes = nullptr;
+    // sin/cos of the angular node tables (interpolation-node directions)
+    const double *th_sin = nullptr, *th_cos = nullptr, *ph_sin = nullptr, *ph_cos = nullptr;
     const std::int32_t *chunk_box = nullptr, *chunk_q0 = nullptr;  // cousin work chunks
     int nchunk = 0;
     int max_pts = 0;  // largest box

@@ -60,7 +60,7 @@ class DevBuf {
 
 struct LevelBufs {
     DevBuf cx, cy, cz, beg, end, cz_ptr, cz_idx, cev_begin, cev_seg, seg_box, seg_gamma,
-        box_seg_begin, pev_begin, pev_seg, ch_ptr, ch_idx, s_nodes, th_nodes, ph_nodes,
+        box_seg_begin, pev_begin, pev_seg, pev_perm, pgrp_begin, pgrp_seg, pgrp_start, pgrp_count, ch_ptr, ch_idx, s_nodes, th_nodes, ph_nodes, th_sin, th_cos, ph_sin, ph_cos,
         chunk_box, chunk_q0;
 };
 
@@ -305,11 +305,25 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         b.box_seg_begin.upload(CL.box_seg_begin);
         b.pev_begin.upload(CL.pev_begin);
         b.pev_seg.upload(CL.pev_seg);
+        b.pev_perm.upload(CL.pev_perm);
+        b.pgrp_begin.upload(CL.pgrp_begin);
+        b.pgrp_seg.upload(CL.pgrp_seg);
+        b.pgrp_start.upload(CL.pgrp_start);
+        b.pgrp_count.upload(CL.pgrp_count);
         b.ch_ptr.upload(C.child_ptr[d - 1]);
         b.ch_idx.upload(C.child_idx[d - 1]);
         b.s_nodes.upload(CL.s_nodes);
         b.th_nodes.upload(CL.th_nodes);
         b.ph_nodes.upload(CL.ph_nodes);
+        {
+            std::vector<double> ts(CL.th_nodes.size()), tc(CL.th_nodes.size()), ps_(CL.ph_nodes.size()), pc_(CL.ph_nodes.size());
+            for (std::size_t i = 0; i < ts.size(); ++i) { ts[i] = std::sin(CL.th_nodes[i]); tc[i] = std::cos(CL.th_nodes[i]); }
+            for (std::size_t i = 0; i < ps_.size(); ++i) { ps_[i] = std::sin(CL.ph_nodes[i]); pc_[i] = std::cos(CL.ph_nodes[i]); }
+            b.th_sin.upload(ts);
+            b.th_cos.upload(tc);
+            b.ph_sin.upload(ps_);
+            b.ph_cos.upload(pc_);
+        }
         b.chunk_box.upload(chunk_box);
         b.chunk_q0.upload(chunk_q0);
         L.d = d;
@@ -340,11 +354,20 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         L.box_seg_begin = b.box_seg_begin.as<std::int32_t>();
         L.pev_begin = b.pev_begin.as<std::int64_t>();
         L.pev_seg = b.pev_seg.as<std::int32_t>();
+        L.pev_perm = b.pev_perm.as<std::uint16_t>();
+        L.pgrp_begin = b.pgrp_begin.as<std::int32_t>();
+        L.pgrp_seg = b.pgrp_seg.as<std::int32_t>();
+        L.pgrp_start = b.pgrp_start.as<std::uint16_t>();
+        L.pgrp_count = b.pgrp_count.as<std::uint16_t>();
         L.ch_ptr = b.ch_ptr.as<std::int32_t>();
         L.ch_idx = b.ch_idx.as<std::int32_t>();
         L.s_nodes = b.s_nodes.as<double>();
         L.th_nodes = b.th_nodes.as<double>();
         L.ph_nodes = b.ph_nodes.as<double>();
+        L.th_sin = b.th_sin.as<double>();
+        L.th_cos = b.th_cos.as<double>();
+        L.ph_sin = b.ph_sin.as<double>();
+        L.ph_cos = b.ph_cos.as<double>();
         L.chunk_box = b.chunk_box.as<std::int32_t>();
         L.chunk_q0 = b.chunk_q0.as<std::int32_t>();
         L.nchunk = int(chunk_box.size());

@@ -14,141 +14,20 @@
 #include <algorithm>
 
 #include "dev_common.cuh"
+#include "ifgf_device.cuh"
 #include "kernels.cuh"
 
 namespace ifgfb200 {
 namespace {
 
 using namespace dev;
-
-constexpr int kMaxOrd = 12;
+using namespace ifgfdev;
 constexpr int kLeafThreads = 384;
 constexpr int kLeafTile = 256;
 constexpr int kCousinThreads = 128;
+constexpr int kCousinSlots = 2;
+constexpr int kParentSlots = 2;
 constexpr int kParentThreads = 320;
-
-struct LocalCoords {
-    double ls, lt, lp;
-};
-
-// Cone coordinates of v = x - centre (inv_r = 1/|v|) relative to the host-decided segment
-// gamma, mapped to [-1,1]^3 (LevelCones::local_coords, ifgf.cpp:178-183).
-__device__ __forceinline__ LocalCoords local_coords(double vx, double vy, double vz, double inv_r,
-                                                    double h, int gamma, const LevelDev& L) {
-    const double s = h * inv_r;
-    double ct = vz * inv_r;
-    ct = fmin(1.0, fmax(-1.0, ct));
-    const double th = acos(ct);
-    double ph = atan2(vy, vx);
-    if (ph < 0.0) ph += kTwoPiD;
-    const int g1 = gamma % L.ns;
-    const int rest = gamma / L.ns;
-    const int g2 = rest % L.nc;
-    const int g3 = rest / L.nc;
-    // the host decision is authoritative; keep phi on the decided side of the 0/2pi seam
-    if (g3 == 0 && ph > kPiD) ph -= kTwoPiD;
-    if (g3 == 2 * L.nc - 1 && ph < kPiD) ph += kTwoPiD;
-    LocalCoords o;
-    o.ls = fma(s, 2.0 * L.inv_ds, -(2 * g1 + 1.0));
-    o.lt = fma(th, 2.0 * L.inv_dth, -(2 * g2 + 1.0));
-    o.lp = fma(ph, 2.0 * L.inv_dph, -(2 * g3 + 1.0));
-    return o;
-}
-
-// sum_{ip,it,is} c[is + ps*(it + pa*ip)] T_is(ls) T_it(lt) T_ip(lp)
-template <int PS, int PA>
-__device__ __forceinline__ double2 eval_series(const double2* __restrict__ c, const double* ts,
-                                               const double* tt, const double* tp, int ps, int pa) {
-    double2 acc = make_double2(0.0, 0.0);
-    if constexpr (PS > 0) {
-#pragma unroll
-        for (int ip = 0; ip < PA; ++ip) {
-            double2 a_t = make_double2(0.0, 0.0);
-#pragma unroll
-            for (int it = 0; it < PA; ++it) {
-                const double2* line = c + PS * (it + PA * ip);
-                double2 a_s = make_double2(0.0, 0.0);
-#pragma unroll
-                for (int is = 0; is < PS; ++is) cfma_r(a_s, ldg2(line + is), ts[is]);
-                cfma_r(a_t, a_s, tt[it]);
-            }
-            cfma_r(acc, a_t, tp[ip]);
-        }
-    } else {
-#pragma unroll 1
-        for (int ip = 0; ip < pa; ++ip) {
-            double2 a_t = make_double2(0.0, 0.0);
-#pragma unroll 1
-            for (int it = 0; it < pa; ++it) {
-                const double2* line = c + ps * (it + pa * ip);
-                double2 a_s = make_double2(0.0, 0.0);
-#pragma unroll 1
-                for (int is = 0; is < ps; ++is) cfma_r(a_s, ldg2(line + is), ts[is]);
-                cfma_r(a_t, a_s, tt[it]);
-            }
-            cfma_r(acc, a_t, tp[ip]);
-        }
-    }
-    return acc;
-}
-
-template <int PS, int PA>
-__device__ __forceinline__ void basis3(const LocalCoords& lc, double* ts, double* tt, double* tp,
-                                       int ps, int pa) {
-    if constexpr (PS > 0) {
-        cheb_row<PS>(lc.ls, ts);
-        cheb_row<PA>(lc.lt, tt);
-        cheb_row<PA>(lc.lp, tp);
-    } else {
-        ts[0] = tt[0] = tp[0] = 1.0;
-        if (ps > 1) ts[1] = lc.ls;
-        if (pa > 1) {
-            tt[1] = lc.lt;
-            tp[1] = lc.lp;
-        }
-        for (int i = 2; i < ps; ++i) ts[i] = 2.0 * lc.ls * ts[i - 1] - ts[i - 2];
-        for (int i = 2; i < pa; ++i) {
-            tt[i] = 2.0 * lc.lt * tt[i - 1] - tt[i - 2];
-            tp[i] = 2.0 * lc.lp * tp[i - 1] - tp[i - 2];
-        }
-    }
-}
-
-// In-place separable value->coefficient transform of `nblk` blocks of P = ps*pa*pa values
-// held in shared memory (v0), using v1 as scratch; the last pass writes to `dst`
-// (global), block b going to dst + b*P. Called by the whole CTA.
-__device__ void block_transform(double2* v0, double2* v1, int nblk, int ps, int pa,
-                                const double* __restrict__ Ms, const double* __restrict__ Ma,
-                                double2* __restrict__ dst) {
-    const int P = ps * pa * pa;
-    const int total = nblk * P;
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {  // along s
-        const int blk = e / P, node = e % P;
-        const int is = node % ps, line = node / ps;
-        const double2* src = v0 + blk * P + line * ps;
-        double2 acc = make_double2(0.0, 0.0);
-        for (int q = 0; q < ps; ++q) cfma_r(acc, src[q], Ms[is * ps + q]);
-        v1[e] = acc;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {  // along theta
-        const int blk = e / P, node = e % P;
-        const int is = node % ps, it = (node / ps) % pa, ip = node / (ps * pa);
-        const double2* src = v1 + blk * P + is + ps * pa * ip;
-        double2 acc = make_double2(0.0, 0.0);
-        for (int q = 0; q < pa; ++q) cfma_r(acc, src[ps * q], Ma[it * pa + q]);
-        v0[e] = acc;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {  // along phi
-        const int blk = e / P, node = e % P;
-        const int is = node % ps, it = (node / ps) % pa, ip = node / (ps * pa);
-        const double2* src = v0 + blk * P + is + ps * it;
-        double2 acc = make_double2(0.0, 0.0);
-        for (int q = 0; q < pa; ++q) cfma_r(acc, src[ps * pa * q], Ma[ip * pa + q]);
-        dst[e] = acc;
-    }
-}
 
 // ------------------------------------------------------------------ leaf fill
 template <int NP>
@@ -281,16 +160,20 @@ template <int NP, int PS, int PA>
 __global__ void __launch_bounds__(kCousinThreads)
 cousin_kernel(LevelDev L, PointsDev P, const double2* __restrict__ store, double k, Pipes pp,
               double2* __restrict__ Sp, double2* __restrict__ Dp) {
+    extern __shared__ double2 cz_smem[];
+    const int ps = L.ps, pa = L.pang;
+    const int NPTS = ps * pa * pa;
+    const int blk_elems = NP * NPTS;
+    double2* wbuf = cz_smem + (threadIdx.x >> 5) * kCousinSlots * blk_elems;
     const int c = blockIdx.x;
     const int tb = L.chunk_box[c];
     const int tbeg = int(L.beg[tb]);
     const int n_t = int(L.end[tb]) - tbeg;
     const int q = L.chunk_q0[c] + threadIdx.x;
-    if (q >= n_t) return;
-    const int t = tbeg + q;
+    const bool act = q < n_t;
+    if (__all_sync(0xffffffffu, !act)) return;  // whole warp idle (no CTA-wide barriers here)
+    const int t = act ? tbeg + q : tbeg;
     const double x = P.x[t], y = P.y[t], z = P.z[t];
-    const int ps = L.ps, pa = L.pang;
-    const int NPTS = ps * pa * pa;
     const double h = L.h;
     const int j0 = L.cz_ptr[tb], j1 = L.cz_ptr[tb + 1];
     const std::int64_t ev0 = L.cev_begin[tb] + q;
@@ -298,38 +181,43 @@ cousin_kernel(LevelDev L, PointsDev P, const double2* __restrict__ store, double
     double ts[PS > 0 ? PS : kMaxOrd], tt[PA > 0 ? PA : kMaxOrd], tp[PA > 0 ? PA : kMaxOrd];
     for (int j = j0; j < j1; ++j) {
         const int sb = L.cz_idx[j];
-        const int so = L.cev_seg[ev0 + std::int64_t(j - j0) * n_t];
+        const int so = act ? L.cev_seg[ev0 + std::int64_t(j - j0) * n_t] : -1;
         const double vx = x - L.cx[sb], vy = y - L.cy[sb], vz = z - L.cz[sb];
         const double r2 = fma(vx, vx, fma(vy, vy, vz * vz));
         const double inv_r = rsqrt(r2);
         const double r = r2 * inv_r;
-        const LocalCoords lc = local_coords(vx, vy, vz, inv_r, h, L.seg_gamma[so], L);
-        basis3<PS, PA>(lc, ts, tt, tp, ps, pa);
-        double sn, cs;
-        sincos(k * r, &sn, &cs);
-        const double f1 = kInv4PiD * inv_r;
-        const double2 e1 = make_double2(cs * f1, sn * f1);  // e^{ikr}/(4 pi r)
-        const double2* blk = store + std::size_t(so) * NP * NPTS;
-#pragma unroll
-        for (int i = 0; i < NP; ++i) {
-            const double2 val = eval_series<PS, PA>(blk + i * NPTS, ts, tt, tp, ps, pa);
-            const double2 w = cmul(e1, val);
-            switch (pp.f[i]) {
-                case 1:
-                    accS = cadd(accS, w);
-                    break;
-                case 2:
-                    cfma_r(accD, w, inv_r);
-                    break;
-                case 3:  // -ik e^{ikr}/(4 pi r) val
-                    accD.x = fma(k, w.y, accD.x);
-                    accD.y = fma(-k, w.x, accD.y);
-                    break;
-                default:
-                    accD = cadd(accD, w);
-            }
+        double2 e1 = make_double2(0.0, 0.0);
+        if (act) {
+            const LocalCoords lc = local_coords(vx, vy, vz, inv_r, h, L.seg_gamma[so], L);
+            basis3<PS, PA>(lc, ts, tt, tp, ps, pa);
+            double sn, cs;
+            sincos(k * r, &sn, &cs);
+            const double f1 = kInv4PiD * inv_r;
+            e1 = make_double2(cs * f1, sn * f1);  // e^{ikr}/(4 pi r)
         }
+        with_staged_block<kCousinSlots>(so, store, blk_elems, wbuf, [&](const double2* blk) {
+#pragma unroll
+            for (int i = 0; i < NP; ++i) {
+                const double2 val = eval_series_sm<PS, PA>(blk + i * NPTS, ts, tt, tp, ps, pa);
+                const double2 w = cmul(e1, val);
+                switch (pp.f[i]) {
+                    case 1:
+                        accS = cadd(accS, w);
+                        break;
+                    case 2:
+                        cfma_r(accD, w, inv_r);
+                        break;
+                    case 3:  // -ik e^{ikr}/(4 pi r) val
+                        accD.x = fma(k, w.y, accD.x);
+                        accD.y = fma(-k, w.x, accD.y);
+                        break;
+                    default:
+                        accD = cadd(accD, w);
+                }
+            }
+        });
     }
+    if (!act) return;
     Sp[t] = cadd(Sp[t], accS);
     Dp[t] = cadd(Dp[t], accD);
 }
@@ -349,6 +237,7 @@ parent_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, doub
     const int NPTS = ps * pa * pa;
     const int cps = Lc.ps, cpa = Lc.pang;
     const int CPTS = cps * cpa * cpa;
+    const int cblk = NPC * CPTS;
     const int G = max(1, int(blockDim.x) / NPTS);
     const int g0 = blockIdx.x * G;
     if (g0 >= Lp.nseg) return;
@@ -356,13 +245,14 @@ parent_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, doub
     const int items = gcount * NPTS;
     double2* v0 = reinterpret_cast<double2*>(smem);
     double2* v1 = v0 + G * NPP * NPTS;
+    double2* wbuf = v1 + G * NPP * NPTS + (threadIdx.x >> 5) * kParentSlots * cblk;
     const double hp = Lp.h, hc = Lc.h;
     double ts[PS > 0 ? PS : kMaxOrd], tt[PA > 0 ? PA : kMaxOrd], tp[PA > 0 ? PA : kMaxOrd];
 
     for (int base = 0; base < items; base += blockDim.x) {
         const int item = base + threadIdx.x;
-        if (item >= items) continue;
-        const int seg_l = item / NPTS, node = item % NPTS;
+        const bool act = item < items;
+        const int seg_l = act ? item / NPTS : 0, node = act ? item % NPTS : 0;
         const int so = g0 + seg_l;
         const int pb = Lp.seg_box[so];
         const int gam = Lp.seg_gamma[so];
@@ -377,61 +267,69 @@ parent_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, doub
         const double x = pcx + rp * sth * cph;
         const double y = pcy + rp * sth * sph;
         const double z = pcz + rp * cth;
-        const int c0 = Lp.ch_ptr[pb], nch = Lp.ch_ptr[pb + 1] - c0;
+        const int c0 = Lp.ch_ptr[pb];
+        const int nch = act ? Lp.ch_ptr[pb + 1] - c0 : 0;
+        const int nch_warp = __reduce_max_sync(0xffffffffu, unsigned(nch));
         const std::int64_t ev = Lc.pev_begin[so] + std::int64_t(node) * nch;
         double2 acc[NPP];
 #pragma unroll
         for (int i = 0; i < NPP; ++i) acc[i] = make_double2(0.0, 0.0);
-        for (int c = 0; c < nch; ++c) {
-            const int ch = Lp.ch_idx[c0 + c];
-            const int cso = Lc.pev_seg[ev + c];
+        for (int c = 0; c < nch_warp; ++c) {
+            const bool live = c < nch;
+            const int ch = live ? Lp.ch_idx[c0 + c] : 0;
+            const int cso = live ? Lc.pev_seg[ev + c] : -1;
             const double ccx = Lc.cx[ch], ccy = Lc.cy[ch], ccz = Lc.cz[ch];
             const double vx = x - ccx, vy = y - ccy, vz = z - ccz;
             const double rc2 = fma(vx, vx, fma(vy, vy, vz * vz));
             const double inv_rc = rsqrt(rc2);
             const double rc = rc2 * inv_rc;
-            const LocalCoords lc = local_coords(vx, vy, vz, inv_rc, hc, Lc.seg_gamma[cso], Lc);
-            basis3<PS, PA>(lc, ts, tt, tp, cps, cpa);
-            // stable r_c - r_p (ifgf.cpp:149-153)
-            const double sx = ccx + pcx - 2.0 * x, sy = ccy + pcy - 2.0 * y, sz = ccz + pcz - 2.0 * z;
-            const double dr = fma(sx, ccx - pcx, fma(sy, ccy - pcy, sz * (ccz - pcz))) / (rc + rp);
-            double sn, cs;
-            sincos(k * dr, &sn, &cs);
-            const double q1 = rp * inv_rc;
-            const double2 ratio1 = make_double2(cs * q1, sn * q1);
-            const double2* blk = cstore + std::size_t(cso) * NPC * CPTS;
-            double2 val[NPC];
-#pragma unroll
-            for (int i = 0; i < NPC; ++i) val[i] = eval_series<PS, PA>(blk + i * CPTS, ts, tt, tp, cps, cpa);
-#pragma unroll
-            for (int i = 0; i < NPP; ++i) {
-                switch (ppar.f[i]) {
-                    case 1:
-                        cfma(acc[i], ratio1, val[cm.w1]);
-                        break;
-                    case 4:
-                        if (cm.w4 >= 0) {
-                            cfma(acc[i], ratio1, val[cm.w4]);
-                        } else {  // child carries W2/W3: re-centre into W4
-                            const double q2 = q1 * inv_rc;
-                            cfma(acc[i], make_double2(cs * q2, sn * q2), val[cm.w2]);
-                            const double2 r3 = cmul(ratio1, val[cm.w3]);
-                            acc[i].x = fma(k, r3.y, acc[i].x);
-                            acc[i].y = fma(-k, r3.x, acc[i].y);
-                        }
-                        break;
-                    case 2: {
-                        const double q3 = q1 * q1;
-                        cfma(acc[i], make_double2(cs * q3, sn * q3), val[cm.w2]);
-                        break;
-                    }
-                    default:  // W3
-                        cfma(acc[i], ratio1, val[cm.w3]);
-                }
+            double sn = 0.0, cs = 0.0, q1 = 0.0;
+            if (live) {
+                const LocalCoords lc = local_coords(vx, vy, vz, inv_rc, hc, Lc.seg_gamma[cso], Lc);
+                basis3<PS, PA>(lc, ts, tt, tp, cps, cpa);
+                // stable r_c - r_p (ifgf.cpp:149-153)
+                const double sx = ccx + pcx - 2.0 * x, sy = ccy + pcy - 2.0 * y, sz = ccz + pcz - 2.0 * z;
+                const double dr = fma(sx, ccx - pcx, fma(sy, ccy - pcy, sz * (ccz - pcz))) / (rc + rp);
+                sincos(k * dr, &sn, &cs);
+                q1 = rp * inv_rc;
             }
-        }
+            const double2 ratio1 = make_double2(cs * q1, sn * q1);
+            with_staged_block<kParentSlots>(cso, cstore, cblk, wbuf, [&](const double2* blk) {
+                double2 val[NPC];
 #pragma unroll
-        for (int i = 0; i < NPP; ++i) v0[(seg_l * NPP + i) * NPTS + node] = acc[i];
+                for (int i = 0; i < NPC; ++i) val[i] = eval_series_sm<PS, PA>(blk + i * CPTS, ts, tt, tp, cps, cpa);
+#pragma unroll
+                for (int i = 0; i < NPP; ++i) {
+                    switch (ppar.f[i]) {
+                        case 1:
+                            cfma(acc[i], ratio1, val[cm.w1]);
+                            break;
+                        case 4:
+                            if (cm.w4 >= 0) {
+                                cfma(acc[i], ratio1, val[cm.w4]);
+                            } else {  // child carries W2/W3: re-centre into W4
+                                const double q2 = q1 * inv_rc;
+                                cfma(acc[i], make_double2(cs * q2, sn * q2), val[cm.w2]);
+                                const double2 r3 = cmul(ratio1, val[cm.w3]);
+                                acc[i].x = fma(k, r3.y, acc[i].x);
+                                acc[i].y = fma(-k, r3.x, acc[i].y);
+                            }
+                            break;
+                        case 2: {
+                            const double q3 = q1 * q1;
+                            cfma(acc[i], make_double2(cs * q3, sn * q3), val[cm.w2]);
+                            break;
+                        }
+                        default:  // W3
+                            cfma(acc[i], ratio1, val[cm.w3]);
+                    }
+                }
+            });
+        }
+        if (act) {
+#pragma unroll
+            for (int i = 0; i < NPP; ++i) v0[(seg_l * NPP + i) * NPTS + node] = acc[i];
+        }
     }
     __syncthreads();
     block_transform(v0, v1, gcount * NPP, ps, pa, Ms, Ma, pstore + std::size_t(g0) * NPP * NPTS);
@@ -464,7 +362,12 @@ void launch_cousin_eval(const LevelDev& L, const PointsDev& P, const double2* st
                         const Pipes& pipes, double2* Sp, double2* Dp, cudaStream_t st) {
     if (L.nchunk == 0) return;
     const bool def = L.ps == 3 && L.pang == 5;
-    auto go = [&](auto kern) { kern<<<L.nchunk, kCousinThreads, 0, st>>>(L, P, store, k, pipes, Sp, Dp); };
+    const std::size_t smem = std::size_t(kCousinThreads / 32) * kCousinSlots * pipes.n * L.ps * L.pang * L.pang *
+                             sizeof(double2);
+    auto go = [&](auto kern) {
+        IFGF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        kern<<<L.nchunk, kCousinThreads, smem, st>>>(L, P, store, k, pipes, Sp, Dp);
+    };
     if (def) {
         switch (pipes.n) {
             case 1: go(cousin_kernel<1, 3, 5>); break;
@@ -502,13 +405,17 @@ void launch_parent_fill(const LevelDev& Lp, const LevelDev& Lc, const double2* c
     }
     const int NPTS = Lp.ps * Lp.pang * Lp.pang;
     const int G = std::max(1, kParentThreads / NPTS);
-    const std::size_t smem = 2 * std::size_t(G) * parent_pipes.n * NPTS * sizeof(double2);
+    const int CPTS = Lc.ps * Lc.pang * Lc.pang;
+    const std::size_t smem = (2 * std::size_t(G) * parent_pipes.n * NPTS +
+                              std::size_t(kParentThreads / 32) * kParentSlots * child_pipes.n * CPTS) *
+                             sizeof(double2);
     const int grid = div_up(Lp.nseg, G);
     const bool def = Lp.ps == 3 && Lp.pang == 5 && Lc.ps == 3 && Lc.pang == 5;
     auto go = [&](auto kern) {
         IFGF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         kern<<<grid, kParentThreads, smem, st>>>(Lp, Lc, child_store, k, parent_pipes, cm, Ms, Ma, parent_store);
     };
+    if (launch_parent_fill_tc(Lp, Lc, child_store, k, parent_pipes, child_pipes, Ms, Ma, parent_store, st)) return;
     const int code = parent_pipes.n * 4 + child_pipes.n;
 #define IFGF_PARENT_CASE(NPP, NPC)                                     \
     case NPP * 4 + NPC:                                                \

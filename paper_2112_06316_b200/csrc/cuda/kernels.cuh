@@ -25,6 +25,11 @@ void launch_parent_fill(const LevelDev& Lp, const LevelDev& Lc, const double2* c
                         double k, const Pipes& parent_pipes, const Pipes& child_pipes,
                         const double* Ms, const double* Ma, double2* parent_store, cudaStream_t st);
 
+// FP64 tensor-core parent fill (parent_tc.cu) for ps = 3, pang = 5; false if not applicable
+bool launch_parent_fill_tc(const LevelDev& Lp, const LevelDev& Lc, const double2* child_store, double k,
+                           const Pipes& parent_pipes, const Pipes& child_pipes, const double* Ms,
+                           const double* Ma, double2* parent_store, cudaStream_t st);
+
 // ---- near field, RP, combine, direct (near_rp_kernels.cu) ----
 struct NearDev {
     int n = 0;       // points

@@ -1,0 +1,286 @@
+// Parent fill (ifgf.cpp:452-568) on the FP64 tensor cores, for the default interpolation
+// orders (ps = 3, pang = 5).
+//
+// One CTA (4 warps) per parent segment. Each warp takes the host's child-segment groups
+// of that segment in turn (all parent-node evaluations that land in one child cone
+// segment, ifgf/coneplan.cpp group_parent_evaluations):
+//   1. the warp's lanes compute, for the group's evaluations, the child-frame local
+//      coordinates and the re-centring factors (node directions from sin/cos tables);
+//   2. tiles of 8 evaluations contract the child's 3x5x5 coefficient block against the
+//      evaluations' basis products with mma.sync.m8n8k4.f64 (DMMA): A = basis products
+//      (rows = evaluations, k = the s index padded 3 -> 4), B = coefficients (columns =
+//      pipe x {re, im}), 25 k-steps over the (theta, phi) indices — every coefficient is
+//      fetched once per warp instead of once per lane;
+//   3. the epilogue applies the re-centring factor and adds into the warp's private
+//      node accumulators (no atomics).
+// A fixed-order sum over the 4 warps and the separable block transform finish the segment.
+// Results equal the per-lane kernel to rounding (~1e-16); the evaluation order is fixed,
+// so the output is bitwise reproducible.
+#include "ifgf_device.cuh"
+#include "kernels.cuh"
+
+namespace ifgfb200 {
+namespace {
+
+using namespace dev;
+using namespace ifgfdev;
+
+constexpr int kWarps = 4;
+constexpr int kGeo = 7;  // ls, lt, lp, ratio.re, ratio.im, extra factor, node (odd stride)
+constexpr int kPS = 3, kPA = 5, kNP = 75;
+constexpr int kGeoSz = kNP * kGeo + 1;  // keeps the accumulators 16-byte aligned
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// Child->parent pipe combinations of the strategies (ifgf.cpp:525-555). Each child pipe
+// feeds one parent pipe with one factor: R1 = ratio1, RI = ratio1/r_c (W2 -> W4),
+// MK = -ik ratio1 (W3 -> W4), RQ = ratio1 r_p/r_c (W2 -> W2).
+enum Fac { R1 = 0, RI = 1, MK = 2, RQ = 3 };
+template <int C>
+struct Combo;
+template <>
+struct Combo<0> {  // (W1,W4) <- (W1,W2,W3): Hybrid, sub-half-wavelength child
+    static constexpr int npp = 2, npc = 3, extra = RI;
+    __device__ static constexpr int dst(int i) { return i == 0 ? 0 : 1; }
+    __device__ static constexpr int fac(int i) { return i == 0 ? R1 : (i == 1 ? RI : MK); }
+};
+template <>
+struct Combo<1> {  // (W1,W4) <- (W1,W4)
+    static constexpr int npp = 2, npc = 2, extra = R1;
+    __device__ static constexpr int dst(int i) { return i; }
+    __device__ static constexpr int fac(int) { return R1; }
+};
+template <>
+struct Combo<2> {  // (W1) <- (W1), or (W4) <- (W4)
+    static constexpr int npp = 1, npc = 1, extra = R1;
+    __device__ static constexpr int dst(int) { return 0; }
+    __device__ static constexpr int fac(int) { return R1; }
+};
+template <>
+struct Combo<3> {  // (W4) <- (W2,W3)
+    static constexpr int npp = 1, npc = 2, extra = RI;
+    __device__ static constexpr int dst(int) { return 0; }
+    __device__ static constexpr int fac(int i) { return i == 0 ? RI : MK; }
+};
+template <>
+struct Combo<4> {  // (W1,W2,W3) <- (W1,W2,W3)
+    static constexpr int npp = 3, npc = 3, extra = RQ;
+    __device__ static constexpr int dst(int i) { return i; }
+    __device__ static constexpr int fac(int i) { return i == 1 ? RQ : R1; }
+};
+template <>
+struct Combo<5> {  // (W2,W3) <- (W2,W3)
+    static constexpr int npp = 2, npc = 2, extra = RQ;
+    __device__ static constexpr int dst(int i) { return i; }
+    __device__ static constexpr int fac(int i) { return i == 0 ? RQ : R1; }
+};
+
+template <int COMBO>
+__global__ void __launch_bounds__(32 * kWarps, 6)
+parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, double k,
+                 const double* __restrict__ Ms, const double* __restrict__ Ma,
+                 double2* __restrict__ pstore) {
+    using CB = Combo<COMBO>;
+    constexpr int NPP = CB::npp, NPC = CB::npc;
+    extern __shared__ double smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int so = blockIdx.x * kWarps + warp;  // one warp per parent segment
+    if (so >= Lp.nseg) return;
+    double* geo = smem + warp * (kGeoSz + 2 * kNP * NPP);                       // per warp
+    double2* acc = reinterpret_cast<double2*>(geo + kGeoSz);                   // 75 x NPP
+    for (int e = lane; e < kNP * NPP; e += 32) acc[e] = make_double2(0.0, 0.0);
+
+    const int pb = Lp.seg_box[so];
+    const int gam = Lp.seg_gamma[so];
+    const int g1 = gam % Lp.ns, g2 = (gam / Lp.ns) % Lp.nc, g3 = gam / Lp.ns / Lp.nc;
+    const int c0 = Lp.ch_ptr[pb], nch = Lp.ch_ptr[pb + 1] - c0;
+    const std::int64_t ev0 = Lc.pev_begin[so];
+    const double hp = Lp.h, hc = Lc.h;
+    const double pcx = Lp.cx[pb], pcy = Lp.cy[pb], pcz = Lp.cz[pb];
+
+    const int r = lane >> 2, tig = lane & 3;
+    const int comp = lane >> 2;  // B column: pipe comp >> 1, re/im comp & 1
+    const bool bcol = comp < 2 * NPC && tig < kPS;
+    const int boff = 2 * ((comp >> 1) * kNP + tig) + (comp & 1);
+    const int gb = Lc.pgrp_begin[so], ge = Lc.pgrp_begin[so + 1];
+    for (int g = gb; g < ge; ++g) {
+        const int cso = Lc.pgrp_seg[g];
+        const int start = Lc.pgrp_start[g], count = Lc.pgrp_count[g];
+        // 1. geometry of the group's evaluations
+        for (int i = lane; i < count; i += 32) {
+            const int e = Lc.pev_perm[ev0 + start + i];
+            const int node = e / nch, c = e - node * nch;
+            const int is = node % kPS, it = (node / kPS) % kPA, ip = node / (kPS * kPA);
+            const double s = Lp.s_nodes[g1 * kPS + is];
+            const double rp = hp / s;
+            const double sth = Lp.th_sin[g2 * kPA + it], cth = Lp.th_cos[g2 * kPA + it];
+            const double sph = Lp.ph_sin[g3 * kPA + ip], cph = Lp.ph_cos[g3 * kPA + ip];
+            const double x = pcx + rp * sth * cph, y = pcy + rp * sth * sph, z = pcz + rp * cth;
+            const int ch = Lp.ch_idx[c0 + c];
+            const double ccx = Lc.cx[ch], ccy = Lc.cy[ch], ccz = Lc.cz[ch];
+            const double vx = x - ccx, vy = y - ccy, vz = z - ccz;
+            const double rc2 = fma(vx, vx, fma(vy, vy, vz * vz));
+            const double inv_rc = rsqrt(rc2);
+            const double rc = rc2 * inv_rc;
+            const LocalCoords lc = local_coords(vx, vy, vz, inv_rc, hc, Lc.seg_gamma[cso], Lc);
+            // stable r_c - r_p (ifgf.cpp:149-153)
+            const double sx = ccx + pcx - 2.0 * x, sy = ccy + pcy - 2.0 * y, sz = ccz + pcz - 2.0 * z;
+            const double dr = fma(sx, ccx - pcx, fma(sy, ccy - pcy, sz * (ccz - pcz))) * fast_rcp(rc + rp);
+            double sn, cs;
+            sincos_bounded(k * dr, &sn, &cs);
+            const double q1 = rp * inv_rc;
+            double* gp = geo + i * kGeo;
+            gp[0] = lc.ls;
+            gp[1] = lc.lt;
+            gp[2] = lc.lp;
+            gp[3] = cs * q1;
+            gp[4] = sn * q1;
+            gp[5] = CB::extra == RI ? inv_rc : q1;
+            gp[6] = double(node);
+        }
+        __syncwarp();
+        // 2. 8-evaluation tensor-core tiles against the child block
+        const double* blk = reinterpret_cast<const double*>(cstore + std::size_t(cso) * NPC * kNP) + boff;
+        for (int t0 = 0; t0 < count; t0 += 8) {
+            const bool valid = t0 + r < count;
+            const double* gp = geo + (valid ? t0 + r : 0) * kGeo;
+            const double ls = gp[0];
+            double ts = tig == 0 ? 1.0 : (tig == 1 ? ls : (tig == 2 ? 2.0 * ls * ls - 1.0 : 0.0));
+            if (!valid) ts = 0.0;
+            double tt[kPA], tq[kPA];
+            cheb_row<kPA>(gp[1], tt);
+            cheb_row<kPA>(gp[2], tq);
+            double d0 = 0.0, d1 = 0.0, f0 = 0.0, f1 = 0.0;
+#pragma unroll
+            for (int ip = 0; ip < kPA; ++ip) {
+                const double tsp = ts * tq[ip];
+#pragma unroll
+                for (int it = 0; it < kPA; ++it) {
+                    const int kc = it + kPA * ip;
+                    const double bv = bcol ? __ldg(blk + 2 * kPS * kc) : 0.0;
+                    if (kc & 1) dmma884(f0, f1, tsp * tt[it], bv);
+                    else dmma884(d0, d1, tsp * tt[it], bv);
+                }
+            }
+            // 3. lane (r, tig) holds (re, im) of child pipe tig for evaluation row r
+            const double2 val = make_double2(d0 + f0, d1 + f1);
+            const double2 r1 = make_double2(gp[3], gp[4]);
+            const double xf = gp[5];
+            int fac = R1;
+#pragma unroll
+            for (int pc = 0; pc < NPC; ++pc)
+                if (tig == pc) fac = CB::fac(pc);
+            double2 ctb;
+            if (fac == R1) {
+                ctb = cmul(r1, val);
+            } else if (fac == MK) {
+                const double2 w = cmul(r1, val);
+                ctb = make_double2(k * w.y, -k * w.x);
+            } else {  // RI or RQ: ratio1 times the stored extra factor
+                ctb = cmul(cscale(r1, xf), val);
+            }
+            if constexpr (COMBO == 0) {  // child W2, W3 -> parent W4: sum across the quad
+                const double ox = __shfl_down_sync(0xffffffffu, ctb.x, 1);
+                const double oy = __shfl_down_sync(0xffffffffu, ctb.y, 1);
+                if (tig == 1) ctb = make_double2(ctb.x + ox, ctb.y + oy);
+            } else if constexpr (COMBO == 3) {
+                const double ox = __shfl_down_sync(0xffffffffu, ctb.x, 1);
+                const double oy = __shfl_down_sync(0xffffffffu, ctb.y, 1);
+                if (tig == 0) ctb = make_double2(ctb.x + ox, ctb.y + oy);
+            }
+            bool writer = valid && tig < NPC;
+            if constexpr (COMBO == 0) writer = writer && tig != 2;
+            if constexpr (COMBO == 3) writer = writer && tig == 0;
+            if (writer) {
+                int dst = 0;
+#pragma unroll
+                for (int pc = 0; pc < NPC; ++pc)
+                    if (tig == pc) dst = CB::dst(pc);
+                double2& a = acc[int(gp[6]) * NPP + dst];
+                a = cadd(a, ctb);
+            }
+        }
+        __syncwarp();
+    }
+    // values -> coefficients (transform3, ifgf.cpp:560-562), warp-local
+    double2* v0 = acc;
+    double2* v1 = reinterpret_cast<double2*>(geo);
+    double2* dst = pstore + std::size_t(so) * NPP * kNP;
+    // acc is node-major (node * NPP + i); transpose into pipe-major blocks while applying
+    // the s-direction transform, then theta, then phi
+    for (int e = lane; e < NPP * kNP; e += 32) {
+        const int blk = e / kNP, node = e % kNP;
+        const int is = node % kPS, line = node / kPS;
+        double2 a = make_double2(0.0, 0.0);
+        for (int q = 0; q < kPS; ++q) cfma_r(a, v0[(line * kPS + q) * NPP + blk], Ms[is * kPS + q]);
+        v1[e] = a;
+    }
+    __syncwarp();
+    for (int e = lane; e < NPP * kNP; e += 32) {
+        const int blk = e / kNP, node = e % kNP;
+        const int is = node % kPS, it = (node / kPS) % kPA, ip = node / (kPS * kPA);
+        const double2* src = v1 + blk * kNP + is + kPS * kPA * ip;
+        double2 a = make_double2(0.0, 0.0);
+        for (int q = 0; q < kPA; ++q) cfma_r(a, src[kPS * q], Ma[it * kPA + q]);
+        v0[e] = a;
+    }
+    __syncwarp();
+    for (int e = lane; e < NPP * kNP; e += 32) {
+        const int blk = e / kNP, node = e % kNP;
+        const int is = node % kPS, it = (node / kPS) % kPA, ip = node / (kPS * kPA);
+        const double2* src = v0 + blk * kNP + is + kPS * it;
+        double2 a = make_double2(0.0, 0.0);
+        for (int q = 0; q < kPA; ++q) cfma_r(a, src[kPS * kPA * q], Ma[ip * kPA + q]);
+        dst[e] = a;
+    }
+}
+
+int combo_of(const Pipes& pp, const Pipes& pc) {
+    auto is = [](const Pipes& p, std::initializer_list<int> f) {
+        if (p.n != int(f.size())) return false;
+        int i = 0;
+        for (int x : f)
+            if (p.f[i++] != x) return false;
+        return true;
+    };
+    if (is(pp, {1, 4}) && is(pc, {1, 2, 3})) return 0;
+    if (is(pp, {1, 4}) && is(pc, {1, 4})) return 1;
+    if ((is(pp, {1}) && is(pc, {1})) || (is(pp, {4}) && is(pc, {4}))) return 2;
+    if (is(pp, {4}) && is(pc, {2, 3})) return 3;
+    if (is(pp, {1, 2, 3}) && is(pc, {1, 2, 3})) return 4;
+    if (is(pp, {2, 3}) && is(pc, {2, 3})) return 5;
+    return -1;
+}
+
+}  // namespace
+
+bool launch_parent_fill_tc(const LevelDev& Lp, const LevelDev& Lc, const double2* child_store, double k,
+                           const Pipes& parent_pipes, const Pipes& child_pipes, const double* Ms,
+                           const double* Ma, double2* parent_store, cudaStream_t st) {
+    const int combo = combo_of(parent_pipes, child_pipes);
+    if (combo < 0 || Lp.ps != kPS || Lp.pang != kPA || Lc.ps != kPS || Lc.pang != kPA || !Lc.pgrp_begin ||
+        !Lp.th_sin)
+        return false;
+    if (Lp.nseg == 0) return true;
+    const std::size_t smem = std::size_t(kWarps) * (kGeoSz + 2 * kNP * parent_pipes.n) * sizeof(double);
+    auto go = [&](auto kern) {
+        IFGF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        kern<<<(Lp.nseg + kWarps - 1) / kWarps, 32 * kWarps, smem, st>>>(Lp, Lc, child_store, k, Ms, Ma, parent_store);
+    };
+    switch (combo) {
+        case 0: go(parent_tc_kernel<0>); break;
+        case 1: go(parent_tc_kernel<1>); break;
+        case 2: go(parent_tc_kernel<2>); break;
+        case 3: go(parent_tc_kernel<3>); break;
+        case 4: go(parent_tc_kernel<4>); break;
+        default: go(parent_tc_kernel<5>); break;
+    }
+    IFGF_CUDA(cudaGetLastError());
+    return true;
+}
+
+}  // namespace ifgfb200

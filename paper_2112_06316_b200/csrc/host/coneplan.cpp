@@ -117,6 +117,44 @@ inline void mark(std::vector<std::uint8_t>& m, std::size_t at) {
     __atomic_store_n(&m[at], std::uint8_t(1), __ATOMIC_RELAXED);
 }
 
+// per parent segment: stable order of its evaluations by child segment, and the groups
+void group_parent_evaluations(ConeLevel& L, std::size_t pseg, int w) {
+    L.pev_perm.assign(L.pev_seg.size(), 0);
+    std::vector<std::int32_t> ngroups(pseg + 1, 0);
+    parallel_for(std::int64_t(pseg), w, [&](std::int64_t so) {
+        const std::int64_t b = L.pev_begin[so], n = L.pev_begin[so + 1] - b;
+        if (n > 65535) throw InternalError("cone plan: too many evaluations per parent segment");
+        std::uint16_t* perm = L.pev_perm.data() + b;
+        for (std::int64_t i = 0; i < n; ++i) perm[i] = std::uint16_t(i);
+        const std::int32_t* seg = L.pev_seg.data() + b;
+        std::stable_sort(perm, perm + n, [&](std::uint16_t x, std::uint16_t y) { return seg[x] < seg[y]; });
+        int g = 0;
+        for (std::int64_t i = 0; i < n; ++i)
+            if (i == 0 || seg[perm[i]] != seg[perm[i - 1]]) ++g;
+        ngroups[so + 1] = g;
+    });
+    L.pgrp_begin.assign(pseg + 1, 0);
+    for (std::size_t so = 0; so < pseg; ++so) L.pgrp_begin[so + 1] = L.pgrp_begin[so] + ngroups[so + 1];
+    const std::size_t ng = std::size_t(L.pgrp_begin[pseg]);
+    L.pgrp_seg.assign(ng, 0);
+    L.pgrp_start.assign(ng, 0);
+    L.pgrp_count.assign(ng, 0);
+    parallel_for(std::int64_t(pseg), w, [&](std::int64_t so) {
+        const std::int64_t b = L.pev_begin[so], n = L.pev_begin[so + 1] - b;
+        const std::uint16_t* perm = L.pev_perm.data() + b;
+        const std::int32_t* seg = L.pev_seg.data() + b;
+        std::int32_t g = L.pgrp_begin[so] - 1;
+        for (std::int64_t i = 0; i < n; ++i) {
+            if (i == 0 || seg[perm[i]] != seg[perm[i - 1]]) {
+                ++g;
+                L.pgrp_seg[g] = seg[perm[i]];
+                L.pgrp_start[g] = std::uint16_t(i);
+            }
+            ++L.pgrp_count[g];
+        }
+    });
+}
+
 }  // namespace
 
 int cone_doublings(double side, double lambda) {
@@ -277,6 +315,7 @@ ConePlanHost build_cone_plan(const BoxTree& t, const BoxRelations& rel,
                     for (int c = 0; c < nch; ++c, ++at)
                         L.pev_seg[at] = ordinal(cidx[cptr[pb] + c], L.pev_seg[at]);
             });
+            group_parent_evaluations(L, PL.nseg(), w);
         }
     }
     return plan;

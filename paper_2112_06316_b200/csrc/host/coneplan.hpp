@@ -41,6 +41,14 @@ struct ConeLevel {
     // parent segment so, node (is + ps*(it + pang*ip)), child slot c -> child segment ordinal
     std::vector<std::int64_t> pev_begin;  // nseg(d-1) + 1 (empty at d = 3)
     std::vector<std::int32_t> pev_seg;
+    // the same evaluations grouped by child segment, per parent segment (FP64 tensor-core
+    // tiles need 8 evaluations of one coefficient block): pev_perm lists local indices
+    // (node * nch + c) in group order; group g of parent segment so covers
+    // [pgrp_start[g], pgrp_start[g] + pgrp_count[g]) of that list and uses pgrp_seg[g]
+    std::vector<std::uint16_t> pev_perm;
+    std::vector<std::int32_t> pgrp_begin;  // nseg(d-1) + 1
+    std::vector<std::int32_t> pgrp_seg;
+    std::vector<std::uint16_t> pgrp_start, pgrp_count;
 
     int segs_per_box() const { return ns * nc * 2 * nc; }
     int nodes_per_seg() const { return ps * pang * pang; }
