@@ -119,7 +119,7 @@ leaf_fill_kernel(LevelDev L, PointsDev P, const double2* __restrict__ a_p, doubl
                     const double nv = nv2 * inv;
                     const double arg = khos * (nv2 - 1.0) * fast_rcp(nv + 1.0);
                     double sn, cs;
-                    sincos(arg, &sn, &cs);
+                    sincos_bounded(arg, &sn, &cs);
                     const double ar = sar[q], ai = sai[q];
                     const double2 pa_ = make_double2(fma(ar, cs, -ai * sn), fma(ar, sn, ai * cs));
                     const double dn = fma(vx, snx[q], fma(vy, sny[q], vz * snz[q]));
@@ -191,7 +191,7 @@ cousin_kernel(LevelDev L, PointsDev P, const double2* __restrict__ store, double
             const LocalCoords lc = local_coords(vx, vy, vz, inv_r, h, L.seg_gamma[so], L);
             basis3<PS, PA>(lc, ts, tt, tp, ps, pa);
             double sn, cs;
-            sincos(k * r, &sn, &cs);
+            sincos_bounded(k * r, &sn, &cs);
             const double f1 = kInv4PiD * inv_r;
             e1 = make_double2(cs * f1, sn * f1);  // e^{ikr}/(4 pi r)
         }
@@ -290,7 +290,7 @@ parent_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, doub
                 // stable r_c - r_p (ifgf.cpp:149-153)
                 const double sx = ccx + pcx - 2.0 * x, sy = ccy + pcy - 2.0 * y, sz = ccz + pcz - 2.0 * z;
                 const double dr = fma(sx, ccx - pcx, fma(sy, ccy - pcy, sz * (ccz - pcz))) / (rc + rp);
-                sincos(k * dr, &sn, &cs);
+                sincos_bounded(k * dr, &sn, &cs);
                 q1 = rp * inv_rc;
             }
             const double2 ratio1 = make_double2(cs * q1, sn * q1);
@@ -343,6 +343,7 @@ void launch_leaf_fill(const LevelDev& L, const PointsDev& P, const double2* a_p,
                       const Pipes& pipes, const double* Ms, const double* Ma, double2* store,
                       cudaStream_t st) {
     if (L.nb == 0 || L.nseg == 0) return;
+    if (launch_leaf_fill_ray(L, P, a_p, k, pipes, Ms, Ma, store, st)) return;
     const int NPTS = L.ps * L.pang * L.pang;
     const int G = std::max(1, kLeafThreads / NPTS);
     const std::size_t smem = 8 * kLeafTile * sizeof(double) + 2 * std::size_t(G) * pipes.n * NPTS * sizeof(double2);

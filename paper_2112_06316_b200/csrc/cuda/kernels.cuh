@@ -25,6 +25,9 @@ void launch_parent_fill(const LevelDev& Lp, const LevelDev& Lc, const double2* c
                         double k, const Pipes& parent_pipes, const Pipes& child_pipes,
                         const double* Ms, const double* Ma, double2* parent_store, cudaStream_t st);
 
+// ray-blocked level-D fill (leaf_ray.cu) for ps = 3; false if not applicable
+bool launch_leaf_fill_ray(const LevelDev& L, const PointsDev& P, const double2* a_p, double k, const Pipes& pipes,
+                          const double* Ms, const double* Ma, double2* store, cudaStream_t st);
 // FP64 tensor-core parent fill (parent_tc.cu) for ps = 3, pang = 5; false if not applicable
 bool launch_parent_fill_tc(const LevelDev& Lp, const LevelDev& Lc, const double2* child_store, double k,
                            const Pipes& parent_pipes, const Pipes& child_pipes, const double* Ms,

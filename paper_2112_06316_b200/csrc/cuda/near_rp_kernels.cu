@@ -49,7 +49,7 @@ __device__ __forceinline__ void pair_kernels(double x, double y, double z, doubl
     const double inv = rsqrt(r2);
     const double r = r2 * inv;
     double sn, cs;
-    sincos(k * r, &sn, &cs);
+    sincos_bounded(k * r, &sn, &cs);
     const double g = kInv4PiD * inv;
     const double2 ga = cmul(make_double2(cs * g, sn * g), a);
     accS.x = fma(sg, ga.x, accS.x);
