@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libifgf_b200.so")
+LIB_PATH = os.environ.get("IFGF_B200_LIB") or os.path.join(HERE, "lib", "libifgf_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "ifgf_b200.h")
 
 d_p = C.POINTER(C.c_double)

@@ -34,6 +34,9 @@ struct LevelDev {
     const double *s_nodes = nullptr, *th_nodes = nullptr, *ph_nodes = nullptr;
     // sin/cos of the angular node tables (interpolation-node directions)
     const double *th_sin = nullptr, *th_cos = nullptr, *ph_sin = nullptr, *ph_cos = nullptr;
+    // cos/sin of the theta- and phi-cell centres (nc and 2nc entries); null when cells are
+    // wider than pi/4 (nc < 4), where local_coords uses acos/atan2
+    const double *thc_cos = nullptr, *thc_sin = nullptr, *phc_cos = nullptr, *phc_sin = nullptr;
     const std::int32_t *chunk_box = nullptr, *chunk_q0 = nullptr;  // cousin work chunks
     int nchunk = 0;
     int max_pts = 0;  // largest box

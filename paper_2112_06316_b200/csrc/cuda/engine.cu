@@ -60,7 +60,7 @@ class DevBuf {
 
 struct LevelBufs {
     DevBuf cx, cy, cz, beg, end, cz_ptr, cz_idx, cev_begin, cev_seg, seg_box, seg_gamma,
-        box_seg_begin, pev_begin, pev_seg, pev_perm, pgrp_begin, pgrp_seg, pgrp_start, pgrp_count, ch_ptr, ch_idx, s_nodes, th_nodes, ph_nodes, th_sin, th_cos, ph_sin, ph_cos,
+        box_seg_begin, pev_begin, pev_seg, pev_perm, pgrp_begin, pgrp_seg, pgrp_start, pgrp_count, ch_ptr, ch_idx, s_nodes, th_nodes, ph_nodes, th_sin, th_cos, ph_sin, ph_cos, thc_cos, thc_sin, phc_cos, phc_sin,
         chunk_box, chunk_q0;
 };
 
@@ -323,6 +323,21 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
             b.th_cos.upload(tc);
             b.ph_sin.upload(ps_);
             b.ph_cos.upload(pc_);
+            if (CL.nc >= 4) {  // cell centres for the acos/atan2-free local coordinates
+                std::vector<double> a(CL.nc), bb(CL.nc), c(2 * CL.nc), d(2 * CL.nc);
+                for (int g = 0; g < CL.nc; ++g) {
+                    a[g] = std::cos((g + 0.5) * CL.dth);
+                    bb[g] = std::sin((g + 0.5) * CL.dth);
+                }
+                for (int g = 0; g < 2 * CL.nc; ++g) {
+                    c[g] = std::cos((g + 0.5) * CL.dph);
+                    d[g] = std::sin((g + 0.5) * CL.dph);
+                }
+                b.thc_cos.upload(a);
+                b.thc_sin.upload(bb);
+                b.phc_cos.upload(c);
+                b.phc_sin.upload(d);
+            }
         }
         b.chunk_box.upload(chunk_box);
         b.chunk_q0.upload(chunk_q0);
@@ -368,6 +383,10 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         L.th_cos = b.th_cos.as<double>();
         L.ph_sin = b.ph_sin.as<double>();
         L.ph_cos = b.ph_cos.as<double>();
+        L.thc_cos = CL.nc >= 4 ? b.thc_cos.as<double>() : nullptr;
+        L.thc_sin = CL.nc >= 4 ? b.thc_sin.as<double>() : nullptr;
+        L.phc_cos = CL.nc >= 4 ? b.phc_cos.as<double>() : nullptr;
+        L.phc_sin = CL.nc >= 4 ? b.phc_sin.as<double>() : nullptr;
         L.chunk_box = b.chunk_box.as<std::int32_t>();
         L.chunk_q0 = b.chunk_q0.as<std::int32_t>();
         L.nchunk = int(chunk_box.size());

@@ -18,7 +18,7 @@ struct LocalCoords {
 
 // Cone coordinates of v = x - centre (inv_r = 1/|v|) relative to the host-decided segment
 // gamma, mapped to [-1,1]^3 (LevelCones::local_coords, ifgf.cpp:178-183).
-__device__ __forceinline__ LocalCoords local_coords(double vx, double vy, double vz, double inv_r,
+__device__ __forceinline__ LocalCoords local_coords_lib(double vx, double vy, double vz, double inv_r,
                                                     double h, int gamma, const LevelDev& L) {
     const double s = h * inv_r;
     double ct = vz * inv_r;
@@ -37,6 +37,91 @@ __device__ __forceinline__ LocalCoords local_coords(double vx, double vy, double
     o.ls = fma(s, 2.0 * L.inv_ds, -(2 * g1 + 1.0));
     o.lt = fma(th, 2.0 * L.inv_dth, -(2 * g2 + 1.0));
     o.lp = fma(ph, 2.0 * L.inv_dph, -(2 * g3 + 1.0));
+    return o;
+}
+
+// atan(t) for |t| <= 0.4225 (cells of at most pi/4: nc >= 4): t * P(t^2), degree-11
+// least-squares fit (max abs error 6e-17 on the interval)
+__device__ __forceinline__ double atan_small(double t) {
+    const double u = t * t;
+    double p = -0.01723604573229859;
+    p = fma(p, u, 0.03744269623222812);
+    p = fma(p, u, -0.05014437831961434);
+    p = fma(p, u, 0.05842271768042808);
+    p = fma(p, u, -0.06662315934685337);
+    p = fma(p, u, 0.07691989116146059);
+    p = fma(p, u, -0.09090893628137384);
+    p = fma(p, u, 0.11111110633111605);
+    p = fma(p, u, -0.14285714276966102);
+    p = fma(p, u, 0.1999999999991704);
+    p = fma(p, u, -0.33333333333333026);
+    p = fma(p, u, 1.0);
+    return t * p;
+}
+
+// host-decided cell of a segment, decoded once (and its centre directions when tabulated)
+struct CellFrame {
+    int g1, g2, g3;
+    double ctc, stc, cpc, spc;
+};
+__device__ __forceinline__ CellFrame cell_frame(int gamma, const LevelDev& L) {
+    CellFrame f;
+    f.g1 = gamma % L.ns;
+    const int rest = gamma / L.ns;
+    f.g2 = rest % L.nc;
+    f.g3 = rest / L.nc;
+    if (L.thc_cos) {
+        f.ctc = L.thc_cos[f.g2];
+        f.stc = L.thc_sin[f.g2];
+        f.cpc = L.phc_cos[f.g3];
+        f.spc = L.phc_sin[f.g3];
+    } else {
+        f.ctc = f.stc = f.cpc = f.spc = 0.0;
+    }
+    return f;
+}
+
+// local coordinates inside a decoded cell (see local_coords below)
+__device__ __forceinline__ LocalCoords local_coords_in(double vx, double vy, double vz, double inv_r, double h,
+                                                       const CellFrame& f, const LevelDev& L) {
+    const int gamma = f.g1 + L.ns * (f.g2 + L.nc * f.g3);
+    if (!L.thc_cos) return local_coords_lib(vx, vy, vz, inv_r, h, gamma, L);
+    const double rho = sqrt(fma(vx, vx, vy * vy));
+    const double tn = fma(rho, f.ctc, -vz * f.stc), td = fma(vz, f.ctc, rho * f.stc);
+    const double pn = fma(vy, f.cpc, -vx * f.spc), pd = fma(vx, f.cpc, vy * f.spc);
+    const double tt = tn / td, tp = pn / pd;
+    if (!(fabs(tt) <= 0.4225 && fabs(tp) <= 0.4225 && td > 0.0 && pd > 0.0))
+        return local_coords_lib(vx, vy, vz, inv_r, h, gamma, L);
+    LocalCoords o;
+    o.ls = fma(h * inv_r, 2.0 * L.inv_ds, -(2 * f.g1 + 1.0));
+    o.lt = atan_small(tt) * (2.0 * L.inv_dth);
+    o.lp = atan_small(tp) * (2.0 * L.inv_dph);
+    return o;
+}
+
+// Same map without acos/atan2: the angles are taken relative to the centre of the
+// host-decided cell, theta - theta_c = atan((rho cos th_c - vz sin th_c) / (vz cos th_c +
+// rho sin th_c)) and likewise for phi (no 0/2pi seam at all), both inside +-pi/(2 nc).
+// Falls back to local_coords_lib if a point lies unexpectedly far outside its cell.
+__device__ __forceinline__ LocalCoords local_coords(double vx, double vy, double vz, double inv_r,
+                                                    double h, int gamma, const LevelDev& L) {
+    if (!L.thc_cos) return local_coords_lib(vx, vy, vz, inv_r, h, gamma, L);
+    const int g1 = gamma % L.ns;
+    const int rest = gamma / L.ns;
+    const int g2 = rest % L.nc;
+    const int g3 = rest / L.nc;
+    const double rho = sqrt(fma(vx, vx, vy * vy));
+    const double ctc = L.thc_cos[g2], stc = L.thc_sin[g2];
+    const double cpc = L.phc_cos[g3], spc = L.phc_sin[g3];
+    const double tn = fma(rho, ctc, -vz * stc), td = fma(vz, ctc, rho * stc);
+    const double pn = fma(vy, cpc, -vx * spc), pd = fma(vx, cpc, vy * spc);
+    const double tt = tn / td, tp = pn / pd;
+    if (!(fabs(tt) <= 0.4225 && fabs(tp) <= 0.4225 && td > 0.0 && pd > 0.0))
+        return local_coords_lib(vx, vy, vz, inv_r, h, gamma, L);
+    LocalCoords o;
+    o.ls = fma(h * inv_r, 2.0 * L.inv_ds, -(2 * g1 + 1.0));
+    o.lt = atan_small(tt) * (2.0 * L.inv_dth);
+    o.lp = atan_small(tp) * (2.0 * L.inv_dph);
     return o;
 }
 

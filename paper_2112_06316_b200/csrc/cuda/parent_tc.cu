@@ -80,7 +80,7 @@ struct Combo<5> {  // (W2,W3) <- (W2,W3)
 };
 
 template <int COMBO>
-__global__ void __launch_bounds__(32 * kWarps, 6)
+__global__ void __launch_bounds__(32 * kWarps, 4)
 parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, double k,
                  const double* __restrict__ Ms, const double* __restrict__ Ma,
                  double2* __restrict__ pstore) {
@@ -97,7 +97,7 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
     const int pb = Lp.seg_box[so];
     const int gam = Lp.seg_gamma[so];
     const int g1 = gam % Lp.ns, g2 = (gam / Lp.ns) % Lp.nc, g3 = gam / Lp.ns / Lp.nc;
-    const int c0 = Lp.ch_ptr[pb], nch = Lp.ch_ptr[pb + 1] - c0;
+    const int c0 = Lp.ch_ptr[pb];
     const std::int64_t ev0 = Lc.pev_begin[so];
     const double hp = Lp.h, hc = Lc.h;
     const double pcx = Lp.cx[pb], pcy = Lp.cy[pb], pcz = Lp.cz[pb];
@@ -110,26 +110,27 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
     for (int g = gb; g < ge; ++g) {
         const int cso = Lc.pgrp_seg[g];
         const int start = Lc.pgrp_start[g], count = Lc.pgrp_count[g];
-        // 1. geometry of the group's evaluations
+        // 1. geometry of the group's evaluations (one child box and one child cell per group)
+        const int c_grp = Lc.pev_perm[ev0 + start] >> 8;
+        const int ch = Lp.ch_idx[c0 + c_grp];
+        const double ccx = Lc.cx[ch], ccy = Lc.cy[ch], ccz = Lc.cz[ch];
+        const CellFrame cf = cell_frame(Lc.seg_gamma[cso], Lc);
         for (int i = lane; i < count; i += 32) {
-            const int e = Lc.pev_perm[ev0 + start + i];
-            const int node = e / nch, c = e - node * nch;
+            const int node = Lc.pev_perm[ev0 + start + i] & 0xff;  // entries are node | c << 8
             const int is = node % kPS, it = (node / kPS) % kPA, ip = node / (kPS * kPA);
             const double s = Lp.s_nodes[g1 * kPS + is];
             const double rp = hp / s;
             const double sth = Lp.th_sin[g2 * kPA + it], cth = Lp.th_cos[g2 * kPA + it];
             const double sph = Lp.ph_sin[g3 * kPA + ip], cph = Lp.ph_cos[g3 * kPA + ip];
             const double x = pcx + rp * sth * cph, y = pcy + rp * sth * sph, z = pcz + rp * cth;
-            const int ch = Lp.ch_idx[c0 + c];
-            const double ccx = Lc.cx[ch], ccy = Lc.cy[ch], ccz = Lc.cz[ch];
             const double vx = x - ccx, vy = y - ccy, vz = z - ccz;
             const double rc2 = fma(vx, vx, fma(vy, vy, vz * vz));
             const double inv_rc = rsqrt(rc2);
             const double rc = rc2 * inv_rc;
-            const LocalCoords lc = local_coords(vx, vy, vz, inv_rc, hc, Lc.seg_gamma[cso], Lc);
+            const LocalCoords lc = local_coords_in(vx, vy, vz, inv_rc, hc, cf, Lc);
             // stable r_c - r_p (ifgf.cpp:149-153)
             const double sx = ccx + pcx - 2.0 * x, sy = ccy + pcy - 2.0 * y, sz = ccz + pcz - 2.0 * z;
-            const double dr = fma(sx, ccx - pcx, fma(sy, ccy - pcy, sz * (ccz - pcz))) * fast_rcp(rc + rp);
+            const double dr = fma(sx, ccx - pcx, fma(sy, ccy - pcy, sz * (ccz - pcz))) / (rc + rp);
             double sn, cs;
             sincos_bounded(k * dr, &sn, &cs);
             const double q1 = rp * inv_rc;
@@ -144,7 +145,12 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
         }
         __syncwarp();
         // 2. 8-evaluation tensor-core tiles against the child block
+        // B fragments of the group's block: k = the s index (padded 3 -> 4), 25 k-steps over
+        // (theta, phi); loaded once per group, reused by all its tiles
         const double* blk = reinterpret_cast<const double*>(cstore + std::size_t(cso) * NPC * kNP) + boff;
+        double bq[kPA * kPA];
+#pragma unroll
+        for (int kc = 0; kc < kPA * kPA; ++kc) bq[kc] = bcol ? __ldg(blk + 2 * kPS * kc) : 0.0;
         for (int t0 = 0; t0 < count; t0 += 8) {
             const bool valid = t0 + r < count;
             const double* gp = geo + (valid ? t0 + r : 0) * kGeo;
@@ -161,9 +167,8 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
 #pragma unroll
                 for (int it = 0; it < kPA; ++it) {
                     const int kc = it + kPA * ip;
-                    const double bv = bcol ? __ldg(blk + 2 * kPS * kc) : 0.0;
-                    if (kc & 1) dmma884(f0, f1, tsp * tt[it], bv);
-                    else dmma884(d0, d1, tsp * tt[it], bv);
+                    if (kc & 1) dmma884(f0, f1, tsp * tt[it], bq[kc]);
+                    else dmma884(d0, d1, tsp * tt[it], bq[kc]);
                 }
             }
             // 3. lane (r, tig) holds (re, im) of child pipe tig for evaluation row r

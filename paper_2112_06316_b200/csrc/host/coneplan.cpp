@@ -118,7 +118,7 @@ inline void mark(std::vector<std::uint8_t>& m, std::size_t at) {
 }
 
 // per parent segment: stable order of its evaluations by child segment, and the groups
-void group_parent_evaluations(ConeLevel& L, std::size_t pseg, int w) {
+void group_parent_evaluations(ConeLevel& L, std::size_t pseg, int w, int P) {
     L.pev_perm.assign(L.pev_seg.size(), 0);
     std::vector<std::int32_t> ngroups(pseg + 1, 0);
     parallel_for(std::int64_t(pseg), w, [&](std::int64_t so) {
@@ -153,6 +153,15 @@ void group_parent_evaluations(ConeLevel& L, std::size_t pseg, int w) {
             ++L.pgrp_count[g];
         }
     });
+    // pack each local index e = node * nch + c as node | c << 8 for the device (P <= 255)
+    if (P <= 255)
+        parallel_for(std::int64_t(pseg), w, [&](std::int64_t so) {
+            const std::int64_t b = L.pev_begin[so], n = L.pev_begin[so + 1] - b;
+            const int nch = int(n / P);
+            std::uint16_t* perm = L.pev_perm.data() + b;
+            for (std::int64_t i = 0; i < n; ++i)
+                perm[i] = std::uint16_t((perm[i] / nch) | ((perm[i] % nch) << 8));
+        });
 }
 
 }  // namespace
@@ -315,7 +324,7 @@ ConePlanHost build_cone_plan(const BoxTree& t, const BoxRelations& rel,
                     for (int c = 0; c < nch; ++c, ++at)
                         L.pev_seg[at] = ordinal(cidx[cptr[pb] + c], L.pev_seg[at]);
             });
-            group_parent_evaluations(L, PL.nseg(), w);
+            group_parent_evaluations(L, PL.nseg(), w, P);
         }
     }
     return plan;

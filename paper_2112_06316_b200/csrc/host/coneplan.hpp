@@ -44,7 +44,8 @@ struct ConeLevel {
     // the same evaluations grouped by child segment, per parent segment (FP64 tensor-core
     // tiles need 8 evaluations of one coefficient block): pev_perm lists local indices
     // (node * nch + c) in group order; group g of parent segment so covers
-    // [pgrp_start[g], pgrp_start[g] + pgrp_count[g]) of that list and uses pgrp_seg[g]
+    // [pgrp_start[g], pgrp_start[g] + pgrp_count[g]) of that list and uses pgrp_seg[g];
+    // when nodes_per_seg <= 255 the entries are packed as node | c << 8
     std::vector<std::uint16_t> pev_perm;
     std::vector<std::int32_t> pgrp_begin;  // nseg(d-1) + 1
     std::vector<std::int32_t> pgrp_seg;
