@@ -160,6 +160,25 @@ int ifgf_operator_kernels_per_apply(const ifgf_operator* op);
 void* ifgf_operator_device_phi(ifgf_operator* op);
 void* ifgf_operator_device_out(ifgf_operator* op);
 
+/* ---- multi-GPU (one process per GPU, NCCL over NVLink) ----
+ * Each operator owns the sources and targets of a leaf-aligned Morton range: the far
+ * field is computed from owned sources for ALL targets and reduced to the target owners
+ * (grouped ncclReduce), near field + RP run target-owned, the owners broadcast their
+ * outputs. Every rank passes the full phi and receives the full out. */
+int ifgf_nccl_unique_id(void* id128);
+/* collective over the world; computes the cost-balanced partition and takes part `rank` */
+int ifgf_operator_set_comm(ifgf_operator* op, int rank, int world, const void* id128);
+/* cost-balanced, leaf-aligned Morton boundaries: parts + 1 values (host only) */
+int ifgf_operator_partition(const ifgf_operator* op, int parts, uint32_t* bounds);
+int ifgf_plan_partition(const ifgf_plan* p, int parts, uint32_t* bounds);
+/* own [lo, hi) without a communicator (single-GPU emulation of one rank) */
+int ifgf_operator_set_partition(ifgf_operator* op, uint32_t lo, uint32_t hi);
+/* near field + RP + combine for the owned targets given the full far field S, D
+ * (original order, e.g. the sum of every rank's ifgf_operator_ifgf_apply); out is zero
+ * outside the owned targets */
+int ifgf_operator_finish_owned(ifgf_operator* op, const double* phi, const double* far_S,
+                               const double* far_D, double* out);
+
 /* ---- GMRES (solver.cpp:169-340 semantics: MGS, Givens, optional restart) ---- */
 int ifgf_gmres_solve(ifgf_operator* op, const double* rhs, double tol, int max_iter,
                      int restart, double* x, double* history, int history_cap,

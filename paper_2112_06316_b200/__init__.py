@@ -5,12 +5,12 @@ operator API (solver.hpp / geometry.hpp / ifgf.hpp / rp.hpp)."""
 from ._lib import (ConvergenceFailure, DegenerateGeometry, DeviceError, IfgfError, InternalError,
                    InvalidArgument, ParseError, lib)
 from .operator import (CombinedOperator, ConeConfig, DlStrategy, Factor, GmresResult, HostPlan,
-                       IncidentField, RpConfig, SolveConfig, SurfaceMesh, gmres_solve, random_density,
-                       solve)
+                       IncidentField, RpConfig, SolveConfig, SurfaceMesh, gmres_solve, nccl_unique_id,
+                       random_density, solve)
 
 __all__ = [
     "CombinedOperator", "ConeConfig", "DlStrategy", "Factor", "GmresResult", "HostPlan", "IncidentField",
-    "RpConfig", "SolveConfig", "SurfaceMesh", "gmres_solve", "random_density", "solve", "lib",
+    "RpConfig", "SolveConfig", "SurfaceMesh", "gmres_solve", "nccl_unique_id", "random_density", "solve", "lib",
     "IfgfError", "InvalidArgument", "ParseError", "DegenerateGeometry", "ConvergenceFailure",
     "InternalError", "DeviceError",
 ]

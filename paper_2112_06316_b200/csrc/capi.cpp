@@ -8,6 +8,8 @@
 #include <random>
 #include <string>
 
+#include <nccl.h>
+
 #include "../../include/ifgf_b200.h"
 #include "engine.hpp"
 #include "host/chebyshev.hpp"
@@ -815,6 +817,62 @@ int ifgf_operator_time_phases(ifgf_operator* op, double* ms7) {
 int ifgf_operator_kernels_per_apply(const ifgf_operator* op) { return op ? op->eng->kernels_per_apply() : -1; }
 void* ifgf_operator_device_phi(ifgf_operator* op) { return op ? op->eng->device_phi() : nullptr; }
 void* ifgf_operator_device_out(ifgf_operator* op) { return op ? op->eng->device_out() : nullptr; }
+
+// ------------------------------------------------------------------ multi-GPU
+int ifgf_nccl_unique_id(void* id128) {
+    return guarded([&] {
+        need(id128, "id");
+        ncclUniqueId id;
+        const ncclResult_t r = ncclGetUniqueId(&id);
+        if (r != ncclSuccess) throw EngineError(kNcclError, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+        static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+        std::memcpy(id128, &id, sizeof id);
+    });
+}
+
+int ifgf_operator_set_comm(ifgf_operator* op, int rank, int world, const void* id128) {
+    return guarded([&] {
+        need(op, "operator");
+        need(id128, "id");
+        op->eng->set_comm(rank, world, id128);
+    });
+}
+
+int ifgf_operator_partition(const ifgf_operator* op, int parts, uint32_t* bounds) {
+    return guarded([&] {
+        need(op, "operator");
+        need(bounds, "bounds");
+        const auto b = op->eng->partition_bounds(parts);
+        std::memcpy(bounds, b.data(), b.size() * sizeof(uint32_t));
+    });
+}
+
+int ifgf_plan_partition(const ifgf_plan* p, int parts, uint32_t* bounds) {
+    return guarded([&] {
+        need(p, "plan");
+        need(bounds, "bounds");
+        const auto b = partition_sources(p->tree, p->rel, p->cones, parts);
+        std::memcpy(bounds, b.data(), b.size() * sizeof(uint32_t));
+    });
+}
+
+int ifgf_operator_set_partition(ifgf_operator* op, uint32_t lo, uint32_t hi) {
+    return guarded([&] {
+        need(op, "operator");
+        op->eng->set_partition(lo, hi);
+    });
+}
+
+int ifgf_operator_finish_owned(ifgf_operator* op, const double* phi, const double* far_S, const double* far_D,
+                               double* out) {
+    return guarded([&] {
+        need(op, "operator");
+        for (const void* p : {(const void*)phi, (const void*)far_S, (const void*)far_D, (const void*)out})
+            need(p, "finish_owned");
+        op->eng->finish_owned(reinterpret_cast<const cplx*>(phi), reinterpret_cast<const cplx*>(far_S),
+                              reinterpret_cast<const cplx*>(far_D), reinterpret_cast<cplx*>(out));
+    });
+}
 
 // ------------------------------------------------------------------ GMRES
 int ifgf_gmres_solve(ifgf_operator* op, const double* rhs, double tol, int max_iter, int restart, double* x,

@@ -37,6 +37,8 @@ struct LevelDev {
     // cos/sin of the theta- and phi-cell centres (nc and 2nc entries); null when cells are
     // wider than pi/4 (nc < 4), where local_coords uses acos/atan2
     const double *thc_cos = nullptr, *thc_sin = nullptr, *phc_cos = nullptr, *phc_sin = nullptr;
+    // multi-GPU source ownership: box has sources in this rank's Morton range (null = all)
+    const std::uint8_t* active = nullptr;
     const std::int32_t *chunk_box = nullptr, *chunk_q0 = nullptr;  // cousin work chunks
     int nchunk = 0;
     int max_pts = 0;  // largest box

@@ -7,6 +7,7 @@
 // ifgf.cpp:577-608; layer_potentials + apply, solver.cpp:78-157). Only two IFGF levels of
 // coefficient blocks are live at a time (ifgf.cpp:589-597), in two ping-pong buffers.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cstring>
@@ -19,6 +20,14 @@
 #include "kernels.cuh"
 
 namespace ifgfb200 {
+
+#define IFGF_NCCL(call)                                                                     \
+    do {                                                                                     \
+        ncclResult_t r_ = (call);                                                            \
+        if (r_ != ncclSuccess)                                                               \
+            throw ::ifgfb200::EngineError(::ifgfb200::kNcclError,                            \
+                                          std::string(#call) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
 
 namespace {
 
@@ -85,6 +94,8 @@ struct Engine::Impl {
     const Surface* surf = nullptr;
     const PairList* pairs = nullptr;
     const BoxTree* tree = nullptr;
+    const BoxRelations* rel = nullptr;
+    const ConePlanHost* cones = nullptr;
 
     // points (Morton order)
     DevBuf px, py, pz, pnx, pny, pnz, jw_p, ones_p, perm, pos, patch_p, identity;
@@ -161,12 +172,22 @@ struct Engine::Impl {
         launch_weights(int(n), perm.as<std::uint32_t>(), phi, jw_p.as<double>(), a_p.as<double2>(), st);
         ++launches;
         launches += run_ifgf(true, true, strategy);
+        if (world > 1) reduce_far_to_owners();  // far-field partials -> target owners
         launch_near_field(near, P, a_p.as<double2>(), k, Sp.as<double2>(), Dp.as<double2>(), st);
         ++launches;
         launch_density_coeffs(rp, phi, coeffs.as<double2>(), st);
-        launch_rp_combine(rp, coeffs.as<double2>(), phi, Sp.as<double2>(), Dp.as<double2>(), gamma,
-                          out, S, D, st);
+        RpDev r = rp;
+        if (world > 1) {  // owned targets in Morton order, then exchanged
+            r.out_m = out_m.as<double2>();
+            S = D = nullptr;
+        }
+        launch_rp_combine(r, coeffs.as<double2>(), phi, Sp.as<double2>(), Dp.as<double2>(), gamma, out, S, D, st);
         launches += 2;
+        if (world > 1) {
+            gather_out_from_owners();
+            launch_unpermute1(int(n), perm.as<std::uint32_t>(), out_m.as<double2>(), out, st);
+            ++launches;
+        }
         return launches;
     }
 
@@ -174,7 +195,82 @@ struct Engine::Impl {
         if (!beta_ready) throw InternalError("beta tables not computed");
     }
 
+    // ---- multi-GPU: source ownership by Morton ranges of leaf boxes
+    std::uint32_t own_lo = 0, own_hi = 0;
+    std::vector<DevBuf> active;  // per level, uint8 per box
+    int rank = 0, world = 1;
+    std::vector<std::uint32_t> bounds;  // world + 1 Morton boundaries
+    ncclComm_t comm = nullptr;
+    DevBuf out_m;
+
+    void drop_graph() {
+        if (graph) cudaGraphExecDestroy(graph);
+        graph = nullptr;
+        eager_done = false;
+    }
+
+    // Morton range [lo, hi) of sources (and targets) owned by this engine; leaf-box aligned
+    void set_partition(std::uint32_t lo, std::uint32_t hi) {
+        if (lo > hi || hi > n) throw InvalidArgument("partition: bad Morton range");
+        own_lo = lo;
+        own_hi = hi;
+        const bool all = lo == 0 && hi == n;
+        active.resize(depth);
+        for (int d = 3; d <= depth; ++d) {
+            const BoxLevel& B = tree->level[d - 1];
+            std::vector<std::uint8_t> a(B.size());
+            for (std::size_t b = 0; b < B.size(); ++b) a[b] = (B.begin[b] < hi && B.end[b] > lo) ? 1 : 0;
+            active[d - 1].upload(a);
+            L[d - 1].active = all ? nullptr : active[d - 1].as<std::uint8_t>();
+        }
+        const BoxLevel& leaves = tree->level[depth - 1];
+        for (std::size_t b = 0; b < leaves.size(); ++b)
+            if ((leaves.begin[b] < lo && leaves.end[b] > lo) || (leaves.begin[b] < hi && leaves.end[b] > hi))
+                throw InvalidArgument("partition: range splits a leaf box");
+        if (depth < 3) {  // leaf activity for the near field
+            std::vector<std::uint8_t> a(leaves.size());
+            for (std::size_t b = 0; b < leaves.size(); ++b) a[b] = (leaves.begin[b] < hi && leaves.end[b] > lo) ? 1 : 0;
+            active.resize(depth);
+            active[depth - 1].upload(a);
+        }
+        near.leaf_active = all ? nullptr : active[depth - 1].as<std::uint8_t>();
+        rp.own_lo = all ? 0u : lo;
+        rp.own_hi = all ? 0xffffffffu : hi;
+        drop_graph();
+    }
+
+    std::vector<std::uint32_t> partition(int parts) const { return partition_sources(*tree, *rel, *cones, parts); }
+
+    void reduce_far_to_owners() {
+        IFGF_NCCL(ncclGroupStart());
+        for (int r = 0; r < world; ++r) {
+            const std::size_t off = bounds[r], cnt = 2 * std::size_t(bounds[r + 1] - bounds[r]);
+            if (!cnt) continue;
+            double* s = reinterpret_cast<double*>(Sp.as<double2>() + off);
+            double* d = reinterpret_cast<double*>(Dp.as<double2>() + off);
+            IFGF_NCCL(ncclReduce(s, s, cnt, ncclFloat64, ncclSum, r, comm, st));
+            IFGF_NCCL(ncclReduce(d, d, cnt, ncclFloat64, ncclSum, r, comm, st));
+        }
+        IFGF_NCCL(ncclGroupEnd());
+    }
+
+    void gather_out_from_owners() {
+        IFGF_NCCL(ncclGroupStart());
+        for (int r = 0; r < world; ++r) {
+            const std::size_t off = bounds[r], cnt = 2 * std::size_t(bounds[r + 1] - bounds[r]);
+            if (!cnt) continue;
+            double* o = reinterpret_cast<double*>(out_m.as<double2>() + off);
+            IFGF_NCCL(ncclBroadcast(o, o, cnt, ncclFloat64, r, comm, st));
+        }
+        IFGF_NCCL(ncclGroupEnd());
+    }
+
     void apply_graph() {
+        if (world > 1) {  // collectives in flight: eager launches
+            kernels = run_apply(d_phi.as<double2>(), d_out.as<double2>(), d_S.as<double2>(), d_D.as<double2>());
+            eager_done = true;
+            return;
+        }
         if (!eager_done) {
             kernels = run_apply(d_phi.as<double2>(), d_out.as<double2>(), d_S.as<double2>(),
                                 d_D.as<double2>());
@@ -205,6 +301,8 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
     e.surf = s.surf;
     e.pairs = s.pairs;
     e.tree = s.tree;
+    e.rel = s.rel;
+    e.cones = s.plan;
     e.n = S.size();
     e.depth = T.depth;
     e.k = s.k;
@@ -533,7 +631,10 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
                 e.ony.as<double>(), e.onz.as<double>(), e.ojw.as<double>(), e.opatch.as<std::int32_t>(),
                 e.tpb.as<std::uint32_t>(), e.pair_patch.as<std::int32_t>()};
     const std::size_t vb = std::max<std::size_t>(n, 1) * sizeof(double2);
-    for (DevBuf* b : {&e.d_phi, &e.d_out, &e.d_S, &e.d_D, &e.a_p, &e.Sp, &e.Dp, &e.scratch}) b->alloc(vb);
+    for (DevBuf* b : {&e.d_phi, &e.d_out, &e.d_S, &e.d_D, &e.a_p, &e.Sp, &e.Dp, &e.scratch, &e.out_m}) b->alloc(vb);
+    e.own_lo = 0;
+    e.own_hi = std::uint32_t(n);
+    e.bounds = {0u, std::uint32_t(n)};
     IFGF_CUDA(cudaDeviceSynchronize());
 }
 
@@ -541,6 +642,7 @@ Engine::~Engine() {
     if (d_) {
         cudaSetDevice(d_->dev);
         if (d_->graph) cudaGraphExecDestroy(d_->graph);
+        if (d_->comm) ncclCommDestroy(d_->comm);
         if (d_->st) cudaStreamDestroy(d_->st);
     }
 }
@@ -629,6 +731,8 @@ void Engine::apply(const cplx* phi, cplx* out, cplx* S, cplx* D) {
     Impl& e = *d_;
     std::lock_guard<std::mutex> g(e.mu);
     e.ensure_beta();
+    if (e.world > 1 && (S || D))
+        throw InvalidArgument("layer_potentials: S and D are target-distributed under a communicator");
     IFGF_CUDA(cudaSetDevice(e.dev));
     const std::size_t bytes = e.n * sizeof(double2);
     IFGF_CUDA(cudaMemcpyAsync(e.d_phi.as<void>(), phi, bytes, cudaMemcpyHostToDevice, e.st));
@@ -838,6 +942,61 @@ std::string Engine::describe() const {
     os << "N=" << e.n << " depth=" << e.depth << " store_elems=" << e.store_elems
        << " beta_entries=" << e.beta_entries << " pairs=" << e.pairs->size();
     return os.str();
+}
+
+std::vector<std::uint32_t> Engine::partition_bounds(int parts) const {
+    if (parts < 1) throw InvalidArgument("partition: need at least one part");
+    return d_->partition(parts);
+}
+
+void Engine::set_partition(std::uint32_t lo, std::uint32_t hi) {
+    Impl& e = *d_;
+    std::lock_guard<std::mutex> g(e.mu);
+    IFGF_CUDA(cudaSetDevice(e.dev));
+    e.set_partition(lo, hi);
+}
+
+void Engine::set_comm(int rank, int world, const void* unique_id) {
+    Impl& e = *d_;
+    std::lock_guard<std::mutex> g(e.mu);
+    if (world < 1 || rank < 0 || rank >= world) throw InvalidArgument("set_comm: bad rank/world");
+    IFGF_CUDA(cudaSetDevice(e.dev));
+    if (e.comm) {
+        ncclCommDestroy(e.comm);
+        e.comm = nullptr;
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, sizeof id);
+    IFGF_NCCL(ncclCommInitRank(&e.comm, world, id, rank));
+    e.rank = rank;
+    e.world = world;
+    e.bounds = e.partition(world);
+    e.set_partition(e.bounds[rank], e.bounds[rank + 1]);
+}
+
+void Engine::finish_owned(const cplx* phi, const cplx* far_S, const cplx* far_D, cplx* out) {
+    Impl& e = *d_;
+    std::lock_guard<std::mutex> g(e.mu);
+    e.ensure_beta();
+    IFGF_CUDA(cudaSetDevice(e.dev));
+    const std::size_t bytes = e.n * sizeof(double2);
+    IFGF_CUDA(cudaMemcpyAsync(e.d_phi.as<void>(), phi, bytes, cudaMemcpyHostToDevice, e.st));
+    IFGF_CUDA(cudaMemcpyAsync(e.d_S.as<void>(), far_S, bytes, cudaMemcpyHostToDevice, e.st));
+    IFGF_CUDA(cudaMemcpyAsync(e.d_D.as<void>(), far_D, bytes, cudaMemcpyHostToDevice, e.st));
+    // far field into Morton order, weighted sources, then the target-owned stages
+    launch_weights(int(e.n), e.perm.as<std::uint32_t>(), e.d_S.as<double2>(), e.ones_p.as<double>(),
+                   e.Sp.as<double2>(), e.st);
+    launch_weights(int(e.n), e.perm.as<std::uint32_t>(), e.d_D.as<double2>(), e.ones_p.as<double>(),
+                   e.Dp.as<double2>(), e.st);
+    launch_weights(int(e.n), e.perm.as<std::uint32_t>(), e.d_phi.as<double2>(), e.jw_p.as<double>(),
+                   e.a_p.as<double2>(), e.st);
+    launch_near_field(e.near, e.P, e.a_p.as<double2>(), e.k, e.Sp.as<double2>(), e.Dp.as<double2>(), e.st);
+    launch_density_coeffs(e.rp, e.d_phi.as<double2>(), e.coeffs.as<double2>(), e.st);
+    IFGF_CUDA(cudaMemsetAsync(e.scratch.as<void>(), 0, bytes, e.st));
+    launch_rp_combine(e.rp, e.coeffs.as<double2>(), e.d_phi.as<double2>(), e.Sp.as<double2>(), e.Dp.as<double2>(),
+                      e.gamma, e.scratch.as<double2>(), nullptr, nullptr, e.st);
+    IFGF_CUDA(cudaMemcpyAsync(out, e.scratch.as<void>(), bytes, cudaMemcpyDeviceToHost, e.st));
+    IFGF_CUDA(cudaStreamSynchronize(e.st));
 }
 
 void* Engine::device_phi() { return d_->d_phi.as<void>(); }

@@ -38,7 +38,7 @@ leaf_fill_kernel(LevelDev L, PointsDev P, const double2* __restrict__ a_p, doubl
     extern __shared__ double smem[];
     const int b = blockIdx.x;
     const int s0 = L.box_seg_begin[b], s1 = L.box_seg_begin[b + 1];
-    if (s0 == s1) return;
+    if (s0 == s1 || (L.active && !L.active[b])) return;
     const int ps = L.ps, pa = L.pang;
     const int NPTS = ps * pa * pa;
     const int G = max(1, int(blockDim.x) / NPTS);
@@ -181,6 +181,7 @@ cousin_kernel(LevelDev L, PointsDev P, const double2* __restrict__ store, double
     double ts[PS > 0 ? PS : kMaxOrd], tt[PA > 0 ? PA : kMaxOrd], tp[PA > 0 ? PA : kMaxOrd];
     for (int j = j0; j < j1; ++j) {
         const int sb = L.cz_idx[j];
+        if (L.active && !L.active[sb]) continue;  // source box owned by another rank
         const int so = act ? L.cev_seg[ev0 + std::int64_t(j - j0) * n_t] : -1;
         const double vx = x - L.cx[sb], vy = y - L.cy[sb], vz = z - L.cz[sb];
         const double r2 = fma(vx, vx, fma(vy, vy, vz * vz));
@@ -275,7 +276,7 @@ parent_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, doub
 #pragma unroll
         for (int i = 0; i < NPP; ++i) acc[i] = make_double2(0.0, 0.0);
         for (int c = 0; c < nch_warp; ++c) {
-            const bool live = c < nch;
+            const bool live = c < nch && (!Lc.active || Lc.active[Lp.ch_idx[c0 + c]]);
             const int ch = live ? Lp.ch_idx[c0 + c] : 0;
             const int cso = live ? Lc.pev_seg[ev + c] : -1;
             const double ccx = Lc.cx[ch], ccy = Lc.cy[ch], ccz = Lc.cz[ch];

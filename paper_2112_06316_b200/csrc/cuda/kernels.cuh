@@ -48,6 +48,7 @@ struct NearDev {
     const std::uint32_t* far_pos = nullptr;   // far nodes as Morton positions
     const std::int32_t *chunk_box = nullptr, *chunk_q0 = nullptr;
     int nchunk = 0;
+    const std::uint8_t* leaf_active = nullptr;  // owned target leaves (null = all)
 };
 void launch_weights(int n, const std::uint32_t* perm, const double2* phi, const double* jw_p,
                     double2* a_p, cudaStream_t st);
@@ -70,7 +71,11 @@ struct RpDev {
     const double2 *beta_s = nullptr, *beta_d = nullptr;
     const std::uint32_t* pos = nullptr;          // original -> Morton
     int max_nn = 0;
+    std::uint32_t own_lo = 0, own_hi = 0xffffffffu;  // owned Morton target range
+    double2* out_m = nullptr;                     // if set: out written in Morton order
 };
+// out[perm[t]] = out_m[t]
+void launch_unpermute1(int n, const std::uint32_t* perm, const double2* in_m, double2* out, cudaStream_t st);
 void launch_density_coeffs(const RpDev& R, const double2* phi, double2* coeffs, cudaStream_t st);
 // out[l] = 1/2 phi + (D_far+near+rp) - i gamma (S_far+near+rp); S/D written when non-null
 void launch_rp_combine(const RpDev& R, const double2* coeffs, const double2* phi,

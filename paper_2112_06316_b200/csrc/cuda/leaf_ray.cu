@@ -36,7 +36,7 @@ leaf_ray_kernel(LevelDev L, PointsDev P, const double2* __restrict__ a_p, double
     extern __shared__ double smem[];
     const int b = blockIdx.x;
     const int s0 = L.box_seg_begin[b], s1 = L.box_seg_begin[b + 1];
-    if (s0 == s1) return;
+    if (s0 == s1 || (L.active && !L.active[b])) return;
     const int pa = L.pang;
     const int NRAY = pa * pa;
     const int NPTS = kPS * NRAY;

@@ -30,6 +30,13 @@ __global__ void weights_kernel(int n, const std::uint32_t* __restrict__ perm,
     a_p[t] = cscale(phi[perm[t]], jw_p[t]);
 }
 
+__global__ void unpermute1_kernel(int n, const std::uint32_t* __restrict__ perm, const double2* __restrict__ in_m,
+                                  double2* __restrict__ out) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    out[perm[t]] = in_m[t];
+}
+
 __global__ void unpermute_kernel(int n, const std::uint32_t* __restrict__ perm,
                                  const double2* __restrict__ Sp, const double2* __restrict__ Dp,
                                  double2* __restrict__ S, double2* __restrict__ D) {
@@ -68,6 +75,7 @@ near_kernel(NearDev N, PointsDev P, const double2* __restrict__ a_p, double k,
             double2* __restrict__ Sp, double2* __restrict__ Dp) {
     const int c = blockIdx.x;
     const int tb = N.chunk_box[c];
+    if (N.leaf_active && !N.leaf_active[tb]) return;  // targets owned by another rank
     const int tbeg = int(N.beg[tb]);
     const int n_t = int(N.end[tb]) - tbeg;
     const int q = N.chunk_q0[c] + threadIdx.x;
@@ -143,6 +151,8 @@ __global__ void rp_combine_kernel(RpDev R, const double2* __restrict__ coeffs,
     const int lane = threadIdx.x & 31;
     if (warp >= R.n) return;
     const int l = warp;
+    const std::uint32_t tm = R.pos[l];
+    if (tm < R.own_lo || tm >= R.own_hi) return;  // target owned by another rank
     double2 as = make_double2(0.0, 0.0), ad = make_double2(0.0, 0.0);
     for (std::uint32_t p = R.tpb[l]; p < R.tpb[l + 1]; ++p) {
         const int q = R.pair_patch[p];
@@ -168,7 +178,9 @@ __global__ void rp_combine_kernel(RpDev R, const double2* __restrict__ coeffs,
     const double2 s = cadd(Sp[t], as);
     const double2 d = cadd(Dp[t], ad);
     const double2 f = phi[l];
-    out[l] = make_double2(0.5 * f.x + d.x + gamma * s.y, 0.5 * f.y + d.y - gamma * s.x);
+    const double2 o = make_double2(0.5 * f.x + d.x + gamma * s.y, 0.5 * f.y + d.y - gamma * s.x);
+    if (R.out_m) R.out_m[t] = o;
+    else out[l] = o;
     if (S) S[l] = s;
     if (D) D[l] = d;
 }
@@ -243,6 +255,12 @@ void launch_unpermute(int n, const std::uint32_t* perm, const double2* Sp, const
                       double2* S, double2* D, cudaStream_t st) {
     if (n == 0) return;
     unpermute_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, perm, Sp, Dp, S, D);
+    IFGF_CUDA(cudaGetLastError());
+}
+
+void launch_unpermute1(int n, const std::uint32_t* perm, const double2* in_m, double2* out, cudaStream_t st) {
+    if (n == 0) return;
+    unpermute1_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, perm, in_m, out);
     IFGF_CUDA(cudaGetLastError());
 }
 

@@ -95,6 +95,7 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
     for (int e = lane; e < kNP * NPP; e += 32) acc[e] = make_double2(0.0, 0.0);
 
     const int pb = Lp.seg_box[so];
+    if (Lp.active && !Lp.active[pb]) return;  // no sources of this rank below
     const int gam = Lp.seg_gamma[so];
     const int g1 = gam % Lp.ns, g2 = (gam / Lp.ns) % Lp.nc, g3 = gam / Lp.ns / Lp.nc;
     const int c0 = Lp.ch_ptr[pb];
@@ -113,6 +114,7 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
         // 1. geometry of the group's evaluations (one child box and one child cell per group)
         const int c_grp = Lc.pev_perm[ev0 + start] >> 8;
         const int ch = Lp.ch_idx[c0 + c_grp];
+        if (Lc.active && !Lc.active[ch]) continue;  // child holds no sources of this rank
         const double ccx = Lc.cx[ch], ccy = Lc.cy[ch], ccz = Lc.cz[ch];
         const CellFrame cf = cell_frame(Lc.seg_gamma[cso], Lc);
         for (int i = lane; i < count; i += 32) {

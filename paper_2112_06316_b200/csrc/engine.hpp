@@ -61,6 +61,18 @@ class Engine {
     // RP correction alone (rp.cpp:421-451), outputs overwritten
     void rp_apply(const cplx* phi, cplx* S, cplx* D);
 
+    // ---- multi-GPU: each engine owns the sources and targets of a
+    // leaf-aligned Morton range; the far field is computed from owned sources for all
+    // targets and reduced to the target owners, near field + RP run target-owned.
+    // cost-balanced boundaries (parts + 1 Morton indices)
+    std::vector<std::uint32_t> partition_bounds(int parts) const;
+    void set_partition(std::uint32_t lo, std::uint32_t hi);
+    // NCCL communicator from a 128-byte ncclUniqueId; sets the partition of `rank`
+    void set_comm(int rank, int world, const void* unique_id);
+    // near field + RP + combine for the owned targets only, given the full far field
+    // (original order); out is zero outside the owned targets
+    void finish_owned(const cplx* phi, const cplx* far_S, const cplx* far_D, cplx* out);
+
     // benchmark helpers: graph replays with device-resident phi (no host copies)
     void upload_density(const cplx* phi);
     double time_device_applies(int iters, bool flush_l2);   // mean ms per apply

@@ -330,6 +330,46 @@ ConePlanHost build_cone_plan(const BoxTree& t, const BoxRelations& rel,
     return plan;
 }
 
+// cost-balanced leaf-aligned boundaries: per leaf box, near pairs + leaf-fill
+// interactions + cousin evaluations (as source box) weighted by their flop counts
+std::vector<std::uint32_t> partition_sources(const BoxTree& t, const BoxRelations& rel, const ConePlanHost& plan,
+                                             int parts) {
+    if (parts < 1) throw InvalidArgument("partition: need at least one part");
+    const std::size_t n = t.perm.size();
+    const int D = t.depth;
+    const BoxLevel& leaves = t.level[D - 1];
+    const std::size_t nb = leaves.size();
+    std::vector<double> cost(nb, 0.0);
+    const Adjacency& nbr = rel.nbr[D - 1];
+    for (std::size_t b = 0; b < nb; ++b) {
+        const double np = double(leaves.end[b] - leaves.begin[b]);
+        double nn = 0;
+        for (int j = nbr.ptr[b]; j < nbr.ptr[b + 1]; ++j) nn += leaves.end[nbr.idx[j]] - leaves.begin[nbr.idx[j]];
+        cost[b] = 47.0 * np * nn;
+        if (D >= 3) {
+            const ConeLevel& CL = plan.level[D - 1];
+            cost[b] += 47.0 * 75.0 * np * double(CL.box_seg_begin[b + 1] - CL.box_seg_begin[b]);
+            const Adjacency& cz = rel.cousin[D - 1];
+            double ce = 0;
+            for (int j = cz.ptr[b]; j < cz.ptr[b + 1]; ++j) ce += leaves.end[cz.idx[j]] - leaves.begin[cz.idx[j]];
+            cost[b] += 1358.0 * ce + 1400.0 * 75.0 * double(CL.box_seg_begin[b + 1] - CL.box_seg_begin[b]);
+        }
+    }
+    double total = 0;
+    for (double c : cost) total += c;
+    std::vector<std::uint32_t> out(parts + 1, 0);
+    double acc = 0;
+    int r = 1;
+    for (std::size_t b = 0; b < nb && r < parts; ++b) {
+        acc += cost[b];
+        while (r < parts && acc >= total * r / parts) out[r++] = leaves.end[b];
+    }
+    for (; r < parts; ++r) out[r] = std::uint32_t(n);
+    out[parts] = std::uint32_t(n);
+    return out;
+}
+
+
 std::string plan_diagnostics(const BoxTree& t, const ConePlanHost& plan) {
     std::ostringstream os;
     os << "levels " << t.depth << "\n";

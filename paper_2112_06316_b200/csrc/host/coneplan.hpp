@@ -71,6 +71,12 @@ ConePlanHost build_cone_plan(const BoxTree& t, const BoxRelations& rel,
                              const std::vector<Vec3>& pts_morton, const ConeParams& p,
                              int workers);
 
+// Cost-balanced, leaf-aligned Morton boundaries (parts + 1) of the multi-GPU source/target
+// ownership: per leaf box, near pairs, leaf-fill interactions and cousin
+// and parent evaluations weighted by their flops
+std::vector<std::uint32_t> partition_sources(const BoxTree& t, const BoxRelations& rel, const ConePlanHost& plan,
+                                             int parts);
+
 // textual per-level counts, the reference's ConePlan::diagnostics (ifgf.cpp:298-310)
 std::string plan_diagnostics(const BoxTree& t, const ConePlanHost& plan);
 

@@ -86,6 +86,13 @@ def _cvec(v, n=None):
     return v
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId for set_comm (rank 0 creates it, the others receive it)"""
+    buf = C.create_string_buffer(128)
+    check(lib().ifgf_nccl_unique_id(buf), "nccl_unique_id")
+    return buf.raw
+
+
 def random_density(n: int, seed: int) -> np.ndarray:
     """U(-1,1) + i U(-1,1) from std::mt19937_64(seed), in the reference harness's draw order."""
     out = np.zeros(n, dtype=np.complex128)
@@ -397,6 +404,26 @@ class CombinedOperator:
 
     def kernels_per_apply(self) -> int:
         return int(lib().ifgf_operator_kernels_per_apply(self._h))
+
+    # ---- multi-GPU
+    def partition(self, parts: int) -> np.ndarray:
+        """cost-balanced, leaf-aligned Morton boundaries (parts + 1)"""
+        b = np.zeros(parts + 1, dtype=np.uint32)
+        check(lib().ifgf_operator_partition(self._h, parts, _ptr(b, u32_p)), "partition")
+        return b
+
+    def set_partition(self, lo: int, hi: int):
+        check(lib().ifgf_operator_set_partition(self._h, int(lo), int(hi)), "set_partition")
+
+    def set_comm(self, rank: int, world: int, unique_id: bytes):
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        check(lib().ifgf_operator_set_comm(self._h, rank, world, buf), "set_comm")
+
+    def finish_owned(self, density, far_S, far_D) -> np.ndarray:
+        phi, fs, fd = _cvec(density, self.n), _cvec(far_S, self.n), _cvec(far_D, self.n)
+        out = np.zeros(self.n, dtype=np.complex128)
+        check(lib().ifgf_operator_finish_owned(self._h, _ptr(phi), _ptr(fs), _ptr(fd), _ptr(out)), "finish_owned")
+        return out
 
     def work(self) -> dict:
         """Algorithmic work of one apply (counts, flops, HBM bytes per phase)."""
