@@ -287,7 +287,7 @@ def run_b200(args, ws, rank, local):
                    "density": "U(-1,1)+iU(-1,1), mt19937_64 seed 1",
                    "parallelism": f"morton-partitioned x{ws} (NCCL reduce/broadcast)" if ws > 1 else "single",
                    "l2": "no flush: each apply streams the plan + beta tables (>> 126 MB L2)"},
-        "setup_s": setup_s, "wall_s_timed": t_wall, "clocks": clocks,
+        "setup_s": setup_s, "setup_breakdown_s": op.setup_times(), "wall_s_timed": t_wall, "clocks": clocks,
         "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": 16 * n,
                 "d2h_bytes_per_step": 16 * n, "ms_per_step": 1e3 * t_e2e / args.steps},
         "gpu_launches": args.steps * op.kernels_per_apply(), "kernels_per_apply": op.kernels_per_apply(),

@@ -130,6 +130,8 @@ int ifgf_operator_create(const ifgf_surface* s, const ifgf_config* cfg, ifgf_ope
 int ifgf_operator_from_plan(ifgf_plan* p, int device, int compute_beta, ifgf_operator** out);
 void ifgf_operator_free(ifgf_operator* op);
 int64_t ifgf_operator_size(const ifgf_operator* op);
+/* setup phases in seconds: {octree+relations, cone plan, proximity, HBM upload, GPU beta} */
+int ifgf_operator_setup_times(const ifgf_operator* op, double* t5);
 double ifgf_operator_gamma(const ifgf_operator* op);
 int ifgf_operator_apply(ifgf_operator* op, const double* phi, double* out);
 int ifgf_operator_layer_potentials(ifgf_operator* op, const double* phi, double* S, double* D);

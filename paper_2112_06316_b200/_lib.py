@@ -82,6 +82,7 @@ _SIGS = {
     "ifgf_operator_free": (None, [vp]),
     "ifgf_operator_size": (C.c_int64, [vp]),
     "ifgf_operator_gamma": (C.c_double, [vp]),
+    "ifgf_operator_setup_times": (C.c_int, [vp, d_p]),
     "ifgf_operator_apply": (C.c_int, [vp, d_p, d_p]),
     "ifgf_operator_layer_potentials": (C.c_int, [vp, d_p, d_p, d_p]),
     "ifgf_operator_apply_device": (C.c_int, [vp, vp, vp]),

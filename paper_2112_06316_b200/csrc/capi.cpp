@@ -47,9 +47,11 @@ struct ifgf_plan {
     ConePlanHost cones;
     PairList pairs;
     double setup_seconds = 0;
+    double t_tree = 0, t_cones = 0, t_pairs = 0;  // host setup phases (s)
 };
 
 struct ifgf_operator {
+    double t_upload = 0, t_beta = 0;  // device setup phases (s)
     std::shared_ptr<ifgf_plan> plan;
     std::unique_ptr<Engine> eng;
 };
@@ -100,8 +102,15 @@ std::shared_ptr<ifgf_plan> make_plan(std::shared_ptr<const Surface> s, const ifg
         p->gamma = std::max(3.0, diam / lambda);
     }
     const auto t0 = std::chrono::steady_clock::now();
+    auto lap = [t = std::chrono::steady_clock::now()]() mutable {
+        const auto now = std::chrono::steady_clock::now();
+        const double dt = std::chrono::duration<double>(now - t).count();
+        t = now;
+        return dt;
+    };
     p->tree = build_boxtree(s->pos, c.k, c.finest_box_lambda);
     p->rel = build_relations(p->tree);
+    p->t_tree = lap();
     std::vector<Vec3> pts(s->size());
     for (std::size_t t = 0; t < pts.size(); ++t) pts[t] = s->pos[p->tree.perm[t]];
     ConeParams cp;
@@ -110,12 +119,14 @@ std::shared_ptr<ifgf_plan> make_plan(std::shared_ptr<const Surface> s, const ifg
     cp.ps = c.ps;
     cp.pang = c.pang;
     p->cones = build_cone_plan(p->tree, p->rel, pts, cp, c.workers);
+    p->t_cones = lap();
     RpParams rp;
     rp.delta_rel = c.delta_rel;
     rp.delta_abs = c.delta_abs;
     rp.n_beta = c.n_beta;
     rp.cov_d = c.cov_d;
     p->pairs = classify_pairs(*s, p->tree, p->rel, rp, c.workers);
+    p->t_pairs = lap();
     p->strategy = c.strategy == 0 ? DlStrategy::W4 : (c.strategy == 1 ? DlStrategy::W2W3 : DlStrategy::Hybrid);
     if (p->strategy == DlStrategy::Hybrid) {  // solver.cpp:55-62
         bool any_sub = false;
@@ -579,8 +590,12 @@ int ifgf_operator_create(const ifgf_surface* s, const ifgf_config* cfg, ifgf_ope
         need(out, "out");
         auto op = std::make_unique<ifgf_operator>();
         op->plan = make_plan(s->s, *cfg);
+        const auto t0 = std::chrono::steady_clock::now();
         op->eng = make_engine(*op->plan, cfg->device);
+        const auto t1 = std::chrono::steady_clock::now();
         op->eng->compute_beta();
+        op->t_upload = std::chrono::duration<double>(t1 - t0).count();
+        op->t_beta = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
         *out = op.release();
     });
 }
@@ -817,6 +832,16 @@ int ifgf_operator_time_phases(ifgf_operator* op, double* ms7) {
 int ifgf_operator_kernels_per_apply(const ifgf_operator* op) { return op ? op->eng->kernels_per_apply() : -1; }
 void* ifgf_operator_device_phi(ifgf_operator* op) { return op ? op->eng->device_phi() : nullptr; }
 void* ifgf_operator_device_out(ifgf_operator* op) { return op ? op->eng->device_out() : nullptr; }
+
+// {octree+relations, cone plan, proximity, HBM upload, GPU beta tables} seconds
+int ifgf_operator_setup_times(const ifgf_operator* op, double* t5) {
+    return guarded([&] {
+        need(op, "operator");
+        need(t5, "t5");
+        const double v[5] = {op->plan->t_tree, op->plan->t_cones, op->plan->t_pairs, op->t_upload, op->t_beta};
+        std::memcpy(t5, v, sizeof v);
+    });
+}
 
 // ------------------------------------------------------------------ multi-GPU
 int ifgf_nccl_unique_id(void* id128) {

@@ -402,7 +402,9 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         b.seg_gamma.upload(CL.seg_gamma);
         b.box_seg_begin.upload(CL.box_seg_begin);
         b.pev_begin.upload(CL.pev_begin);
-        b.pev_seg.upload(CL.pev_seg);
+        // per-evaluation child ordinals are only read by the generic-order parent kernel;
+        // the tensor-core kernel (ps = 3, pang = 5) works from the grouped permutation
+        if (!(CL.ps == 3 && CL.pang == 5)) b.pev_seg.upload(CL.pev_seg);
         b.pev_perm.upload(CL.pev_perm);
         b.pgrp_begin.upload(CL.pgrp_begin);
         b.pgrp_seg.upload(CL.pgrp_seg);

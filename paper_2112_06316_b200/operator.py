@@ -405,6 +405,11 @@ class CombinedOperator:
     def kernels_per_apply(self) -> int:
         return int(lib().ifgf_operator_kernels_per_apply(self._h))
 
+    def setup_times(self) -> dict:
+        v = np.zeros(5)
+        check(lib().ifgf_operator_setup_times(self._h, _ptr(v)), "setup_times")
+        return dict(zip(["tree", "cone_plan", "proximity", "upload", "beta"], v.tolist()))
+
     # ---- multi-GPU
     def partition(self, parts: int) -> np.ndarray:
         """cost-balanced, leaf-aligned Morton boundaries (parts + 1)"""
