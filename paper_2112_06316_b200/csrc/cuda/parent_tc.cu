@@ -1,21 +1,23 @@
 // Parent fill (ifgf.cpp:452-568) on the FP64 tensor cores, for the default interpolation
 // orders (ps = 3, pang = 5).
 //
-// One CTA (4 warps) per parent segment. Each warp takes the host's child-segment groups
+// One warp per parent segment (4 per CTA). The warp takes the host's child-segment groups
 // of that segment in turn (all parent-node evaluations that land in one child cone
-// segment, ifgf/coneplan.cpp group_parent_evaluations):
+// segment, csrc/host/coneplan.cpp group_parent_evaluations):
 //   1. the warp's lanes compute, for the group's evaluations, the child-frame local
 //      coordinates and the re-centring factors (node directions from sin/cos tables);
-//   2. tiles of 8 evaluations contract the child's 3x5x5 coefficient block against the
-//      evaluations' basis products with mma.sync.m8n8k4.f64 (DMMA): A = basis products
-//      (rows = evaluations, k = the s index padded 3 -> 4), B = coefficients (columns =
-//      pipe x {re, im}), 25 k-steps over the (theta, phi) indices — every coefficient is
-//      fetched once per warp instead of once per lane;
-//   3. the epilogue applies the re-centring factor and adds into the warp's private
-//      node accumulators (no atomics).
-// A fixed-order sum over the 4 warps and the separable block transform finish the segment.
-// Results equal the per-lane kernel to rounding (~1e-16); the evaluation order is fixed,
-// so the output is bitwise reproducible.
+//   2. tiles of 8 evaluations contract the child's 3x5x5 coefficient block with
+//      mma.sync.m8n8k4.f64 (DMMA): A = T_s(s) T_t(theta) (rows = evaluations, k = the s
+//      index padded 3 -> 4), B = coefficients with columns = (phi sub-index, pipe, re/im):
+//      the 8 columns hold 4 / pipes phi indices at once, so a tile takes 5 x ceil(5 /
+//      (4 / pipes)) DMMAs (25 for 3 pipes, 15 for 2, 10 for 1), one accumulator per phi
+//      group; B is loaded once per group and reused by all its tiles;
+//   3. the epilogue weights the accumulators by T_p(phi), sums the phi sub-indices across
+//      the quad, applies the re-centring factor and adds into the warp's private node
+//      accumulators (no atomics).
+// The separable block transform (warp-local) finishes the segment. Results equal the
+// per-lane kernel to rounding (~1e-16); the evaluation order is fixed, so the output is
+// bitwise reproducible run to run.
 #include "ifgf_device.cuh"
 #include "kernels.cuh"
 
@@ -104,8 +106,10 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
     const double pcx = Lp.cx[pb], pcy = Lp.cy[pb], pcz = Lp.cz[pb];
 
     const int r = lane >> 2, tig = lane & 3;
-    const int comp = lane >> 2;  // B column: pipe comp >> 1, re/im comp & 1
-    const bool bcol = comp < 2 * NPC && tig < kPS;
+    // B column n = lane >> 2 = 2 NPC sub + 2 pipe + re/im: IPG phi indices share one DMMA
+    constexpr int IPG = 4 / NPC, NIPG = (kPA + IPG - 1) / IPG;
+    const int ncol = lane >> 2, bsub = ncol / (2 * NPC), comp = ncol % (2 * NPC);
+    const bool bcol = bsub < IPG && tig < kPS;
     const int boff = 2 * ((comp >> 1) * kNP + tig) + (comp & 1);
     const int gb = Lc.pgrp_begin[so], ge = Lc.pgrp_begin[so + 1];
     for (int g = gb; g < ge; ++g) {
@@ -150,31 +154,52 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
         // B fragments of the group's block: k = the s index (padded 3 -> 4), 25 k-steps over
         // (theta, phi); loaded once per group, reused by all its tiles
         const double* blk = reinterpret_cast<const double*>(cstore + std::size_t(cso) * NPC * kNP) + boff;
-        double bq[kPA * kPA];
+        double bq[kPA * NIPG];
 #pragma unroll
-        for (int kc = 0; kc < kPA * kPA; ++kc) bq[kc] = bcol ? __ldg(blk + 2 * kPS * kc) : 0.0;
+        for (int q = 0; q < NIPG; ++q)
+#pragma unroll
+            for (int it = 0; it < kPA; ++it) {
+                const int ip = IPG * q + bsub;
+                bq[q * kPA + it] = (bcol && ip < kPA) ? __ldg(blk + 2 * kPS * (it + kPA * ip)) : 0.0;
+            }
         for (int t0 = 0; t0 < count; t0 += 8) {
             const bool valid = t0 + r < count;
             const double* gp = geo + (valid ? t0 + r : 0) * kGeo;
             const double ls = gp[0];
             double ts = tig == 0 ? 1.0 : (tig == 1 ? ls : (tig == 2 ? 2.0 * ls * ls - 1.0 : 0.0));
             if (!valid) ts = 0.0;
-            double tt[kPA], tq[kPA];
+            double tt[kPA];
             cheb_row<kPA>(gp[1], tt);
-            cheb_row<kPA>(gp[2], tq);
-            double d0 = 0.0, d1 = 0.0, f0 = 0.0, f1 = 0.0;
+            double d[NIPG][2];
 #pragma unroll
-            for (int ip = 0; ip < kPA; ++ip) {
-                const double tsp = ts * tq[ip];
+            for (int q = 0; q < NIPG; ++q) d[q][0] = d[q][1] = 0.0;
 #pragma unroll
-                for (int it = 0; it < kPA; ++it) {
-                    const int kc = it + kPA * ip;
-                    if (kc & 1) dmma884(f0, f1, tsp * tt[it], bq[kc]);
-                    else dmma884(d0, d1, tsp * tt[it], bq[kc]);
-                }
+            for (int it = 0; it < kPA; ++it) {
+                const double a = ts * tt[it];
+#pragma unroll
+                for (int q = 0; q < NIPG; ++q) dmma884(d[q][0], d[q][1], a, bq[q * kPA + it]);
             }
-            // 3. lane (r, tig) holds (re, im) of child pipe tig for evaluation row r
-            const double2 val = make_double2(d0 + f0, d1 + f1);
+            // 3. lane (r, tig) holds columns 2 tig, 2 tig + 1 = (re, im) of pipe tig % NPC at
+            // phi sub-index tig / NPC: weight by T(phi) and sum the sub-indices over the quad
+            double tq[kPA];
+            cheb_row<kPA>(gp[2], tq);
+            const int sub = tig / NPC;
+            double2 val = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < NIPG; ++q) {
+                double w = 0.0;
+#pragma unroll
+                for (int s = 0; s < IPG; ++s)
+                    if (IPG * q + s < kPA && sub == s) w = tq[IPG * q + s];
+                val.x = fma(w, d[q][0], val.x);
+                val.y = fma(w, d[q][1], val.y);
+            }
+#pragma unroll
+            for (int off = NPC; off < NPC * IPG; off <<= 1) {
+                val.x += __shfl_down_sync(0xffffffffu, val.x, off);
+                val.y += __shfl_down_sync(0xffffffffu, val.y, off);
+            }
+            // lanes tig < NPC now hold (re, im) of child pipe tig for evaluation row r
             const double2 r1 = make_double2(gp[3], gp[4]);
             const double xf = gp[5];
             int fac = R1;
