@@ -203,6 +203,26 @@ def roofline_for(phases, work, pk):
     return out
 
 
+KERNEL_FAMILY = {"leaf": "leaf_ray_kernel", "cousin": "cousin_kernel", "parent": "parent_tc_kernel",
+                 "near": "near_kernel", "rp": "rp_combine_kernel"}
+
+
+def ncu_traffic(cfg_name, phase):
+    """dram__bytes_read.sum + dram__bytes_write.sum per apply of the phase's kernel from the newest
+    committed ncu launch list for this config (profiles/r*_ncu_launches_<cfg>.json, written by
+    tools/ncu_launches.py); None when there is none."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_launches_{cfg_name}.json")))
+    if not files:
+        return None, None
+    try:
+        k = json.load(open(files[-1]))["kernels"].get(KERNEL_FAMILY[phase])
+        return (k["dram_bytes_per_apply"] if k else None), os.path.relpath(files[-1], ROOT)
+    except Exception:
+        return None, None
+
+
 def run_b200(args, ws, rank, local):
     import torch
 
@@ -268,14 +288,21 @@ def run_b200(args, ws, rank, local):
     roofs = roofline_for(phases, work, pk)
     dom = max(roofs, key=lambda p: roofs[p]["ms"])
     r = roofs[dom]
+    traffic, traffic_src = ncu_traffic(args.config, dom)
+    # north_star: HBM GB/s is the stated roofline of the propagation / SpMV kernels and FP64 of
+    # the leaf / near-field kernels; the FP64 pipe is what binds the propagation kernels
+    # (SURVEY.md 8(d)), so both fractions are reported
+    binding = {"bound": "fp64", "achieved": r["fp64_tflops"], "peak": pk["fp64_tflops"], "unit": "TFLOP/s",
+               "frac": r["fp64_frac"], "peak_source": pk["source_fp64"]}
     if r["stated_bound"] == "fp64":
-        roof = {"bound": "fp64", "kernel": dom, "achieved": r["fp64_tflops"], "peak": pk["fp64_tflops"],
-                "unit": "TFLOP/s", "frac": r["fp64_frac"], "traffic": None,
-                "peak_source": pk["source_fp64"]}
+        roof = dict(binding, kernel=dom, traffic=traffic)
     else:
         roof = {"bound": "hbm", "kernel": dom, "achieved": r["hbm_gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": r["hbm_frac"], "traffic": None, "peak_source": pk["source_hbm"],
-                "fp64_frac": r["fp64_frac"]}
+                "frac": r["hbm_frac"], "traffic": traffic, "peak_source": pk["source_hbm"], "binding": binding}
+    roof["algorithmic_bytes"] = r["bytes"]
+    roof["algorithmic_flops"] = r["flops"]
+    roof["per"] = "one apply (all launches of the kernel: one per level)"
+    roof["traffic_source"] = traffic_src
 
     line = {
         "metric": "cf_operator_points_per_s", "value": value, "unit": "points/s",

@@ -89,7 +89,8 @@ __device__ __forceinline__ LocalCoords local_coords_in(double vx, double vy, dou
     const double rho = sqrt(fma(vx, vx, vy * vy));
     const double tn = fma(rho, f.ctc, -vz * f.stc), td = fma(vz, f.ctc, rho * f.stc);
     const double pn = fma(vy, f.cpc, -vx * f.spc), pd = fma(vx, f.cpc, vy * f.spc);
-    const double tt = tn / td, tp = pn / pd;
+    const double inv = 1.0 / (td * pd);  // one division for both tangents
+    const double tt = tn * pd * inv, tp = pn * td * inv;
     if (!(fabs(tt) <= 0.4225 && fabs(tp) <= 0.4225 && td > 0.0 && pd > 0.0))
         return local_coords_lib(vx, vy, vz, inv_r, h, gamma, L);
     LocalCoords o;
@@ -115,7 +116,8 @@ __device__ __forceinline__ LocalCoords local_coords(double vx, double vy, double
     const double cpc = L.phc_cos[g3], spc = L.phc_sin[g3];
     const double tn = fma(rho, ctc, -vz * stc), td = fma(vz, ctc, rho * stc);
     const double pn = fma(vy, cpc, -vx * spc), pd = fma(vx, cpc, vy * spc);
-    const double tt = tn / td, tp = pn / pd;
+    const double inv = 1.0 / (td * pd);  // one division for both tangents
+    const double tt = tn * pd * inv, tp = pn * td * inv;
     if (!(fabs(tt) <= 0.4225 && fabs(tp) <= 0.4225 && td > 0.0 && pd > 0.0))
         return local_coords_lib(vx, vy, vz, inv_r, h, gamma, L);
     LocalCoords o;

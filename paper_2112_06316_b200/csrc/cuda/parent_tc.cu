@@ -7,11 +7,11 @@
 //   1. the warp's lanes compute, for the group's evaluations, the child-frame local
 //      coordinates and the re-centring factors (node directions from sin/cos tables);
 //   2. tiles of 8 evaluations contract the child's 3x5x5 coefficient block with
-//      mma.sync.m8n8k4.f64 (DMMA): A = T_s(s) T_t(theta) (rows = evaluations, k = the s
-//      index padded 3 -> 4), B = coefficients with columns = (phi sub-index, pipe, re/im):
-//      the 8 columns hold 4 / pipes phi indices at once, so a tile takes 5 x ceil(5 /
-//      (4 / pipes)) DMMAs (25 for 3 pipes, 15 for 2, 10 for 1), one accumulator per phi
-//      group; B is loaded once per group and reused by all its tiles;
+//      mma.sync.m8n8k4.f64 (DMMA): A = T_s(s) T_t(theta) (rows = evaluations, k = the 15
+//      (s, theta) index pairs in 4 steps of 4), B = coefficients with columns = (phi
+//      sub-index, pipe, re/im): the 8 columns hold 4 / pipes phi indices at once, so a
+//      tile takes 4 x ceil(5 / (4 / pipes)) DMMAs (20 for 3 pipes, 12 for 2, 8 for 1), one
+//      accumulator per phi group; B is loaded once per group and reused by all its tiles;
 //   3. the epilogue weights the accumulators by T_p(phi), sums the phi sub-indices across
 //      the quad, applies the re-centring factor and adds into the warp's private node
 //      accumulators (no atomics).
@@ -30,6 +30,8 @@ using namespace ifgfdev;
 constexpr int kWarps = 4;
 constexpr int kGeo = 7;  // ls, lt, lp, ratio.re, ratio.im, extra factor, node (odd stride)
 constexpr int kPS = 3, kPA = 5, kNP = 75;
+constexpr int kKS = kPA - 1;  // DMMA k-steps over the 15 (s, theta) pairs (4 x 4 slots)
+static_assert(kPS == 3 && kPA == 5, "the k-slot map below assumes 3 x 5 (s, theta) pairs");
 constexpr int kGeoSz = kNP * kGeo + 1;  // keeps the accumulators 16-byte aligned
 
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
@@ -109,8 +111,8 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
     // B column n = lane >> 2 = 2 NPC sub + 2 pipe + re/im: IPG phi indices share one DMMA
     constexpr int IPG = 4 / NPC, NIPG = (kPA + IPG - 1) / IPG;
     const int ncol = lane >> 2, bsub = ncol / (2 * NPC), comp = ncol % (2 * NPC);
-    const bool bcol = bsub < IPG && tig < kPS;
-    const int boff = 2 * ((comp >> 1) * kNP + tig) + (comp & 1);
+    const bool bcol = bsub < IPG;
+    const int boff = 2 * (comp >> 1) * kNP + (comp & 1);
     const int gb = Lc.pgrp_begin[so], ge = Lc.pgrp_begin[so + 1];
     for (int g = gb; g < ge; ++g) {
         const int cso = Lc.pgrp_seg[g];
@@ -151,33 +153,44 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
         }
         __syncwarp();
         // 2. 8-evaluation tensor-core tiles against the child block
-        // B fragments of the group's block: k = the s index (padded 3 -> 4), 25 k-steps over
-        // (theta, phi); loaded once per group, reused by all its tiles
+        // B fragments of the group's block: k runs over the 15 (s, theta) index pairs in 4
+        // steps of 4: slot (j, tig) holds (is, it) = (tig, j) for tig < 3 and (j, 4) for
+        // tig = 3 (slot (3, 3) is padding); one accumulator per phi group. Loaded once per
+        // group, reused by all its tiles.
         const double* blk = reinterpret_cast<const double*>(cstore + std::size_t(cso) * NPC * kNP) + boff;
-        double bq[kPA * NIPG];
+        const bool lo = tig < kPS;
+        double bq[kKS * NIPG];
 #pragma unroll
         for (int q = 0; q < NIPG; ++q)
 #pragma unroll
-            for (int it = 0; it < kPA; ++it) {
+            for (int j = 0; j < kKS; ++j) {
                 const int ip = IPG * q + bsub;
-                bq[q * kPA + it] = (bcol && ip < kPA) ? __ldg(blk + 2 * kPS * (it + kPA * ip)) : 0.0;
+                const int is = lo ? tig : j, it = lo ? j : kPA - 1;
+                bq[q * kKS + j] = (bcol && ip < kPA && (lo || j < kPS))
+                                      ? __ldg(blk + 2 * (is + kPS * (it + kPA * ip)))
+                                      : 0.0;
             }
         for (int t0 = 0; t0 < count; t0 += 8) {
             const bool valid = t0 + r < count;
             const double* gp = geo + (valid ? t0 + r : 0) * kGeo;
-            const double ls = gp[0];
-            double ts = tig == 0 ? 1.0 : (tig == 1 ? ls : (tig == 2 ? 2.0 * ls * ls - 1.0 : 0.0));
-            if (!valid) ts = 0.0;
-            double tt[kPA];
+            double ts[kPS], tt[kPA];
+            cheb_row<kPS>(gp[0], ts);
             cheb_row<kPA>(gp[1], tt);
+            // lane-constant operand choice: T_tig(s) for the first three k columns, T_4(theta)
+            // for the fourth (zero rows past the group's end)
+            double tsel = tig == 0 ? ts[0] : (tig == 1 ? ts[1] : ts[2]);
+            double t4 = tt[kPA - 1];
+            if (!valid) tsel = t4 = 0.0;
             double d[NIPG][2];
 #pragma unroll
             for (int q = 0; q < NIPG; ++q) d[q][0] = d[q][1] = 0.0;
 #pragma unroll
-            for (int it = 0; it < kPA; ++it) {
-                const double a = ts * tt[it];
+            for (int j = 0; j < kKS; ++j) {
+                const double x = lo ? tsel : (j < kPS ? ts[j] : 0.0);
+                const double y = lo ? tt[j] : t4;
+                const double a = x * y;
 #pragma unroll
-                for (int q = 0; q < NIPG; ++q) dmma884(d[q][0], d[q][1], a, bq[q * kPA + it]);
+                for (int q = 0; q < NIPG; ++q) dmma884(d[q][0], d[q][1], a, bq[q * kKS + j]);
             }
             // 3. lane (r, tig) holds columns 2 tig, 2 tig + 1 = (re, im) of pipe tig % NPC at
             // phi sub-index tig / NPC: weight by T(phi) and sum the sub-indices over the quad
