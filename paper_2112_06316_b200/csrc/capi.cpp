@@ -907,10 +907,9 @@ int ifgf_gmres_solve(ifgf_operator* op, const double* rhs, double tol, int max_i
         need(rhs, "rhs");
         const std::size_t n = op->eng->size();
         const auto b = as_cplx(rhs, n);
-        ApplyFn apply = [&](const cplx* in, cplx* out) { op->eng->apply(in, out); };
         GmresOutcome r;
         try {
-            r = gmres(apply, b, tol, max_iter, restart);
+            r = op->eng->gmres(b.data(), tol, max_iter, restart);  // device-resident Krylov basis
         } catch (const ConvergenceFailure& e) {
             if (history)
                 for (int i = 0; i < history_cap && i < int(e.history.size()); ++i) history[i] = e.history[i];

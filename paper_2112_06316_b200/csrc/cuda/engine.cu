@@ -755,6 +755,147 @@ void Engine::apply_device(const void* phi, void* out, void* S, void* D) {
     IFGF_CUDA(cudaStreamSynchronize(e.st));
 }
 
+// Restarted MGS-GMRES with Givens rotations (solver.cpp:177-300), vectors in HBM. Each
+// Arnoldi step: V_j -> d_phi (device copy), one graph apply -> d_out = w, MGS against
+// V_0..V_j with the coefficients kept on the device, |w|, then ONE copy of the column
+// H[0..j+1] to the host for the rotations and the residual estimate.
+GmresOutcome Engine::gmres(const cplx* rhs, double tol, int max_iter, int restart) {
+    Impl& e = *d_;
+    std::lock_guard<std::mutex> g(e.mu);
+    e.ensure_beta();
+    if (tol <= 0) throw InvalidArgument("gmres_solve: tolerance must be positive");
+    if (max_iter < 0) throw InvalidArgument("gmres_solve: max_iter must be >= 0");
+    IFGF_CUDA(cudaSetDevice(e.dev));
+    const std::int64_t n = std::int64_t(e.n);
+    const std::size_t vb = std::size_t(n) * sizeof(double2);
+    const int m_max = restart > 0 ? std::min(restart, std::max(max_iter, 1)) : std::max(max_iter, 1);
+    DevBuf b, x, r, V, H, partial, yv;
+    b.alloc(vb);
+    x.alloc(vb);
+    r.alloc(vb);
+    V.alloc(std::size_t(m_max + 1) * vb);
+    H.alloc(std::size_t(m_max + 2) * sizeof(double2));
+    partial.alloc(std::size_t(gmres_reduce_blocks()) * sizeof(double2));
+    yv.alloc(std::size_t(m_max + 1) * sizeof(double2));
+    cudaStream_t st = e.st;
+    IFGF_CUDA(cudaMemcpyAsync(b.as<void>(), rhs, vb, cudaMemcpyHostToDevice, st));
+    IFGF_CUDA(cudaMemsetAsync(x.as<void>(), 0, vb, st));
+    auto Vi = [&](int i) { return V.as<double2>() + std::size_t(i) * std::size_t(n); };
+    auto read_h = [&](int cnt, std::vector<cplx>& dst) {
+        dst.resize(cnt);
+        IFGF_CUDA(cudaMemcpyAsync(dst.data(), H.as<void>(), cnt * sizeof(double2), cudaMemcpyDeviceToHost, st));
+        IFGF_CUDA(cudaStreamSynchronize(st));
+    };
+    auto apply_to = [&](const double2* in) {  // d_out = A in
+        IFGF_CUDA(cudaMemcpyAsync(e.d_phi.as<void>(), in, vb, cudaMemcpyDeviceToDevice, st));
+        e.apply_graph();
+    };
+    std::vector<cplx> hcol;
+    launch_cdot(n, b.as<double2>(), b.as<double2>(), partial.as<double2>(), H.as<double2>(), true, st);
+    read_h(1, hcol);
+    const double bnorm = hcol[0].real();
+    GmresOutcome total;
+    if (bnorm == 0.0) {
+        total.x.assign(std::size_t(n), cplx{});
+        total.converged = true;
+        return total;
+    }
+    bool x_nonzero = false;
+    // one Arnoldi cycle of length m from the current x; returns converged
+    auto cycle = [&](int m, GmresOutcome& res) {
+        if (x_nonzero) {
+            apply_to(x.as<double2>());
+            launch_csub(n, b.as<double2>(), e.d_out.as<double2>(), r.as<double2>(), st);
+        } else {
+            IFGF_CUDA(cudaMemcpyAsync(r.as<void>(), b.as<void>(), vb, cudaMemcpyDeviceToDevice, st));
+        }
+        launch_cdot(n, r.as<double2>(), r.as<double2>(), partial.as<double2>(), H.as<double2>(), true, st);
+        read_h(1, hcol);
+        const double beta = hcol[0].real();
+        if (beta / bnorm <= tol) return true;
+        launch_cscale_inv(n, H.as<double2>(), r.as<double2>(), Vi(0), st);  // V_0 = r / beta
+        std::vector<std::vector<cplx>> Hh;
+        std::vector<cplx> cs(m), sn(m), gv(m + 1, cplx{});
+        gv[0] = beta;
+        for (int j = 0; j < m; ++j) {
+            apply_to(Vi(j));
+            double2* w = e.d_out.as<double2>();
+            for (int i = 0; i <= j; ++i) {
+                double2* hi = H.as<double2>() + i;
+                launch_cdot(n, Vi(i), w, partial.as<double2>(), hi, false, st);
+                launch_caxpy_dev(n, hi, w, Vi(i), st);
+            }
+            launch_cdot(n, w, w, partial.as<double2>(), H.as<double2>() + j + 1, true, st);
+            read_h(j + 2, hcol);
+            Hh.push_back(hcol);
+            std::vector<cplx>& Hj = Hh.back();
+            const double hn = Hj[j + 1].real();
+            ++res.iterations;
+            for (int i = 0; i < j; ++i) {
+                const cplx t = std::conj(cs[i]) * Hj[i] + std::conj(sn[i]) * Hj[i + 1];
+                Hj[i + 1] = -sn[i] * Hj[i] + cs[i] * Hj[i + 1];
+                Hj[i] = t;
+            }
+            const double den = std::sqrt(std::norm(Hj[j]) + hn * hn);
+            if (den < 1e-300) {
+                res.history.push_back(std::abs(gv[j]) / bnorm);
+                throw ConvergenceFailure("gmres: Arnoldi breakdown", res.history);
+            }
+            cs[j] = Hj[j] / den;
+            sn[j] = cplx(hn / den, 0.0);
+            Hj[j] = std::conj(cs[j]) * Hj[j] + std::conj(sn[j]) * hn;
+            Hj[j + 1] = 0.0;
+            gv[j + 1] = -sn[j] * gv[j];
+            gv[j] = std::conj(cs[j]) * gv[j];
+            const double rel = std::abs(gv[j + 1]) / bnorm;
+            res.history.push_back(rel);
+            if (rel <= tol || j == m - 1 || hn < 1e-14) {
+                std::vector<cplx> y(j + 1);
+                for (int i = j; i >= 0; --i) {
+                    cplx acc = gv[i];
+                    for (int t = i + 1; t <= j; ++t) acc -= Hh[t][i] * y[t];
+                    y[i] = acc / Hh[i][i];
+                }
+                IFGF_CUDA(cudaMemcpyAsync(yv.as<void>(), y.data(), y.size() * sizeof(double2),
+                                          cudaMemcpyHostToDevice, st));
+                launch_cupdate(n, j + 1, yv.as<double2>(), V.as<double2>(), n, x.as<double2>(), st);
+                x_nonzero = true;
+                return rel <= tol;
+            }
+            launch_cscale_inv(n, H.as<double2>() + j + 1, w, Vi(j + 1), st);  // V_{j+1} = w / hn
+        }
+        return false;
+    };
+    try {
+        if (restart <= 0) {
+            GmresOutcome part;
+            total.converged = cycle(std::max(max_iter, 0), part);
+            total.iterations = part.iterations;
+            total.history = std::move(part.history);
+        } else {
+            while (total.iterations < max_iter) {
+                const int len = std::min(restart, max_iter - total.iterations);
+                GmresOutcome part;
+                const bool ok = cycle(len, part);
+                total.iterations += part.iterations;
+                total.history.insert(total.history.end(), part.history.begin(), part.history.end());
+                if (ok) {
+                    total.converged = true;
+                    break;
+                }
+            }
+        }
+    } catch (const ConvergenceFailure& f) {
+        std::vector<double> h = total.history;
+        h.insert(h.end(), f.history.begin(), f.history.end());
+        throw ConvergenceFailure(f.what(), h);
+    }
+    total.x.resize(std::size_t(n));
+    IFGF_CUDA(cudaMemcpyAsync(total.x.data(), x.as<void>(), vb, cudaMemcpyDeviceToHost, st));
+    IFGF_CUDA(cudaStreamSynchronize(st));
+    return total;
+}
+
 void Engine::ifgf_apply(const cplx* a, bool single, bool dbl, DlStrategy s, cplx* S, cplx* D) {
     Impl& e = *d_;
     std::lock_guard<std::mutex> g(e.mu);

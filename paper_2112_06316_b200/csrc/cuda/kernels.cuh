@@ -77,6 +77,17 @@ struct RpDev {
 // out[perm[t]] = out_m[t]
 void launch_unpermute1(int n, const std::uint32_t* perm, const double2* in_m, double2* out, cudaStream_t st);
 void launch_density_coeffs(const RpDev& R, const double2* phi, double2* coeffs, cudaStream_t st);
+
+// device-resident GMRES vector kernels (gmres_kernels.cu); reductions deterministic
+int gmres_reduce_blocks();
+// dst = sum conj(a) b (as_norm: dst = (sqrt(re), 0)); partial holds gmres_reduce_blocks() entries
+void launch_cdot(std::int64_t n, const double2* a, const double2* b, double2* partial, double2* dst, bool as_norm,
+                 cudaStream_t st);
+void launch_caxpy_dev(std::int64_t n, const double2* h, double2* w, const double2* v, cudaStream_t st);  // w -= h v
+void launch_cscale_inv(std::int64_t n, const double2* h, const double2* w, double2* v, cudaStream_t st);  // v = w/h
+void launch_csub(std::int64_t n, const double2* b, const double2* ax, double2* r, cudaStream_t st);      // r = b - ax
+void launch_cupdate(std::int64_t n, int m, const double2* y, const double2* V, std::int64_t ld, double2* x,
+                    cudaStream_t st);  // x += sum y_i V_i
 // out[l] = 1/2 phi + (D_far+near+rp) - i gamma (S_far+near+rp); S/D written when non-null
 void launch_rp_combine(const RpDev& R, const double2* coeffs, const double2* phi,
                        const double2* Sp, const double2* Dp, double gamma, double2* out,

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "host/boxtree.hpp"
+#include "host/gmres.hpp"
 #include "host/coneplan.hpp"
 #include "host/proximity.hpp"
 #include "host/surface.hpp"
@@ -60,6 +61,12 @@ class Engine {
     void apply_direct(const cplx* phi, cplx* out);
     // RP correction alone (rp.cpp:421-451), outputs overwritten
     void rp_apply(const cplx* phi, cplx* S, cplx* D);
+
+    // restarted MGS-GMRES on the device (solver.cpp:177-300 semantics): Krylov basis in HBM,
+    // operator applies from the captured graph, only Hessenberg columns cross to the host.
+    // rhs in original node order. Under a communicator every rank runs the same iteration
+    // on replicated vectors (the applies are collective, the reductions deterministic).
+    GmresOutcome gmres(const cplx* rhs, double tol, int max_iter, int restart);
 
     // ---- multi-GPU: each engine owns the sources and targets of a
     // leaf-aligned Morton range; the far field is computed from owned sources for all

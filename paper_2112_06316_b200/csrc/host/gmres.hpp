@@ -1,9 +1,8 @@
-// Restarted MGS-GMRES with Givens rotations around a matrix-free apply, with the
-// iteration semantics of /root/reference/proj/src/solver.cpp:169-300 (relative residual
+// Result of the restarted MGS-GMRES (solver.cpp:169-300 semantics: relative residual
 // history per iteration, restart re-entry with x0, Arnoldi breakdown -> ConvergenceFailure).
+// The iteration itself runs on the device: Engine::gmres (cuda/engine.cu).
 #pragma once
 
-#include <functional>
 #include <vector>
 
 #include "core.hpp"
@@ -16,10 +15,5 @@ struct GmresOutcome {
     int iterations = 0;
     bool converged = false;
 };
-
-using ApplyFn = std::function<void(const cplx* in, cplx* out)>;
-
-GmresOutcome gmres(const ApplyFn& apply, const std::vector<cplx>& rhs, double tol, int max_iter,
-                   int restart);
 
 }  // namespace ifgfb200
