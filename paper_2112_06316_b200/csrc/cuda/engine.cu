@@ -85,6 +85,8 @@ Pipes make_pipes(const std::vector<int>& f) {
 struct Engine::Impl {
     int dev = 0;
     cudaStream_t st = nullptr;
+    cudaStream_t st2 = nullptr;            // side stream: near field + RP, concurrent with the IFGF
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::mutex mu;
     std::size_t n = 0;
     int depth = 0;
@@ -120,7 +122,7 @@ struct Engine::Impl {
     std::vector<double> rule_x, rule_w;
     int max_dudv = 1, max_nunv = 1, max_dv = 1, max_nu = 1;
     // work vectors
-    DevBuf d_phi, d_out, d_S, d_D, a_p, Sp, Dp, scratch, flush;
+    DevBuf d_phi, d_out, d_S, d_D, a_p, Sp, Dp, Sn, Dn, scratch, flush;
     PointsDev P;
     DirectDev direct;
     // graph of the full apply on (d_phi -> d_out, d_S, d_D)
@@ -164,25 +166,36 @@ struct Engine::Impl {
         return launches;
     }
 
-    // full operator on d_phi -> out, S, D (device pointers)
+    // full operator on d_phi -> out, S, D (device pointers). The near field and the RP
+    // correction do not depend on the far field: they run on the side stream st2 into
+    // (Sn, Dn) while the IFGF fills (Sp, Dp) on st; a combine kernel joins both.
     int run_apply(const double2* phi, double2* out, double2* S, double2* D) {
         int launches = 0;
-        IFGF_CUDA(cudaMemsetAsync(Sp.as<void>(), 0, n * sizeof(double2), st));
-        IFGF_CUDA(cudaMemsetAsync(Dp.as<void>(), 0, n * sizeof(double2), st));
+        const std::size_t vb = n * sizeof(double2);
+        IFGF_CUDA(cudaMemsetAsync(Sp.as<void>(), 0, vb, st));
+        IFGF_CUDA(cudaMemsetAsync(Dp.as<void>(), 0, vb, st));
+        IFGF_CUDA(cudaMemsetAsync(Sn.as<void>(), 0, vb, st));
+        IFGF_CUDA(cudaMemsetAsync(Dn.as<void>(), 0, vb, st));
         launch_weights(int(n), perm.as<std::uint32_t>(), phi, jw_p.as<double>(), a_p.as<double2>(), st);
         ++launches;
+        IFGF_CUDA(cudaEventRecord(ev_fork, st));
+        IFGF_CUDA(cudaStreamWaitEvent(st2, ev_fork, 0));
+        launch_near_field(near, P, a_p.as<double2>(), k, Sn.as<double2>(), Dn.as<double2>(), st2);
+        launch_density_coeffs(rp, phi, coeffs.as<double2>(), st2);
+        launch_rp_accum(rp, coeffs.as<double2>(), Sn.as<double2>(), Dn.as<double2>(), st2);
+        launches += 3;
+        IFGF_CUDA(cudaEventRecord(ev_join, st2));
         launches += run_ifgf(true, true, strategy);
         if (world > 1) reduce_far_to_owners();  // far-field partials -> target owners
-        launch_near_field(near, P, a_p.as<double2>(), k, Sp.as<double2>(), Dp.as<double2>(), st);
-        ++launches;
-        launch_density_coeffs(rp, phi, coeffs.as<double2>(), st);
+        IFGF_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
         RpDev r = rp;
         if (world > 1) {  // owned targets in Morton order, then exchanged
             r.out_m = out_m.as<double2>();
             S = D = nullptr;
         }
-        launch_rp_combine(r, coeffs.as<double2>(), phi, Sp.as<double2>(), Dp.as<double2>(), gamma, out, S, D, st);
-        launches += 2;
+        launch_combine(r, phi, Sp.as<double2>(), Dp.as<double2>(), Sn.as<double2>(), Dn.as<double2>(), gamma, out, S,
+                       D, st);
+        ++launches;
         if (world > 1) {
             gather_out_from_owners();
             launch_unpermute1(int(n), perm.as<std::uint32_t>(), out_m.as<double2>(), out, st);
@@ -293,6 +306,9 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
     e.dev = device;
     IFGF_CUDA(cudaSetDevice(device));
     IFGF_CUDA(cudaStreamCreateWithFlags(&e.st, cudaStreamNonBlocking));
+    IFGF_CUDA(cudaStreamCreateWithFlags(&e.st2, cudaStreamNonBlocking));
+    IFGF_CUDA(cudaEventCreateWithFlags(&e.ev_fork, cudaEventDisableTiming));
+    IFGF_CUDA(cudaEventCreateWithFlags(&e.ev_join, cudaEventDisableTiming));
     const Surface& S = *s.surf;
     const BoxTree& T = *s.tree;
     const BoxRelations& R = *s.rel;
@@ -633,7 +649,8 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
                 e.ony.as<double>(), e.onz.as<double>(), e.ojw.as<double>(), e.opatch.as<std::int32_t>(),
                 e.tpb.as<std::uint32_t>(), e.pair_patch.as<std::int32_t>()};
     const std::size_t vb = std::max<std::size_t>(n, 1) * sizeof(double2);
-    for (DevBuf* b : {&e.d_phi, &e.d_out, &e.d_S, &e.d_D, &e.a_p, &e.Sp, &e.Dp, &e.scratch, &e.out_m}) b->alloc(vb);
+    for (DevBuf* b : {&e.d_phi, &e.d_out, &e.d_S, &e.d_D, &e.a_p, &e.Sp, &e.Dp, &e.Sn, &e.Dn, &e.scratch, &e.out_m})
+        b->alloc(vb);
     e.own_lo = 0;
     e.own_hi = std::uint32_t(n);
     e.bounds = {0u, std::uint32_t(n)};
@@ -645,6 +662,9 @@ Engine::~Engine() {
         cudaSetDevice(d_->dev);
         if (d_->graph) cudaGraphExecDestroy(d_->graph);
         if (d_->comm) ncclCommDestroy(d_->comm);
+        if (d_->ev_fork) cudaEventDestroy(d_->ev_fork);
+        if (d_->ev_join) cudaEventDestroy(d_->ev_join);
+        if (d_->st2) cudaStreamDestroy(d_->st2);
         if (d_->st) cudaStreamDestroy(d_->st);
     }
 }

@@ -78,6 +78,12 @@ struct RpDev {
 void launch_unpermute1(int n, const std::uint32_t* perm, const double2* in_m, double2* out, cudaStream_t st);
 void launch_density_coeffs(const RpDev& R, const double2* phi, double2* coeffs, cudaStream_t st);
 
+// concurrent-apply split of rp_combine: RP accumulated into the near buffers (Morton order),
+// then the combine of far (Sp, Dp) + near/RP (Sn, Dn)
+void launch_rp_accum(const RpDev& R, const double2* coeffs, double2* Sn, double2* Dn, cudaStream_t st);
+void launch_combine(const RpDev& R, const double2* phi, const double2* Sp, const double2* Dp, const double2* Sn,
+                    const double2* Dn, double gamma, double2* out, double2* S, double2* D, cudaStream_t st);
+
 // device-resident GMRES vector kernels (gmres_kernels.cu); reductions deterministic
 int gmres_reduce_blocks();
 // dst = sum conj(a) b (as_norm: dst = (sqrt(re), 0)); partial holds gmres_reduce_blocks() entries

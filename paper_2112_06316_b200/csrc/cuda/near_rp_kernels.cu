@@ -185,6 +185,62 @@ __global__ void rp_combine_kernel(RpDev R, const double2* __restrict__ coeffs,
     if (D) D[l] = d;
 }
 
+// RP correction alone, accumulated into the Morton-order near-field buffers (Sn, Dn): the
+// same warp-per-target beta streaming as rp_combine_kernel, for the side stream of the
+// concurrent apply
+__global__ void rp_accum_kernel(RpDev R, const double2* __restrict__ coeffs, double2* __restrict__ Sn,
+                                double2* __restrict__ Dn) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= R.n) return;
+    const int l = warp;
+    const std::uint32_t tm = R.pos[l];
+    if (tm < R.own_lo || tm >= R.own_hi) return;  // target owned by another rank
+    double2 as = make_double2(0.0, 0.0), ad = make_double2(0.0, 0.0);
+    for (std::uint32_t p = R.tpb[l]; p < R.tpb[l + 1]; ++p) {
+        const int q = R.pair_patch[p];
+        const int nn = R.patch_nu[q] * R.patch_nv[q];
+        const double2* a = coeffs + R.patch_start[q];
+        const double2* bs = R.beta_s + R.beta_off[p];
+        const double2* bd = R.beta_d + R.beta_off[p];
+        for (int i = lane; i < nn; i += 32) {
+            const double2 ai = a[i];
+            cfma(as, ai, __ldcs(bs + i));
+            cfma(ad, ai, __ldcs(bd + i));
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        as.x += __shfl_xor_sync(0xffffffffu, as.x, o);
+        as.y += __shfl_xor_sync(0xffffffffu, as.y, o);
+        ad.x += __shfl_xor_sync(0xffffffffu, ad.x, o);
+        ad.y += __shfl_xor_sync(0xffffffffu, ad.y, o);
+    }
+    if (lane != 0) return;
+    Sn[tm] = cadd(Sn[tm], as);
+    Dn[tm] = cadd(Dn[tm], ad);
+}
+
+// out = 1/2 phi + D - i gamma S with S = far + (near + RP), per original target
+// (solver.cpp:152-156, ifgf.cpp:603-606 un-permute)
+__global__ void combine_kernel(RpDev R, const double2* __restrict__ phi, const double2* __restrict__ Sp,
+                               const double2* __restrict__ Dp, const double2* __restrict__ Sn,
+                               const double2* __restrict__ Dn, double gamma, double2* __restrict__ out,
+                               double2* __restrict__ S, double2* __restrict__ D) {
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= R.n) return;
+    const std::uint32_t t = R.pos[l];
+    if (t < R.own_lo || t >= R.own_hi) return;
+    const double2 s = cadd(Sp[t], Sn[t]);
+    const double2 d = cadd(Dp[t], Dn[t]);
+    const double2 f = phi[l];
+    const double2 o = make_double2(0.5 * f.x + d.x + gamma * s.y, 0.5 * f.y + d.y - gamma * s.x);
+    if (R.out_m) R.out_m[t] = o;
+    else out[l] = o;
+    if (S) S[l] = s;
+    if (D) D[l] = d;
+}
+
 constexpr int kDirectThreads = 256;
 
 __global__ void __launch_bounds__(kDirectThreads)
@@ -286,6 +342,20 @@ void launch_rp_combine(const RpDev& R, const double2* coeffs, const double2* phi
     const long warps = R.n;
     const int grid = int((warps * 32 + threads - 1) / threads);
     rp_combine_kernel<<<grid, threads, 0, st>>>(R, coeffs, phi, Sp, Dp, gamma, out, S, D);
+    IFGF_CUDA(cudaGetLastError());
+}
+
+void launch_rp_accum(const RpDev& R, const double2* coeffs, double2* Sn, double2* Dn, cudaStream_t st) {
+    if (R.n == 0) return;
+    const int threads = 256;
+    rp_accum_kernel<<<int((long(R.n) * 32 + threads - 1) / threads), threads, 0, st>>>(R, coeffs, Sn, Dn);
+    IFGF_CUDA(cudaGetLastError());
+}
+
+void launch_combine(const RpDev& R, const double2* phi, const double2* Sp, const double2* Dp, const double2* Sn,
+                    const double2* Dn, double gamma, double2* out, double2* S, double2* D, cudaStream_t st) {
+    if (R.n == 0) return;
+    combine_kernel<<<(R.n + 255) / 256, 256, 0, st>>>(R, phi, Sp, Dp, Sn, Dn, gamma, out, S, D);
     IFGF_CUDA(cudaGetLastError());
 }
 
