@@ -8,12 +8,12 @@
 //      coordinates and the re-centring factors (node directions from sin/cos tables);
 //   2. tiles of 8 evaluations contract the child's 3x5x5 coefficient block with
 //      mma.sync.m8n8k4.f64 (DMMA): A = T_s(s) T_t(theta) (rows = evaluations, k = the 15
-//      (s, theta) index pairs in 4 steps of 4), B = coefficients with columns = (phi
-//      sub-index, pipe, re/im): the 8 columns hold 4 / pipes phi indices at once, so a
-//      tile takes 4 x ceil(5 / (4 / pipes)) DMMAs (20 for 3 pipes, 12 for 2, 8 for 1), one
-//      accumulator per phi group; B is loaded once per group and reused by all its tiles;
-//   3. the epilogue weights the accumulators by T_p(phi), sums the phi sub-indices across
-//      the quad, applies the re-centring factor and adds into the warp's private node
+//      (s, theta) index pairs in 4 steps of 4), B = coefficients whose 8 columns hold 4
+//      (pipe, phi index) pairs x {re, im}, one accumulator per column group: a tile takes
+//      4 x ceil(5 pipes / 4) DMMAs (16 for 3 pipes, 12 for 2, 8 for 1); B is loaded once
+//      per group and reused by all its tiles;
+//   3. the epilogue weights the accumulators by T_p(phi), gathers each pipe's phi terms
+//      within the quad (shuffles), applies the re-centring factor and adds into the warp's private node
 //      accumulators (no atomics).
 // The separable block transform (warp-local) finishes the segment. Results equal the
 // per-lane kernel to rounding (~1e-16); the evaluation order is fixed, so the output is
@@ -108,11 +108,30 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
     const double pcx = Lp.cx[pb], pcy = Lp.cy[pb], pcz = Lp.cz[pb];
 
     const int r = lane >> 2, tig = lane & 3;
-    // B column n = lane >> 2 = 2 NPC sub + 2 pipe + re/im: IPG phi indices share one DMMA
-    constexpr int IPG = 4 / NPC, NIPG = (kPA + IPG - 1) / IPG;
-    const int ncol = lane >> 2, bsub = ncol / (2 * NPC), comp = ncol % (2 * NPC);
-    const bool bcol = bsub < IPG;
-    const int boff = 2 * (comp >> 1) * kNP + (comp & 1);
+    // B column n = lane >> 2 = 2 c + re/im; column pair c of accumulator group q holds one
+    // (pipe, phi index). 3 pipes: c < 3 -> (c, q) for q = 0..3 and c = 3 -> (q, 4), i.e.
+    // 15 pairs in 4 groups; fewer pipes: IPG = 4 / pipes phi indices per group,
+    // c = pipes * sub + pipe -> (pipe, IPG q + sub).
+    constexpr int IPG = 4 / NPC;
+    constexpr int NQ = NPC == 3 ? 4 : (kPA + IPG - 1) / IPG;
+    const int ncol = lane >> 2, bc = ncol >> 1, reim = ncol & 1;
+    auto pair_of = [](int q, int c, int& pipe, int& ip) -> bool {
+        if constexpr (NPC == 3) {
+            if (c < 3) {
+                pipe = c;
+                ip = q;
+                return true;
+            }
+            pipe = q;
+            ip = kPA - 1;
+            return q < 3;
+        } else {
+            const int sub = c / NPC;
+            pipe = c % NPC;
+            ip = IPG * q + sub;
+            return sub < IPG && ip < kPA;
+        }
+    };
     const int gb = Lc.pgrp_begin[so], ge = Lc.pgrp_begin[so + 1];
     for (int g = gb; g < ge; ++g) {
         const int cso = Lc.pgrp_seg[g];
@@ -157,19 +176,21 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
         // steps of 4: slot (j, tig) holds (is, it) = (tig, j) for tig < 3 and (j, 4) for
         // tig = 3 (slot (3, 3) is padding); one accumulator per phi group. Loaded once per
         // group, reused by all its tiles.
-        const double* blk = reinterpret_cast<const double*>(cstore + std::size_t(cso) * NPC * kNP) + boff;
+        const double* blk = reinterpret_cast<const double*>(cstore + std::size_t(cso) * NPC * kNP) + reim;
         const bool lo = tig < kPS;
-        double bq[kKS * NIPG];
+        double bq[kKS * NQ];
 #pragma unroll
-        for (int q = 0; q < NIPG; ++q)
+        for (int q = 0; q < NQ; ++q) {
+            int pipe, ip;
+            const bool live = pair_of(q, bc, pipe, ip);
 #pragma unroll
             for (int j = 0; j < kKS; ++j) {
-                const int ip = IPG * q + bsub;
                 const int is = lo ? tig : j, it = lo ? j : kPA - 1;
-                bq[q * kKS + j] = (bcol && ip < kPA && (lo || j < kPS))
-                                      ? __ldg(blk + 2 * (is + kPS * (it + kPA * ip)))
+                bq[q * kKS + j] = (live && (lo || j < kPS))
+                                      ? __ldg(blk + 2 * (pipe * kNP + is + kPS * (it + kPA * ip)))
                                       : 0.0;
             }
+        }
         for (int t0 = 0; t0 < count; t0 += 8) {
             const bool valid = t0 + r < count;
             const double* gp = geo + (valid ? t0 + r : 0) * kGeo;
@@ -181,36 +202,55 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
             double tsel = tig == 0 ? ts[0] : (tig == 1 ? ts[1] : ts[2]);
             double t4 = tt[kPA - 1];
             if (!valid) tsel = t4 = 0.0;
-            double d[NIPG][2];
+            double d[NQ][2];
 #pragma unroll
-            for (int q = 0; q < NIPG; ++q) d[q][0] = d[q][1] = 0.0;
+            for (int q = 0; q < NQ; ++q) d[q][0] = d[q][1] = 0.0;
 #pragma unroll
             for (int j = 0; j < kKS; ++j) {
                 const double x = lo ? tsel : (j < kPS ? ts[j] : 0.0);
                 const double y = lo ? tt[j] : t4;
                 const double a = x * y;
 #pragma unroll
-                for (int q = 0; q < NIPG; ++q) dmma884(d[q][0], d[q][1], a, bq[q * kKS + j]);
+                for (int q = 0; q < NQ; ++q) dmma884(d[q][0], d[q][1], a, bq[q * kKS + j]);
             }
-            // 3. lane (r, tig) holds columns 2 tig, 2 tig + 1 = (re, im) of pipe tig % NPC at
-            // phi sub-index tig / NPC: weight by T(phi) and sum the sub-indices over the quad
+            // 3. lane (r, tig) holds columns 2 tig, 2 tig + 1 of each group = (re, im) of the
+            // pair (pipe, phi index) of column pair tig: weight by T(phi), gather the pipes
             double tq[kPA];
             cheb_row<kPA>(gp[2], tq);
-            const int sub = tig / NPC;
             double2 val = make_double2(0.0, 0.0);
+            if constexpr (NPC == 3) {
 #pragma unroll
-            for (int q = 0; q < NIPG; ++q) {
-                double w = 0.0;
+                for (int q = 0; q < NQ; ++q) {
+                    val.x = fma(tq[q], d[q][0], val.x);
+                    val.y = fma(tq[q], d[q][1], val.y);
+                }
+                // phi index 4 of pipe q sits in lane 3 of the quad, group q
+                const int src = (lane & ~3) | 3;
 #pragma unroll
-                for (int s = 0; s < IPG; ++s)
-                    if (IPG * q + s < kPA && sub == s) w = tq[IPG * q + s];
-                val.x = fma(w, d[q][0], val.x);
-                val.y = fma(w, d[q][1], val.y);
-            }
+                for (int q = 0; q < 3; ++q) {
+                    const double ex = __shfl_sync(0xffffffffu, d[q][0], src);
+                    const double ey = __shfl_sync(0xffffffffu, d[q][1], src);
+                    if (tig == q) {
+                        val.x = fma(tq[kPA - 1], ex, val.x);
+                        val.y = fma(tq[kPA - 1], ey, val.y);
+                    }
+                }
+            } else {
+                const int sub = tig / NPC;
 #pragma unroll
-            for (int off = NPC; off < NPC * IPG; off <<= 1) {
-                val.x += __shfl_down_sync(0xffffffffu, val.x, off);
-                val.y += __shfl_down_sync(0xffffffffu, val.y, off);
+                for (int q = 0; q < NQ; ++q) {
+                    double w = 0.0;
+#pragma unroll
+                    for (int s = 0; s < IPG; ++s)
+                        if (IPG * q + s < kPA && sub == s) w = tq[IPG * q + s];
+                    val.x = fma(w, d[q][0], val.x);
+                    val.y = fma(w, d[q][1], val.y);
+                }
+#pragma unroll
+                for (int off = NPC; off < NPC * IPG; off <<= 1) {
+                    val.x += __shfl_down_sync(0xffffffffu, val.x, off);
+                    val.y += __shfl_down_sync(0xffffffffu, val.y, off);
+                }
             }
             // lanes tig < NPC now hold (re, im) of child pipe tig for evaluation row r
             const double2 r1 = make_double2(gp[3], gp[4]);
