@@ -37,6 +37,12 @@ struct LevelDev {
     // cos/sin of the theta- and phi-cell centres (nc and 2nc entries); null when cells are
     // wider than pi/4 (nc < 4), where local_coords uses acos/atan2
     const double *thc_cos = nullptr, *thc_sin = nullptr, *phc_cos = nullptr, *phc_sin = nullptr;
+    // parent-fill geometry templates for this level's children (host/coneplan.hpp
+    // parent_templates): slot per cone cell (-1: none), 8 doubles per (slot, octant, node)
+    // entry and the template child cell; null when the level does not use them
+    const std::int32_t* tmpl_slot = nullptr;
+    const double* tmpl = nullptr;
+    const std::int32_t* tmpl_gc = nullptr;
     // multi-GPU source ownership: box has sources in this rank's Morton range (null = all)
     const std::uint8_t* active = nullptr;
     const std::int32_t *chunk_box = nullptr, *chunk_q0 = nullptr;  // cousin work chunks

@@ -10,6 +10,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 #include <cstring>
 #include <mutex>
 #include <sstream>
@@ -70,7 +72,7 @@ class DevBuf {
 struct LevelBufs {
     DevBuf cx, cy, cz, beg, end, cz_ptr, cz_idx, cev_begin, cev_seg, seg_box, seg_gamma,
         box_seg_begin, pev_begin, pev_seg, pev_perm, pgrp_begin, pgrp_seg, pgrp_start, pgrp_count, ch_ptr, ch_idx, s_nodes, th_nodes, ph_nodes, th_sin, th_cos, ph_sin, ph_cos, thc_cos, thc_sin, phc_cos, phc_sin,
-        chunk_box, chunk_q0;
+        chunk_box, chunk_q0, tmpl_slot, tmpl, tmpl_gc;
 };
 
 Pipes make_pipes(const std::vector<int>& f) {
@@ -514,6 +516,38 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
     e.storeB.alloc(std::max<std::size_t>(store, 1) * sizeof(double2));
     e.Ms.upload(cheb::transform(e.ps));
     e.Ma.upload(cheb::transform(e.pang));
+
+    // ---- parent-fill geometry templates where a level's cone cells are reused by many
+    // parent segments (at least 8 evaluations per template entry); IFGF_PARENT_TEMPLATES=0
+    // turns them off
+    {
+        const char* env = std::getenv("IFGF_PARENT_TEMPLATES");
+        const bool enabled = !(env && std::string(env) == "0");
+        for (int d = 4; enabled && d <= T.depth; ++d) {
+            const ConeLevel& PL = C.level[d - 2];
+            const ConeLevel& CL = C.level[d - 1];
+            if (PL.ps != 3 || PL.pang != 5 || CL.ps != 3 || CL.pang != 5) continue;
+            std::vector<std::int32_t> slot(PL.segs_per_box(), -1), gammas;
+            for (std::int32_t g : PL.seg_gamma)
+                if (slot[g] < 0) {
+                    slot[g] = std::int32_t(gammas.size());
+                    gammas.push_back(g);
+                }
+            const std::size_t entries = gammas.size() * 8 * std::size_t(PL.nodes_per_seg());
+            if (entries * 8 > CL.pev_perm.size() || entries * 64 > (std::size_t(2) << 30)) continue;
+            std::vector<double> tab;
+            std::vector<std::int32_t> gc;
+            parent_templates(T, C, d, gammas, 0, tab, gc);
+            LevelBufs& b = e.lb[d - 2];
+            b.tmpl_slot.upload(slot);
+            b.tmpl.upload(tab);
+            b.tmpl_gc.upload(gc);
+            LevelDev& L = e.L[d - 2];
+            L.tmpl_slot = b.tmpl_slot.as<std::int32_t>();
+            L.tmpl = b.tmpl.as<double>();
+            L.tmpl_gc = b.tmpl_gc.as<std::int32_t>();
+        }
+    }
 
     // ---- near field
     {

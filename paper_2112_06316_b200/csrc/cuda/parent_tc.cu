@@ -103,6 +103,7 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
     const int gam = Lp.seg_gamma[so];
     const int g1 = gam % Lp.ns, g2 = (gam / Lp.ns) % Lp.nc, g3 = gam / Lp.ns / Lp.nc;
     const int c0 = Lp.ch_ptr[pb];
+    const int tslot = Lp.tmpl_slot ? Lp.tmpl_slot[gam] : -1;
     const std::int64_t ev0 = Lc.pev_begin[so];
     const double hp = Lp.h, hc = Lc.h;
     const double pcx = Lp.cx[pb], pcy = Lp.cy[pb], pcz = Lp.cz[pb];
@@ -141,9 +142,26 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
         const int ch = Lp.ch_idx[c0 + c_grp];
         if (Lc.active && !Lc.active[ch]) continue;  // child holds no sources of this rank
         const double ccx = Lc.cx[ch], ccy = Lc.cy[ch], ccz = Lc.cz[ch];
-        const CellFrame cf = cell_frame(Lc.seg_gamma[cso], Lc);
+        const int cgam = Lc.seg_gamma[cso];
+        const CellFrame cf = cell_frame(cgam, Lc);
+        // geometry template of (parent cell, child octant), host/coneplan.hpp parent_templates
+        const int oct = (ccx > pcx ? 1 : 0) | (ccy > pcy ? 2 : 0) | (ccz > pcz ? 4 : 0);
+        const std::size_t tbase = (std::size_t(tslot) * 8 + oct) * kNP;
         for (int i = lane; i < count; i += 32) {
             const int node = Lc.pev_perm[ev0 + start + i] & 0xff;  // entries are node | c << 8
+            double* gp = geo + i * kGeo;
+            if (tslot >= 0 && Lp.tmpl_gc[tbase + node] == cgam) {
+                const double2* te = reinterpret_cast<const double2*>(Lp.tmpl + (tbase + node) * 8);
+                const double2 e0 = __ldg(te), e1 = __ldg(te + 1), e2 = __ldg(te + 2), e3 = __ldg(te + 3);
+                gp[0] = e0.x;
+                gp[1] = e0.y;
+                gp[2] = e1.x;
+                gp[3] = e1.y;
+                gp[4] = e2.x;
+                gp[5] = CB::extra == RI ? e2.y : e3.x;
+                gp[6] = double(node);
+                continue;
+            }
             const int is = node % kPS, it = (node / kPS) % kPA, ip = node / (kPS * kPA);
             const double s = Lp.s_nodes[g1 * kPS + is];
             const double rp = hp / s;
@@ -161,7 +179,6 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
             double sn, cs;
             sincos_bounded(k * dr, &sn, &cs);
             const double q1 = rp * inv_rc;
-            double* gp = geo + i * kGeo;
             gp[0] = lc.ls;
             gp[1] = lc.lt;
             gp[2] = lc.lp;

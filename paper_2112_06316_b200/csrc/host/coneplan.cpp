@@ -330,6 +330,50 @@ ConePlanHost build_cone_plan(const BoxTree& t, const BoxRelations& rel,
     return plan;
 }
 
+void parent_templates(const BoxTree& t, const ConePlanHost& plan, int d, const std::vector<std::int32_t>& gammas,
+                      int workers, std::vector<double>& entries, std::vector<std::int32_t>& gc) {
+    const ConeLevel& PL = plan.level[d - 2];
+    const ConeLevel& CL = plan.level[d - 1];
+    const int P = PL.nodes_per_seg();
+    const double hp = t.half_diag(d - 1), hc = t.half_diag(d), half = 0.5 * t.side(d);
+    const double k = plan.k;
+    entries.assign(gammas.size() * 8 * std::size_t(P) * 8, 0.0);
+    gc.assign(gammas.size() * 8 * std::size_t(P), -1);
+    const Vec3 origin{0.0, 0.0, 0.0};
+    parallel_for(std::int64_t(gammas.size()), worker_count(workers), [&](std::int64_t slot) {
+        const int gam = gammas[slot];
+        const int g1 = gam % PL.ns, g2 = (gam / PL.ns) % PL.nc, g3 = gam / PL.ns / PL.nc;
+        for (int o = 0; o < 8; ++o) {
+            const Vec3 off{(o & 1) ? half : -half, (o & 2) ? half : -half, (o & 4) ? half : -half};
+            for (int ip = 0; ip < PL.pang; ++ip)
+                for (int it = 0; it < PL.pang; ++it)
+                    for (int is = 0; is < PL.ps; ++is) {
+                        const int node = is + PL.ps * (it + PL.pang * ip);
+                        const double s = PL.s_nodes[std::size_t(g1) * PL.ps + is];
+                        const Vec3 x = from_cone(s, PL.th_nodes[std::size_t(g2) * PL.pang + it],
+                                                 PL.ph_nodes[std::size_t(g3) * PL.pang + ip], origin, hp);
+                        const Cone cc = to_cone(x, off, hc);
+                        const int g = segment_gamma(CL, cc);
+                        const int c1 = g % CL.ns, c2 = (g / CL.ns) % CL.nc, c3 = g / CL.ns / CL.nc;
+                        const Vec3 v = x - off;
+                        const double rc = len(v), rp = hp / s;
+                        const Vec3 sv = off - 2.0 * x;  // stable r_c - r_p (ifgf.cpp:149-153)
+                        const double dr = dot3(sv, off) / (rc + rp);
+                        const std::size_t at = (std::size_t(slot) * 8 + o) * P + node;
+                        double* e = entries.data() + at * 8;
+                        e[0] = 2.0 * cc.s / CL.ds - (2 * c1 + 1.0);
+                        e[1] = 2.0 * (cc.th - (c2 + 0.5) * CL.dth) / CL.dth;
+                        e[2] = 2.0 * (cc.ph - (c3 + 0.5) * CL.dph) / CL.dph;
+                        e[3] = rp / rc * std::cos(k * dr);
+                        e[4] = rp / rc * std::sin(k * dr);
+                        e[5] = 1.0 / rc;
+                        e[6] = rp / rc;
+                        gc[at] = g;
+                    }
+        }
+    });
+}
+
 // cost-balanced leaf-aligned boundaries: per leaf box, near pairs + leaf-fill
 // interactions + cousin evaluations (as source box) weighted by their flop counts
 std::vector<std::uint32_t> partition_sources(const BoxTree& t, const BoxRelations& rel, const ConePlanHost& plan,

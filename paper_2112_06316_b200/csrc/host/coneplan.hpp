@@ -71,6 +71,17 @@ ConePlanHost build_cone_plan(const BoxTree& t, const BoxRelations& rel,
                              const std::vector<Vec3>& pts_morton, const ConeParams& p,
                              int workers);
 
+// Parent-fill geometry templates (device data, not decisions). The position of a parent
+// interpolation node relative to a child box depends only on the parent cone cell, the
+// node and the child's octant (box centres are exact grid points up to one rounding), so
+// per (parent cell gamma_p, octant, node) the child cell the node falls in and its
+// continuous data are tabulated once per level: entry = {ls, lt, lp, re/im of
+// (r_p/r_c) e^{ik(r_c - r_p)}, 1/r_c, r_p/r_c, 0} (8 doubles) and gc = child cell. The
+// per-box decisions stay the host's (pev ordinals); a device evaluation uses an entry only
+// when gc equals its host-decided child cell. d = child level (parent level d - 1).
+void parent_templates(const BoxTree& t, const ConePlanHost& plan, int d, const std::vector<std::int32_t>& gammas,
+                      int workers, std::vector<double>& entries, std::vector<std::int32_t>& gc);
+
 // Cost-balanced, leaf-aligned Morton boundaries (parts + 1) of the multi-GPU source/target
 // ownership: per leaf box, near pairs, leaf-fill interactions and cousin
 // and parent evaluations weighted by their flops
