@@ -1,0 +1,136 @@
+// Cousin evaluation (ifgf.cpp:396-450) on the FP64 tensor cores, for the default
+// interpolation orders (ps = 3, pang = 5).
+//
+// One warp per <= 32 targets of a box (independent warp items, 4 per CTA), one lane per
+// target. Per cousin source box the warp
+//   1. computes each lane's local coordinates in its host-decided segment (cev_seg) and
+//      the centred factor e^{ikr}/(4 pi r) into warp shared memory;
+//   2. forms groups of lanes that evaluate the same segment (ballot on the ordinal), lists
+//      each group's lanes, loads the segment's B fragments once and runs 8-row DMMA tiles
+//      over the group (tc_common.cuh: 16 DMMAs per tile for 3 pipes, 12 for 2);
+//   3. applies the pipe factors (W1 -> S; W2 (1/r), W3 (-ik), W4 -> D), sums the pipes of
+//      each evaluation across the quad and adds into the target's shared accumulators.
+// Every target gets its cousins' contributions in cousin-list order: deterministic.
+#include "ifgf_device.cuh"
+#include "kernels.cuh"
+#include "tc_common.cuh"
+
+namespace ifgfb200 {
+namespace {
+
+using namespace dev;
+using namespace ifgfdev;
+using namespace tc;
+
+constexpr int kThreads = 128, kWarps = kThreads / 32;
+constexpr int kCG = 7;  // ls, lt, lp, e1.re, e1.im, 1/r (odd stride)
+
+template <int NPC>
+__global__ void __launch_bounds__(kThreads, 4)
+cousin_tc_kernel(LevelDev L, PointsDev P, const double2* __restrict__ store, double k, Pipes pp,
+                 double2* __restrict__ Sp, double2* __restrict__ Dp) {
+    using LY = Layout<NPC>;
+    __shared__ double sgeo[kWarps][32 * kCG];
+    __shared__ double2 sacc[kWarps][32][2];
+    __shared__ int slist[kWarps][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int r = lane >> 2, tig = lane & 3;
+    const int wc = blockIdx.x * kWarps + warp;  // one warp item = <= 32 targets of one box
+    if (wc >= L.nwchunk) return;
+    const int tb = L.wchunk_box[wc];
+    const int tbeg = int(L.beg[tb]);
+    const int n_t = int(L.end[tb]) - tbeg;
+    const int q = L.wchunk_q0[wc] + lane;
+    const bool act = q < n_t;
+    const int t = act ? tbeg + q : tbeg;
+    const double x = P.x[t], y = P.y[t], z = P.z[t];
+    const double h = L.h;
+    sacc[warp][lane][0] = sacc[warp][lane][1] = make_double2(0.0, 0.0);
+    const int fpipe = tig < NPC ? pp.f[tig] : 0;  // factor code of the pipe this lane gathers
+    const int j0 = L.cz_ptr[tb], j1 = L.cz_ptr[tb + 1];
+    const std::int64_t ev0 = L.cev_begin[tb] + q;
+    double* mygeo = sgeo[warp] + lane * kCG;
+    for (int j = j0; j < j1; ++j) {
+        const int sb = L.cz_idx[j];
+        if (L.active && !L.active[sb]) continue;  // source box owned by another rank
+        const int so = act ? L.cev_seg[ev0 + std::int64_t(j - j0) * n_t] : -1;
+        if (act) {
+            const double vx = x - L.cx[sb], vy = y - L.cy[sb], vz = z - L.cz[sb];
+            const double r2 = fma(vx, vx, fma(vy, vy, vz * vz));
+            const double inv_r = rsqrt(r2);
+            const LocalCoords lc = local_coords(vx, vy, vz, inv_r, h, L.seg_gamma[so], L);
+            double sn, cs;
+            sincos_bounded(k * (r2 * inv_r), &sn, &cs);
+            const double f1 = kInv4PiD * inv_r;
+            mygeo[0] = lc.ls;
+            mygeo[1] = lc.lt;
+            mygeo[2] = lc.lp;
+            mygeo[3] = cs * f1;  // e^{ikr}/(4 pi r)
+            mygeo[4] = sn * f1;
+            mygeo[5] = inv_r;
+        }
+        __syncwarp();
+        unsigned pending = __ballot_sync(0xffffffffu, act);
+        while (pending) {
+            const int seg = __shfl_sync(0xffffffffu, so, __ffs(pending) - 1);
+            const unsigned gmask = __ballot_sync(0xffffffffu, act && so == seg);
+            pending &= ~gmask;
+            if ((gmask >> lane) & 1u) slist[warp][__popc(gmask & ((1u << lane) - 1u))] = lane;
+            __syncwarp();
+            const int count = __popc(gmask);
+            double bq[LY::NB];
+            load_b<NPC>(store + std::size_t(seg) * NPC * kNP, lane, bq);
+            for (int t0 = 0; t0 < count; t0 += 8) {
+                const bool valid = t0 + r < count;
+                const int src = valid ? slist[warp][t0 + r] : 0;
+                const double* gp = sgeo[warp] + src * kCG;
+                double d[LY::NQ][2];
+                tile_mma<NPC>(gp[0], gp[1], valid, tig, bq, d);
+                const double2 val = tile_gather<NPC>(gp[2], lane, d);
+                const double2 w = cmul(make_double2(gp[3], gp[4]), val);
+                double2 cS = make_double2(0.0, 0.0), cD = make_double2(0.0, 0.0);
+                switch (fpipe) {
+                    case 1: cS = w; break;
+                    case 2: cD = cscale(w, gp[5]); break;
+                    case 3: cD = make_double2(k * w.y, -k * w.x); break;  // -ik e^{ikr}/(4 pi r) val
+                    case 4: cD = w; break;
+                    default: break;
+                }
+#pragma unroll
+                for (int o = 1; o < 4; o <<= 1) {
+                    cS.x += __shfl_xor_sync(0xffffffffu, cS.x, o);
+                    cS.y += __shfl_xor_sync(0xffffffffu, cS.y, o);
+                    cD.x += __shfl_xor_sync(0xffffffffu, cD.x, o);
+                    cD.y += __shfl_xor_sync(0xffffffffu, cD.y, o);
+                }
+                if (valid && tig == 0) {
+                    sacc[warp][src][0] = cadd(sacc[warp][src][0], cS);
+                    sacc[warp][src][1] = cadd(sacc[warp][src][1], cD);
+                }
+            }
+            __syncwarp();
+        }
+    }
+    __syncwarp();
+    if (!act) return;
+    Sp[t] = cadd(Sp[t], sacc[warp][lane][0]);
+    Dp[t] = cadd(Dp[t], sacc[warp][lane][1]);
+}
+
+}  // namespace
+
+bool launch_cousin_eval_tc(const LevelDev& L, const PointsDev& P, const double2* store, double k, const Pipes& pipes,
+                           double2* Sp, double2* Dp, cudaStream_t st) {
+    if (L.ps != kPS || L.pang != kPA || pipes.n < 1 || pipes.n > 3) return false;
+    if (L.nwchunk == 0) return true;
+    const int grid = (L.nwchunk + kWarps - 1) / kWarps;
+    switch (pipes.n) {
+        case 1: cousin_tc_kernel<1><<<grid, kThreads, 0, st>>>(L, P, store, k, pipes, Sp, Dp); break;
+        case 2: cousin_tc_kernel<2><<<grid, kThreads, 0, st>>>(L, P, store, k, pipes, Sp, Dp); break;
+        default: cousin_tc_kernel<3><<<grid, kThreads, 0, st>>>(L, P, store, k, pipes, Sp, Dp); break;
+    }
+    IFGF_CUDA(cudaGetLastError());
+    return true;
+}
+
+}  // namespace ifgfb200

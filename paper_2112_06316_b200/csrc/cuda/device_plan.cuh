@@ -47,6 +47,8 @@ struct LevelDev {
     const std::uint8_t* active = nullptr;
     const std::int32_t *chunk_box = nullptr, *chunk_q0 = nullptr;  // cousin work chunks
     int nchunk = 0;
+    const std::int32_t *wchunk_box = nullptr, *wchunk_q0 = nullptr;  // 32-target warp items
+    int nwchunk = 0;
     int max_pts = 0;  // largest box
 };
 

@@ -72,7 +72,7 @@ class DevBuf {
 struct LevelBufs {
     DevBuf cx, cy, cz, beg, end, cz_ptr, cz_idx, cev_begin, cev_seg, seg_box, seg_gamma,
         box_seg_begin, pev_begin, pev_seg, pev_perm, pgrp_begin, pgrp_seg, pgrp_start, pgrp_count, ch_ptr, ch_idx, s_nodes, th_nodes, ph_nodes, th_sin, th_cos, ph_sin, ph_cos, thc_cos, thc_sin, phc_cos, phc_sin,
-        chunk_box, chunk_q0, tmpl_slot, tmpl, tmpl_gc;
+        chunk_box, chunk_q0, wchunk_box, wchunk_q0, tmpl_slot, tmpl, tmpl_gc;
 };
 
 Pipes make_pipes(const std::vector<int>& f) {
@@ -407,6 +407,18 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
                     chunk_box.push_back(std::int32_t(i));
                     chunk_q0.push_back(std::int32_t(q));
                 }
+        std::vector<std::int32_t> wchunk_box, wchunk_q0;  // one warp per 32 targets
+        for (std::size_t i = 0; i < nb; ++i)
+            if (R.cousin[d - 1].count(i) > 0)
+                for (std::uint32_t q = 0; q < B.end[i] - B.begin[i]; q += 32) {
+                    wchunk_box.push_back(std::int32_t(i));
+                    wchunk_q0.push_back(std::int32_t(q));
+                }
+        b.wchunk_box.upload(wchunk_box);
+        b.wchunk_q0.upload(wchunk_q0);
+        L.wchunk_box = b.wchunk_box.as<std::int32_t>();
+        L.wchunk_q0 = b.wchunk_q0.as<std::int32_t>();
+        L.nwchunk = int(wchunk_box.size());
         b.cx.upload(cx);
         b.cy.upload(cy);
         b.cz.upload(cz);

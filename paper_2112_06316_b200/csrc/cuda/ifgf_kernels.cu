@@ -14,6 +14,8 @@
 #include <algorithm>
 
 #include "dev_common.cuh"
+#include <cstdlib>
+
 #include "ifgf_device.cuh"
 #include "kernels.cuh"
 
@@ -363,6 +365,11 @@ void launch_leaf_fill(const LevelDev& L, const PointsDev& P, const double2* a_p,
 void launch_cousin_eval(const LevelDev& L, const PointsDev& P, const double2* store, double k,
                         const Pipes& pipes, double2* Sp, double2* Dp, cudaStream_t st) {
     if (L.nchunk == 0) return;
+    static const bool tc_off = [] {
+        const char* e = std::getenv("IFGF_COUSIN_TC");
+        return e && e[0] == '0';
+    }();
+    if (!tc_off && launch_cousin_eval_tc(L, P, store, k, pipes, Sp, Dp, st)) return;
     const bool def = L.ps == 3 && L.pang == 5;
     const std::size_t smem = std::size_t(kCousinThreads / 32) * kCousinSlots * pipes.n * L.ps * L.pang * L.pang *
                              sizeof(double2);

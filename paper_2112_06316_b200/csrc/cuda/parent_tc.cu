@@ -20,6 +20,7 @@
 // bitwise reproducible run to run.
 #include "ifgf_device.cuh"
 #include "kernels.cuh"
+#include "tc_common.cuh"
 
 namespace ifgfb200 {
 namespace {
@@ -27,18 +28,11 @@ namespace {
 using namespace dev;
 using namespace ifgfdev;
 
+using namespace tc;
+
 constexpr int kWarps = 4;
 constexpr int kGeo = 7;  // ls, lt, lp, ratio.re, ratio.im, extra factor, node (odd stride)
-constexpr int kPS = 3, kPA = 5, kNP = 75;
-constexpr int kKS = kPA - 1;  // DMMA k-steps over the 15 (s, theta) pairs (4 x 4 slots)
-static_assert(kPS == 3 && kPA == 5, "the k-slot map below assumes 3 x 5 (s, theta) pairs");
 constexpr int kGeoSz = kNP * kGeo + 1;  // keeps the accumulators 16-byte aligned
-
-__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                 : "+d"(d0), "+d"(d1)
-                 : "d"(a), "d"(b));
-}
 
 // Child->parent pipe combinations of the strategies (ifgf.cpp:525-555). Each child pipe
 // feeds one parent pipe with one factor: R1 = ratio1, RI = ratio1/r_c (W2 -> W4),
@@ -109,30 +103,7 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
     const double pcx = Lp.cx[pb], pcy = Lp.cy[pb], pcz = Lp.cz[pb];
 
     const int r = lane >> 2, tig = lane & 3;
-    // B column n = lane >> 2 = 2 c + re/im; column pair c of accumulator group q holds one
-    // (pipe, phi index). 3 pipes: c < 3 -> (c, q) for q = 0..3 and c = 3 -> (q, 4), i.e.
-    // 15 pairs in 4 groups; fewer pipes: IPG = 4 / pipes phi indices per group,
-    // c = pipes * sub + pipe -> (pipe, IPG q + sub).
-    constexpr int IPG = 4 / NPC;
-    constexpr int NQ = NPC == 3 ? 4 : (kPA + IPG - 1) / IPG;
-    const int ncol = lane >> 2, bc = ncol >> 1, reim = ncol & 1;
-    auto pair_of = [](int q, int c, int& pipe, int& ip) -> bool {
-        if constexpr (NPC == 3) {
-            if (c < 3) {
-                pipe = c;
-                ip = q;
-                return true;
-            }
-            pipe = q;
-            ip = kPA - 1;
-            return q < 3;
-        } else {
-            const int sub = c / NPC;
-            pipe = c % NPC;
-            ip = IPG * q + sub;
-            return sub < IPG && ip < kPA;
-        }
-    };
+    using LY = Layout<NPC>;
     const int gb = Lc.pgrp_begin[so], ge = Lc.pgrp_begin[so + 1];
     for (int g = gb; g < ge; ++g) {
         const int cso = Lc.pgrp_seg[g];
@@ -189,86 +160,15 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
         }
         __syncwarp();
         // 2. 8-evaluation tensor-core tiles against the child block
-        // B fragments of the group's block: k runs over the 15 (s, theta) index pairs in 4
-        // steps of 4: slot (j, tig) holds (is, it) = (tig, j) for tig < 3 and (j, 4) for
-        // tig = 3 (slot (3, 3) is padding); one accumulator per phi group. Loaded once per
-        // group, reused by all its tiles.
-        const double* blk = reinterpret_cast<const double*>(cstore + std::size_t(cso) * NPC * kNP) + reim;
-        const bool lo = tig < kPS;
-        double bq[kKS * NQ];
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            int pipe, ip;
-            const bool live = pair_of(q, bc, pipe, ip);
-#pragma unroll
-            for (int j = 0; j < kKS; ++j) {
-                const int is = lo ? tig : j, it = lo ? j : kPA - 1;
-                bq[q * kKS + j] = (live && (lo || j < kPS))
-                                      ? __ldg(blk + 2 * (pipe * kNP + is + kPS * (it + kPA * ip)))
-                                      : 0.0;
-            }
-        }
+        // B fragments of the group's block, reused by all its tiles (tc_common.cuh)
+        double bq[LY::NB];
+        load_b<NPC>(cstore + std::size_t(cso) * NPC * kNP, lane, bq);
         for (int t0 = 0; t0 < count; t0 += 8) {
             const bool valid = t0 + r < count;
             const double* gp = geo + (valid ? t0 + r : 0) * kGeo;
-            double ts[kPS], tt[kPA];
-            cheb_row<kPS>(gp[0], ts);
-            cheb_row<kPA>(gp[1], tt);
-            // lane-constant operand choice: T_tig(s) for the first three k columns, T_4(theta)
-            // for the fourth (zero rows past the group's end)
-            double tsel = tig == 0 ? ts[0] : (tig == 1 ? ts[1] : ts[2]);
-            double t4 = tt[kPA - 1];
-            if (!valid) tsel = t4 = 0.0;
-            double d[NQ][2];
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) d[q][0] = d[q][1] = 0.0;
-#pragma unroll
-            for (int j = 0; j < kKS; ++j) {
-                const double x = lo ? tsel : (j < kPS ? ts[j] : 0.0);
-                const double y = lo ? tt[j] : t4;
-                const double a = x * y;
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) dmma884(d[q][0], d[q][1], a, bq[q * kKS + j]);
-            }
-            // 3. lane (r, tig) holds columns 2 tig, 2 tig + 1 of each group = (re, im) of the
-            // pair (pipe, phi index) of column pair tig: weight by T(phi), gather the pipes
-            double tq[kPA];
-            cheb_row<kPA>(gp[2], tq);
-            double2 val = make_double2(0.0, 0.0);
-            if constexpr (NPC == 3) {
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) {
-                    val.x = fma(tq[q], d[q][0], val.x);
-                    val.y = fma(tq[q], d[q][1], val.y);
-                }
-                // phi index 4 of pipe q sits in lane 3 of the quad, group q
-                const int src = (lane & ~3) | 3;
-#pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    const double ex = __shfl_sync(0xffffffffu, d[q][0], src);
-                    const double ey = __shfl_sync(0xffffffffu, d[q][1], src);
-                    if (tig == q) {
-                        val.x = fma(tq[kPA - 1], ex, val.x);
-                        val.y = fma(tq[kPA - 1], ey, val.y);
-                    }
-                }
-            } else {
-                const int sub = tig / NPC;
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) {
-                    double w = 0.0;
-#pragma unroll
-                    for (int s = 0; s < IPG; ++s)
-                        if (IPG * q + s < kPA && sub == s) w = tq[IPG * q + s];
-                    val.x = fma(w, d[q][0], val.x);
-                    val.y = fma(w, d[q][1], val.y);
-                }
-#pragma unroll
-                for (int off = NPC; off < NPC * IPG; off <<= 1) {
-                    val.x += __shfl_down_sync(0xffffffffu, val.x, off);
-                    val.y += __shfl_down_sync(0xffffffffu, val.y, off);
-                }
-            }
+            double d[LY::NQ][2];
+            tile_mma<NPC>(gp[0], gp[1], valid, tig, bq, d);
+            const double2 val = tile_gather<NPC>(gp[2], lane, d);
             // lanes tig < NPC now hold (re, im) of child pipe tig for evaluation row r
             const double2 r1 = make_double2(gp[3], gp[4]);
             const double xf = gp[5];
