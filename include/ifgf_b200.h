@@ -26,6 +26,10 @@
  *   ifgf_gmres_solve        gmres_solve(std::function apply, ...)      solver.hpp:94-95
  *   ifgf_solve              solve(mesh, incident, cfg)                 solver.hpp:111-112
  *   ifgf_plan_diagnostics   ConePlan::diagnostics                      ifgf.hpp:74
+ *   ifgf_far_field          far_field (+ FarFieldGrid::make)           postprocess.hpp:34-37
+ *   ifgf_near_field         near_field                                 postprocess.hpp:39-41
+ *   ifgf_mie_far_field      mie_far_field                              postprocess.hpp:44-45
+ *   ifgf_eps_metric         eps_far / eps_near                         postprocess.hpp:49-52
  */
 #ifndef IFGF_B200_H
 #define IFGF_B200_H
@@ -189,6 +193,25 @@ int ifgf_gmres_solve(ifgf_operator* op, const double* rhs, double tol, int max_i
 int ifgf_solve(ifgf_operator* op, double theta, double phi, double tol, int max_iter,
                int restart, double* density, double* history, int history_cap,
                int* iterations, int* converged);
+
+/* ---- fields after the solve (postprocess.cpp). The dense sums run on
+ * GPU `device` over the oversampled per-patch Fejér quadrature of the density. ---- */
+/* far-field pattern on the (n_phi x n_theta) grid, polar index fastest (postprocess.cpp:62-104):
+ * dirs (3*n_phi*n_theta, may be NULL) and values (2*n_phi*n_theta) */
+int ifgf_far_field(const ifgf_surface* s, const double* density, double gamma, double k, int n_phi,
+                   int n_theta, int device, double* dirs, double* values);
+/* scattered / total field at npts points (3*npts) for plane-wave incidence (theta, phi) or,
+ * when nsrc > 0, point sources src (3*nsrc, solver.cpp:25-35); flagged[i] = 1 within
+ * flag_distance of the quadrature or inside the scatterer (postprocess.cpp:106-139) */
+int ifgf_near_field(const ifgf_surface* s, const double* density, double gamma, double k,
+                    double inc_theta, double inc_phi, const double* src, int64_t nsrc,
+                    const double* points, int64_t npts, double flag_distance, int device,
+                    double* scattered, double* total, uint8_t* flagged);
+/* sound-soft sphere far field for a plane wave along direction (3) at n directions (3*n) */
+int ifgf_mie_far_field(double radius, double k, const double* direction, const double* dirs,
+                       int64_t n, int extra_terms, double* values);
+/* max | |ref| - |apx| | / |ref| over nonzero ref (complex interleaved, length 2n) */
+int ifgf_eps_metric(const double* ref, const double* apx, int64_t n, double* eps, int* skipped);
 
 #ifdef __cplusplus
 }

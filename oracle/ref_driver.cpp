@@ -13,6 +13,7 @@
 //   rp_singular_apply                     src/rp.cpp:421-451
 //   gmres_solve / solve                   src/solver.cpp:270-340
 //   save_beta_cache                       src/rp.cpp:515-536
+//   far_field / near_field / mie_far_field src/postprocess.cpp:83-205
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -24,6 +25,7 @@
 
 #include "ifgf/geometry.hpp"
 #include "ifgf/ifgf.hpp"
+#include "ifgf/postprocess.hpp"
 #include "ifgf/rp.hpp"
 #include "ifgf/solver.hpp"
 
@@ -450,6 +452,56 @@ int ref_solve(void* mesh, double k, double gamma, double theta, double phi, doub
         for (int i = 0; i < int(res.residual_history.size()) && i < hist_cap; ++i)
             hist_out[i] = res.residual_history[i];
         return res.iterations;
+    } catch (const std::exception& e) {
+        return -fail(e);
+    }
+}
+
+// postprocess (postprocess.hpp:34-52)
+int ref_far_field(void* mesh, const double* density, double gamma, double k, int n_phi, int n_theta,
+                  double* dirs, double* values) {
+    try {
+        const auto phi = to_cplx(density, M(mesh).size());
+        const FarFieldGrid g = far_field(M(mesh), phi, gamma, k, n_phi, n_theta, 0);
+        for (std::size_t i = 0; i < g.directions.size(); ++i) {
+            dirs[3 * i] = g.directions[i].x;
+            dirs[3 * i + 1] = g.directions[i].y;
+            dirs[3 * i + 2] = g.directions[i].z;
+        }
+        from_cplx(g.values, values);
+        return 0;
+    } catch (const std::exception& e) {
+        return -fail(e);
+    }
+}
+
+int ref_near_field(void* mesh, const double* density, double gamma, double k, double theta, double phi,
+                   const double* points, long npts, double flag_distance, double* scattered, double* total,
+                   unsigned char* flagged) {
+    try {
+        const auto dens = to_cplx(density, M(mesh).size());
+        std::vector<Vec3> pts(npts);
+        for (long i = 0; i < npts; ++i) pts[i] = {points[3 * i], points[3 * i + 1], points[3 * i + 2]};
+        IncidentField inc;
+        inc.theta = theta;
+        inc.phi = phi;
+        const NearFieldGrid g = near_field(M(mesh), dens, gamma, k, inc, pts, flag_distance, 0);
+        from_cplx(g.scattered, scattered);
+        from_cplx(g.total, total);
+        for (long i = 0; i < npts; ++i) flagged[i] = g.flagged[i];
+        return 0;
+    } catch (const std::exception& e) {
+        return -fail(e);
+    }
+}
+
+int ref_mie_far_field(double radius, double k, const double* direction, const double* dirs, long n,
+                      int extra, double* values) {
+    try {
+        std::vector<Vec3> d(n);
+        for (long i = 0; i < n; ++i) d[i] = {dirs[3 * i], dirs[3 * i + 1], dirs[3 * i + 2]};
+        from_cplx(mie_far_field(radius, k, {direction[0], direction[1], direction[2]}, d, extra), values);
+        return 0;
     } catch (const std::exception& e) {
         return -fail(e);
     }

@@ -13,6 +13,7 @@
 #include "../../include/ifgf_b200.h"
 #include "engine.hpp"
 #include "host/chebyshev.hpp"
+#include "fields_gpu.hpp"
 #include "host/gmres.hpp"
 
 #ifdef _OPENMP
@@ -946,6 +947,100 @@ int ifgf_solve(ifgf_operator* op, double theta, double phi, double tol, int max_
             throw ConvergenceFailure("solve: GMRES did not reach tolerance " + std::to_string(tol) + " in " +
                                          std::to_string(it) + " iterations",
                                      {});
+    });
+}
+
+// ------------------------------------------------------------------ fields
+int ifgf_far_field(const ifgf_surface* s, const double* density, double gamma, double k, int n_phi, int n_theta,
+                   int device, double* dirs, double* values) {
+    return guarded([&] {
+        need(s, "surface");
+        need(density, "density");
+        need(values, "values");
+        if (k <= 0) throw InvalidArgument("far_field: wavenumber must be positive");
+        const Surface& S = *s->s;
+        const auto phi = as_cplx(density, S.size());
+        const FineQuad q = oversample_for_fields(S, phi.data(), k);
+        const std::vector<Vec3> d = far_field_directions(n_phi, n_theta);
+        gpu_far_field(q, d, k, gamma, device, reinterpret_cast<cplx*>(values));
+        if (dirs)
+            for (std::size_t i = 0; i < d.size(); ++i) {
+                dirs[3 * i] = d[i].x;
+                dirs[3 * i + 1] = d[i].y;
+                dirs[3 * i + 2] = d[i].z;
+            }
+    });
+}
+
+int ifgf_near_field(const ifgf_surface* s, const double* density, double gamma, double k, double inc_theta,
+                    double inc_phi, const double* src, int64_t nsrc, const double* points, int64_t npts,
+                    double flag_distance, int device, double* scattered, double* total, uint8_t* flagged) {
+    return guarded([&] {
+        need(s, "surface");
+        need(density, "density");
+        if (npts > 0) {
+            need(points, "points");
+            need(scattered, "scattered");
+            need(total, "total");
+            need(flagged, "flagged");
+        }
+        if (nsrc > 0) need(src, "point sources");
+        if (k <= 0) throw InvalidArgument("near_field: wavenumber must be positive");
+        const Surface& S = *s->s;
+        const auto phi = as_cplx(density, S.size());
+        const FineQuad q = oversample_for_fields(S, phi.data(), k);
+        std::vector<Vec3> pts(std::size_t(std::max<int64_t>(npts, 0)));
+        for (std::size_t i = 0; i < pts.size(); ++i) pts[i] = {points[3 * i], points[3 * i + 1], points[3 * i + 2]};
+        std::vector<double> dmin(pts.size()), gauss(pts.size());
+        cplx* sc = reinterpret_cast<cplx*>(scattered);
+        gpu_near_field(q, pts, k, gamma, device, sc, dmin.data(), gauss.data());
+        // incident field (solver.cpp:25-35)
+        const Vec3 dir{std::cos(inc_theta) * std::sin(inc_phi), std::sin(inc_theta) * std::sin(inc_phi),
+                       std::cos(inc_phi)};
+        for (std::size_t i = 0; i < pts.size(); ++i) {
+            cplx inc{};
+            if (nsrc > 0) {
+                for (int64_t j = 0; j < nsrc; ++j) {
+                    const Vec3 y{src[3 * j], src[3 * j + 1], src[3 * j + 2]};
+                    const double r = len(pts[i] - y);
+                    if (r < 1e-12) throw InvalidArgument("incident_at: point source coincides with node");
+                    inc += std::polar(1.0 / r, k * r);
+                }
+            } else {
+                inc = std::polar(1.0, k * dot3(dir, pts[i]));
+            }
+            const cplx t = sc[i] + inc;
+            total[2 * i] = t.real();
+            total[2 * i + 1] = t.imag();
+            flagged[i] = (dmin[i] <= flag_distance || gauss[i] < -0.5) ? 1 : 0;
+        }
+    });
+}
+
+int ifgf_mie_far_field(double radius, double k, const double* direction, const double* dirs, int64_t n,
+                       int extra_terms, double* values) {
+    return guarded([&] {
+        need(direction, "direction");
+        if (n > 0) {
+            need(dirs, "directions");
+            need(values, "values");
+        }
+        std::vector<Vec3> d(std::size_t(std::max<int64_t>(n, 0)));
+        for (std::size_t i = 0; i < d.size(); ++i) d[i] = {dirs[3 * i], dirs[3 * i + 1], dirs[3 * i + 2]};
+        const auto v = mie_far_field(radius, k, {direction[0], direction[1], direction[2]}, d, extra_terms);
+        if (!v.empty()) std::memcpy(values, v.data(), v.size() * sizeof(cplx));
+    });
+}
+
+int ifgf_eps_metric(const double* ref, const double* apx, int64_t n, double* eps, int* skipped) {
+    return guarded([&] {
+        need(eps, "eps");
+        if (n > 0) {
+            need(ref, "reference");
+            need(apx, "approximation");
+        }
+        *eps = eps_metric(reinterpret_cast<const cplx*>(ref), reinterpret_cast<const cplx*>(apx),
+                          std::size_t(std::max<int64_t>(n, 0)), skipped);
     });
 }
 
