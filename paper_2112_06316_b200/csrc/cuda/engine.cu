@@ -531,10 +531,11 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
 
     // ---- parent-fill geometry templates where a level's cone cells are reused by many
     // parent segments (at least 8 evaluations per template entry); IFGF_PARENT_TEMPLATES=0
-    // turns them off
+    // turns them off, =force builds them on every level (tests)
     {
         const char* env = std::getenv("IFGF_PARENT_TEMPLATES");
         const bool enabled = !(env && std::string(env) == "0");
+        const bool force = env && std::string(env) == "force";
         for (int d = 4; enabled && d <= T.depth; ++d) {
             const ConeLevel& PL = C.level[d - 2];
             const ConeLevel& CL = C.level[d - 1];
@@ -546,7 +547,7 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
                     gammas.push_back(g);
                 }
             const std::size_t entries = gammas.size() * 8 * std::size_t(PL.nodes_per_seg());
-            if (entries * 8 > CL.pev_perm.size() || entries * 64 > (std::size_t(2) << 30)) continue;
+            if (!force && (entries * 8 > CL.pev_perm.size() || entries * 64 > (std::size_t(2) << 30))) continue;
             std::vector<double> tab;
             std::vector<std::int32_t> gc;
             parent_templates(T, C, d, gammas, 0, tab, gc);

@@ -1,0 +1,55 @@
+"""Parity of the kernel variants the default cases do not reach: non-default interpolation
+orders (generic leaf / cousin / parent kernels), forced parent-fill geometry templates,
+the per-lane cousin kernel, and a stretched spheroid (cfg4's geometry class: elongated
+patches, different pipe plans per level)."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2112_06316_b200 as P
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.mark.parametrize("ps,pang", [(2, 4), (4, 6), (3, 7)])
+def test_nondefault_orders(ref, ps, pang):
+    pm = P.SurfaceMesh.sphere(1.0, 1, 6, 6)
+    rm = ref.RefMesh.sphere(1.0, 1, 6, 6)
+    k = 2 * np.pi
+    op = P.CombinedOperator(pm, P.SolveConfig(k=k, cone=P.ConeConfig(ps=ps, pang=pang)))
+    ro = ref.RefOperator(rm, k, ps=ps, pang=pang)
+    phi = P.random_density(pm.size(), 1)
+    assert rel_l2(op.apply(phi), ro.apply(phi)) <= TOL
+
+
+@pytest.mark.parametrize("env,value", [("IFGF_PARENT_TEMPLATES", "force"), ("IFGF_PARENT_TEMPLATES", "0"),
+                                       ("IFGF_COUSIN_TC", "0")])
+@pytest.mark.parametrize("splits,nu,k", [(2, 6, 4 * np.pi), (2, 16, 4 * np.pi), (3, 6, 8 * np.pi)])
+def test_kernel_variants(ref, monkeypatch, env, value, splits, nu, k):
+    monkeypatch.setenv(env, value)  # read when the operator (and its kernels) are set up
+    pm = P.SurfaceMesh.sphere(1.0, splits, nu, nu)
+    rm = ref.RefMesh.sphere(1.0, splits, nu, nu)
+    op = P.CombinedOperator(pm, P.SolveConfig(k=k))
+    ro = ref.RefOperator(rm, k)
+    phi = P.random_density(pm.size(), 2)
+    assert rel_l2(op.apply(phi), ro.apply(phi)) <= TOL
+
+
+@pytest.mark.parametrize("axes,k", [((4.0, 1.0, 1.0), 2 * np.pi), ((2.5, 0.6, 1.2), 3 * np.pi)])
+def test_spheroid_parity(ref, axes, k):
+    pm = P.SurfaceMesh.spheroid(2, 8, 8, *axes)
+    rm = ref.RefMesh.spheroid(2, 8, 8, *axes)
+    op = P.CombinedOperator(pm, P.SolveConfig(k=k))
+    ro = ref.RefOperator(rm, k)
+    phi = P.random_density(pm.size(), 3)
+    S, D = op.layer_potentials(phi)
+    rS, rD = ro.layer_potentials(phi)
+    assert rel_l2(S, rS) <= TOL and rel_l2(D, rD) <= TOL
+    assert rel_l2(op.apply(phi), ro.apply(phi)) <= TOL
