@@ -13,6 +13,8 @@
 #include "../../include/ifgf_b200.h"
 #include "engine.hpp"
 #include "host/chebyshev.hpp"
+#include <cuda_runtime.h>
+
 #include "fields_gpu.hpp"
 #include "host/gmres.hpp"
 
@@ -126,7 +128,14 @@ std::shared_ptr<ifgf_plan> make_plan(std::shared_ptr<const Surface> s, const ifg
     rp.delta_abs = c.delta_abs;
     rp.n_beta = c.n_beta;
     rp.cov_d = c.cov_d;
-    p->pairs = classify_pairs(*s, p->tree, p->rel, rp, c.workers);
+    // closest-point searches on the GPU when one is there (bitwise equal to the host's)
+    int ndev = 0;
+    const bool gpu = c.device >= 0 && cudaGetDeviceCount(&ndev) == cudaSuccess && c.device < ndev;
+    if (!gpu) cudaGetLastError();  // clear a no-device error
+    const int dev = c.device;
+    const ClosestPointBatch batch = [dev](const Surface& sf, const std::vector<ClosestPointRequest>& rq,
+                                          std::vector<ClosestPoint>& out) { gpu_closest_points(sf, rq, out, dev); };
+    p->pairs = classify_pairs(*s, p->tree, p->rel, rp, c.workers, gpu ? &batch : nullptr);
     p->t_pairs = lap();
     p->strategy = c.strategy == 0 ? DlStrategy::W4 : (c.strategy == 1 ? DlStrategy::W2W3 : DlStrategy::Hybrid);
     if (p->strategy == DlStrategy::Hybrid) {  // solver.cpp:55-62

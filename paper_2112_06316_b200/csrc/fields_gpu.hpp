@@ -1,10 +1,12 @@
-// GPU field sums over an oversampled surface quadrature (cuda/fields.cu); plain C++
-// interface for the C-ABI layer.
+// GPU helpers called from the host setup / C-ABI layer, plain C++ interface: field sums
+// over an oversampled surface quadrature (cuda/fields.cu) and the batched closest-point
+// searches of the pair classification (cuda/proximity_kernels.cu).
 #pragma once
 
 #include <vector>
 
 #include "host/fields.hpp"
+#include "host/proximity.hpp"
 
 namespace ifgfb200 {
 
@@ -14,5 +16,8 @@ void gpu_far_field(const FineQuad& q, const std::vector<Vec3>& dirs, double k, d
 // (postprocess.cpp:106-139; the caller adds the incident field and sets the flags)
 void gpu_near_field(const FineQuad& q, const std::vector<Vec3>& pts, double k, double gamma, int device,
                     cplx* scattered, double* dmin, double* gauss);
+// closest_point_on for every non-own request, bit for bit (ClosestPointBatch)
+void gpu_closest_points(const Surface& s, const std::vector<ClosestPointRequest>& req, std::vector<ClosestPoint>& res,
+                        int device);
 
 }  // namespace ifgfb200

@@ -1,68 +1,13 @@
 #include "proximity.hpp"
 
+#include "closest_point.hpp"
+
 #include <algorithm>
 #include <limits>
 
 namespace ifgfb200 {
 
 namespace {
-
-constexpr double kInvGolden = 0.6180339887498949;
-constexpr double kSearchTol = 1e-12;
-constexpr int kSweeps = 50;
-
-// Clenshaw of one u-line, then of the v-column (chebyshev.cpp:12-25, 63-74); stack storage,
-// identical operation order to cheb::eval_2d.
-inline double series_at(const double* c, int du, int dv, double u, double v) {
-    double row[64] = {};
-    for (int j = 0; j < dv; ++j) {
-        const double* a = c + std::size_t(du) * j;
-        double b1 = 0, b2 = 0;
-        for (int i = du - 1; i >= 1; --i) {
-            const double b0 = a[i] + 2.0 * u * b1 - b2;
-            b2 = b1;
-            b1 = b0;
-        }
-        row[j] = a[0] + u * b1 - b2;
-    }
-    double b1 = 0, b2 = 0;
-    for (int j = dv - 1; j >= 1; --j) {
-        const double b0 = row[j] + 2.0 * v * b1 - b2;
-        b2 = b1;
-        b1 = b0;
-    }
-    return row[0] + v * b1 - b2;
-}
-
-inline double dist2_to(const Patch& p, const Vec3& x, double u, double v) {
-    const Vec3 y{series_at(p.pos_c[0].data(), p.du, p.dv, u, v),
-                 series_at(p.pos_c[1].data(), p.du, p.dv, u, v),
-                 series_at(p.pos_c[2].data(), p.du, p.dv, u, v)};
-    return len2(x - y);
-}
-
-template <class F>
-double golden(F&& f, double a, double b) {
-    double c = b - (b - a) * kInvGolden;
-    double d = a + (b - a) * kInvGolden;
-    double fc = f(c), fd = f(d);
-    while (b - a > kSearchTol) {
-        if (fc < fd) {
-            b = d;
-            d = c;
-            fd = fc;
-            c = b - (b - a) * kInvGolden;
-            fc = f(c);
-        } else {
-            a = c;
-            c = d;
-            fc = fd;
-            d = a + (b - a) * kInvGolden;
-            fd = f(d);
-        }
-    }
-    return 0.5 * (a + b);
-}
 
 std::uint64_t fnv(const void* data, std::size_t n, std::uint64_t h) {
     const auto* b = static_cast<const unsigned char*>(data);
@@ -76,15 +21,11 @@ std::uint64_t fnv(const void* data, std::size_t n, std::uint64_t h) {
 }  // namespace
 
 ClosestPoint closest_point_on(const Patch& p, const Vec3& x, double u0, double v0) {
-    if (p.du > 64 || p.dv > 64) throw InvalidArgument("closest point: series extent above 64");
-    double u = std::clamp(u0, -1.0, 1.0), v = std::clamp(v0, -1.0, 1.0);
-    for (int sweep = 0; sweep < kSweeps; ++sweep) {
-        const double u_prev = u, v_prev = v;
-        u = golden([&](double q) { return dist2_to(p, x, q, v); }, -1.0, 1.0);
-        v = golden([&](double q) { return dist2_to(p, x, u, q); }, -1.0, 1.0);
-        if (std::abs(u - u_prev) < kSearchTol && std::abs(v - v_prev) < kSearchTol) break;
-    }
-    return {u, v, std::sqrt(dist2_to(p, x, u, v))};
+    if (p.du > cp::kMaxExtent || p.dv > cp::kMaxExtent) throw InvalidArgument("closest point: series extent above 64");
+    const cp::PatchSeries ps{p.pos_c[0].data(), p.pos_c[1].data(), p.pos_c[2].data(), p.du, p.dv};
+    ClosestPoint out;
+    cp::solve(ps, x.x, x.y, x.z, u0, v0, out.u, out.v, out.dist);
+    return out;
 }
 
 double grade_w(double tau, int d) {
@@ -138,7 +79,7 @@ double grade_xi_deriv(double alpha, double tau, int d) {
 }
 
 PairList classify_pairs(const Surface& s, const BoxTree& t, const BoxRelations& rel,
-                        const RpParams& cfg, int workers) {
+                        const RpParams& cfg, int workers, const ClosestPointBatch* batch) {
     if (cfg.n_beta < 2 || cfg.cov_d < 2)
         throw InvalidArgument("classify_targets: n_beta >= 2 and cov_d >= 2 required");
     const std::size_t n = s.size();
@@ -168,6 +109,10 @@ PairList classify_pairs(const Surface& s, const BoxTree& t, const BoxRelations& 
     };
     std::vector<std::vector<Found>> per(n);
     const int w = worker_count(workers);
+    // (1) per target: candidate patches of the neighbour leaves; the own patch is a pair at
+    // the node's parameters, others need a closest-point search unless the nearest node is
+    // already beyond delta + spacing
+    std::vector<std::vector<ClosestPointRequest>> req(n);
 #pragma omp parallel for schedule(dynamic, 64) num_threads(w)
     for (std::int64_t l = 0; l < std::int64_t(n); ++l) {
         const std::int32_t tb = t.leaf_of[l];
@@ -179,28 +124,60 @@ PairList classify_pairs(const Surface& s, const BoxTree& t, const BoxRelations& 
         cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
         const Vec3 x = s.pos[l];
         for (std::int32_t q : cand) {
-            Found f;
-            f.q = q;
             if (q == s.patch_of[l]) {
-                f.u = s.pu[l];
-                f.v = s.pv[l];
-            } else {
-                double best = std::numeric_limits<double>::max();
-                std::size_t arg = s.patch_start[q];
-                for (std::size_t m = s.patch_start[q]; m < s.patch_start[q + 1]; ++m) {
-                    const double d2 = len2(s.pos[m] - x);
-                    if (d2 < best) {
-                        best = d2;
-                        arg = m;
-                    }
-                }
-                if (std::sqrt(best) > out.delta[q] + spacing[q]) continue;
-                const ClosestPoint cp = closest_point_on(s.patches[q], x, s.pu[arg], s.pv[arg]);
-                if (cp.dist > out.delta[q]) continue;
-                f.u = cp.u;
-                f.v = cp.v;
+                req[l].push_back({std::uint32_t(l), q, s.pu[l], s.pv[l], true});
+                continue;
             }
-            for (std::size_t m = s.patch_start[q]; m < s.patch_start[q + 1]; ++m)
+            double best = std::numeric_limits<double>::max();
+            std::size_t arg = s.patch_start[q];
+            for (std::size_t m = s.patch_start[q]; m < s.patch_start[q + 1]; ++m) {
+                const double d2 = len2(s.pos[m] - x);
+                if (d2 < best) {
+                    best = d2;
+                    arg = m;
+                }
+            }
+            if (std::sqrt(best) > out.delta[q] + spacing[q]) continue;
+            req[l].push_back({std::uint32_t(l), q, s.pu[arg], s.pv[arg], false});
+        }
+    }
+    // (2) the closest-point searches, batched (GPU when given, else host threads)
+    std::vector<ClosestPointRequest> flat;
+    std::vector<std::size_t> off(n + 1, 0);
+    for (std::size_t l = 0; l < n; ++l) off[l + 1] = off[l] + req[l].size();
+    flat.reserve(off[n]);
+    for (std::size_t l = 0; l < n; ++l) {
+        flat.insert(flat.end(), req[l].begin(), req[l].end());
+        req[l].clear();
+        req[l].shrink_to_fit();
+    }
+    std::vector<ClosestPoint> res(flat.size());
+    if (batch) {
+        (*batch)(s, flat, res);
+    } else {
+#pragma omp parallel for schedule(dynamic, 16) num_threads(w)
+        for (std::int64_t i = 0; i < std::int64_t(flat.size()); ++i)
+            if (!flat[i].own)
+                res[i] = closest_point_on(s.patches[flat[i].q], s.pos[flat[i].target], flat[i].u0, flat[i].v0);
+    }
+    // (3) pairs within delta, with the far-node correction lists
+#pragma omp parallel for schedule(dynamic, 64) num_threads(w)
+    for (std::int64_t l = 0; l < std::int64_t(n); ++l) {
+        const std::int32_t tb = t.leaf_of[l];
+        const auto nb0 = nbr.idx.begin() + nbr.ptr[tb], nb1 = nbr.idx.begin() + nbr.ptr[tb + 1];
+        for (std::size_t i = off[l]; i < off[l + 1]; ++i) {
+            const ClosestPointRequest& r = flat[i];
+            Found f;
+            f.q = r.q;
+            if (r.own) {
+                f.u = r.u0;
+                f.v = r.v0;
+            } else {
+                if (res[i].dist > out.delta[r.q]) continue;
+                f.u = res[i].u;
+                f.v = res[i].v;
+            }
+            for (std::size_t m = s.patch_start[r.q]; m < s.patch_start[r.q + 1]; ++m)
                 if (!std::binary_search(nb0, nb1, t.leaf_of[m])) f.far.push_back(std::uint32_t(m));
             per[l].push_back(std::move(f));
         }

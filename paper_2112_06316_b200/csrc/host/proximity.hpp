@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <vector>
 
 #include "boxtree.hpp"
@@ -36,8 +37,21 @@ struct ClosestPoint {
 };
 ClosestPoint closest_point_on(const Patch& p, const Vec3& x, double u0, double v0);
 
+// one closest-point search of classify_pairs: target node, patch, start parameters (the
+// nearest node's); `own` pairs (the target's own patch) need no search
+struct ClosestPointRequest {
+    std::uint32_t target;
+    std::int32_t q;
+    double u0, v0;
+    bool own;
+};
+// batched solver for the non-own requests (the GPU one: cuda/proximity_kernels.cu); must
+// return closest_point_on's results bit for bit
+using ClosestPointBatch = std::function<void(const Surface&, const std::vector<ClosestPointRequest>&,
+                                             std::vector<ClosestPoint>&)>;
+
 PairList classify_pairs(const Surface& s, const BoxTree& t, const BoxRelations& rel,
-                        const RpParams& cfg, int workers);
+                        const RpParams& cfg, int workers, const ClosestPointBatch* batch = nullptr);
 
 // graded change of variables (rp.cpp:139-192)
 double grade_w(double tau, int d);

@@ -53,3 +53,19 @@ def test_spheroid_parity(ref, axes, k):
     rS, rD = ro.layer_potentials(phi)
     assert rel_l2(S, rS) <= TOL and rel_l2(D, rD) <= TOL
     assert rel_l2(op.apply(phi), ro.apply(phi)) <= TOL
+
+
+@pytest.mark.parametrize("mesh", ["sphere", "spheroid"])
+def test_gpu_closest_points_bitwise(ref, mesh):
+    # pair classification with the golden-section searches batched on the GPU equals the
+    # host restatement and the reference bit for bit (pairs, ubar/vbar, far lists)
+    if mesh == "sphere":
+        pm, rm, k = P.SurfaceMesh.sphere(1.0, 2, 16, 16), ref.RefMesh.sphere(1.0, 2, 16, 16), 4 * np.pi
+    else:
+        pm, rm, k = P.SurfaceMesh.spheroid(2, 8, 8, 4.0, 1.0, 1.0), ref.RefMesh.spheroid(2, 8, 8, 4.0, 1.0, 1.0), 2 * np.pi
+    gpu = P.HostPlan(pm, P.SolveConfig(k=k, device=0)).proximity()
+    cpu = P.HostPlan(pm, P.SolveConfig(k=k, device=-1)).proximity()
+    theirs = ref.RefOperator(rm, k, n_beta=8).proximity()
+    for key in theirs:
+        assert np.array_equal(gpu[key], theirs[key]), key
+        assert np.array_equal(cpu[key], theirs[key]), key
