@@ -23,7 +23,7 @@ using namespace ifgfdev;
 using namespace tc;
 
 constexpr int kThreads = 128, kWarps = kThreads / 32;
-constexpr int kCG = 7;  // ls, lt, lp, e1.re, e1.im, 1/r (odd stride)
+constexpr int kCG = kRowLen + 4;  // A slots, T(phi), e1.re, e1.im, 1/r, pad (odd stride)
 
 template <int NPC>
 __global__ void __launch_bounds__(kThreads, 4)
@@ -62,12 +62,10 @@ cousin_tc_kernel(LevelDev L, PointsDev P, const double2* __restrict__ store, dou
             double sn, cs;
             sincos_bounded(k * (r2 * inv_r), &sn, &cs);
             const double f1 = kInv4PiD * inv_r;
-            mygeo[0] = lc.ls;
-            mygeo[1] = lc.lt;
-            mygeo[2] = lc.lp;
-            mygeo[3] = cs * f1;  // e^{ikr}/(4 pi r)
-            mygeo[4] = sn * f1;
-            mygeo[5] = inv_r;
+            fill_row(lc.ls, lc.lt, lc.lp, mygeo);
+            mygeo[kRowLen] = cs * f1;  // e^{ikr}/(4 pi r)
+            mygeo[kRowLen + 1] = sn * f1;
+            mygeo[kRowLen + 2] = inv_r;
         }
         __syncwarp();
         unsigned pending = __ballot_sync(0xffffffffu, act);
@@ -85,13 +83,13 @@ cousin_tc_kernel(LevelDev L, PointsDev P, const double2* __restrict__ store, dou
                 const int src = valid ? slist[warp][t0 + r] : 0;
                 const double* gp = sgeo[warp] + src * kCG;
                 double d[LY::NQ][2];
-                tile_mma<NPC>(gp[0], gp[1], valid, tig, bq, d);
-                const double2 val = tile_gather<NPC>(gp[2], lane, d);
-                const double2 w = cmul(make_double2(gp[3], gp[4]), val);
+                tile_mma_row<NPC>(gp, valid, tig, bq, d);
+                const double2 val = tile_gather_row<NPC>(gp, lane, d);
+                const double2 w = cmul(make_double2(gp[kRowLen], gp[kRowLen + 1]), val);
                 double2 cS = make_double2(0.0, 0.0), cD = make_double2(0.0, 0.0);
                 switch (fpipe) {
                     case 1: cS = w; break;
-                    case 2: cD = cscale(w, gp[5]); break;
+                    case 2: cD = cscale(w, gp[kRowLen + 2]); break;
                     case 3: cD = make_double2(k * w.y, -k * w.x); break;  // -ik e^{ikr}/(4 pi r) val
                     case 4: cD = w; break;
                     default: break;

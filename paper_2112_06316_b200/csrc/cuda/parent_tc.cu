@@ -31,8 +31,9 @@ using namespace ifgfdev;
 using namespace tc;
 
 constexpr int kWarps = 4;
-constexpr int kGeo = 7;  // ls, lt, lp, ratio.re, ratio.im, extra factor, node (odd stride)
-constexpr int kGeoSz = kNP * kGeo + 1;  // keeps the accumulators 16-byte aligned
+constexpr int kRow = kRowLen + 4;     // A slots, T(phi), ratio.re, ratio.im, extra factor, node (odd)
+constexpr int kGeoSz = 32 * kRow;      // one chunk of 32 evaluation rows per warp (even: the
+                                       // accumulators behind it stay 16-byte aligned)
 
 // Child->parent pipe combinations of the strategies (ifgf.cpp:525-555). Each child pipe
 // feeds one parent pipe with one factor: R1 = ratio1, RI = ratio1/r_c (W2 -> W4),
@@ -118,95 +119,102 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
         // geometry template of (parent cell, child octant), host/coneplan.hpp parent_templates
         const int oct = (ccx > pcx ? 1 : 0) | (ccy > pcy ? 2 : 0) | (ccz > pcz ? 4 : 0);
         const std::size_t tbase = (std::size_t(tslot) * 8 + oct) * kNP;
-        for (int i = lane; i < count; i += 32) {
-            const int node = Lc.pev_perm[ev0 + start + i] & 0xff;  // entries are node | c << 8
-            double* gp = geo + i * kGeo;
-            if (tslot >= 0 && Lp.tmpl_gc[tbase + node] == cgam) {
-                const double2* te = reinterpret_cast<const double2*>(Lp.tmpl + (tbase + node) * 8);
-                const double2 e0 = __ldg(te), e1 = __ldg(te + 1), e2 = __ldg(te + 2), e3 = __ldg(te + 3);
-                gp[0] = e0.x;
-                gp[1] = e0.y;
-                gp[2] = e1.x;
-                gp[3] = e1.y;
-                gp[4] = e2.x;
-                gp[5] = CB::extra == RI ? e2.y : e3.x;
-                gp[6] = double(node);
-                continue;
-            }
-            const int is = node % kPS, it = (node / kPS) % kPA, ip = node / (kPS * kPA);
-            const double s = Lp.s_nodes[g1 * kPS + is];
-            const double rp = hp / s;
-            const double sth = Lp.th_sin[g2 * kPA + it], cth = Lp.th_cos[g2 * kPA + it];
-            const double sph = Lp.ph_sin[g3 * kPA + ip], cph = Lp.ph_cos[g3 * kPA + ip];
-            const double x = pcx + rp * sth * cph, y = pcy + rp * sth * sph, z = pcz + rp * cth;
-            const double vx = x - ccx, vy = y - ccy, vz = z - ccz;
-            const double rc2 = fma(vx, vx, fma(vy, vy, vz * vz));
-            const double inv_rc = rsqrt(rc2);
-            const double rc = rc2 * inv_rc;
-            const LocalCoords lc = local_coords_in(vx, vy, vz, inv_rc, hc, cf, Lc);
-            // stable r_c - r_p (ifgf.cpp:149-153)
-            const double sx = ccx + pcx - 2.0 * x, sy = ccy + pcy - 2.0 * y, sz = ccz + pcz - 2.0 * z;
-            const double dr = fma(sx, ccx - pcx, fma(sy, ccy - pcy, sz * (ccz - pcz))) / (rc + rp);
-            double sn, cs;
-            sincos_bounded(k * dr, &sn, &cs);
-            const double q1 = rp * inv_rc;
-            gp[0] = lc.ls;
-            gp[1] = lc.lt;
-            gp[2] = lc.lp;
-            gp[3] = cs * q1;
-            gp[4] = sn * q1;
-            gp[5] = CB::extra == RI ? inv_rc : q1;
-            gp[6] = double(node);
-        }
-        __syncwarp();
-        // 2. 8-evaluation tensor-core tiles against the child block
         // B fragments of the group's block, reused by all its tiles (tc_common.cuh)
         double bq[LY::NB];
         load_b<NPC>(cstore + std::size_t(cso) * NPC * kNP, lane, bq);
-        for (int t0 = 0; t0 < count; t0 += 8) {
-            const bool valid = t0 + r < count;
-            const double* gp = geo + (valid ? t0 + r : 0) * kGeo;
-            double d[LY::NQ][2];
-            tile_mma<NPC>(gp[0], gp[1], valid, tig, bq, d);
-            const double2 val = tile_gather<NPC>(gp[2], lane, d);
-            // lanes tig < NPC now hold (re, im) of child pipe tig for evaluation row r
-            const double2 r1 = make_double2(gp[3], gp[4]);
-            const double xf = gp[5];
-            int fac = R1;
-#pragma unroll
-            for (int pc = 0; pc < NPC; ++pc)
-                if (tig == pc) fac = CB::fac(pc);
-            double2 ctb;
-            if (fac == R1) {
-                ctb = cmul(r1, val);
-            } else if (fac == MK) {
-                const double2 w = cmul(r1, val);
-                ctb = make_double2(k * w.y, -k * w.x);
-            } else {  // RI or RQ: ratio1 times the stored extra factor
-                ctb = cmul(cscale(r1, xf), val);
+        for (int e0 = 0; e0 < count; e0 += 32) {  // chunks of 32 evaluations, one per lane
+            const int cn = min(32, count - e0);
+            if (lane < cn) {
+                const int node = Lc.pev_perm[ev0 + start + e0 + lane] & 0xff;  // entries are node | c << 8
+                double ls, lt, lp, r1x, r1y, xf;
+                if (tslot >= 0 && Lp.tmpl_gc[tbase + node] == cgam) {
+                    const double2* te = reinterpret_cast<const double2*>(Lp.tmpl + (tbase + node) * 8);
+                    const double2 t0 = __ldg(te), t1 = __ldg(te + 1), t2 = __ldg(te + 2), t3 = __ldg(te + 3);
+                    ls = t0.x;
+                    lt = t0.y;
+                    lp = t1.x;
+                    r1x = t1.y;
+                    r1y = t2.x;
+                    xf = CB::extra == RI ? t2.y : t3.x;
+                } else {
+                    const int is = node % kPS, it = (node / kPS) % kPA, ip = node / (kPS * kPA);
+                    const double s = Lp.s_nodes[g1 * kPS + is];
+                    const double rp = hp / s;
+                    const double sth = Lp.th_sin[g2 * kPA + it], cth = Lp.th_cos[g2 * kPA + it];
+                    const double sph = Lp.ph_sin[g3 * kPA + ip], cph = Lp.ph_cos[g3 * kPA + ip];
+                    const double x = pcx + rp * sth * cph, y = pcy + rp * sth * sph, z = pcz + rp * cth;
+                    const double vx = x - ccx, vy = y - ccy, vz = z - ccz;
+                    const double rc2 = fma(vx, vx, fma(vy, vy, vz * vz));
+                    const double inv_rc = rsqrt(rc2);
+                    const double rc = rc2 * inv_rc;
+                    const LocalCoords lc = local_coords_in(vx, vy, vz, inv_rc, hc, cf, Lc);
+                    // stable r_c - r_p (ifgf.cpp:149-153)
+                    const double sx = ccx + pcx - 2.0 * x, sy = ccy + pcy - 2.0 * y, sz = ccz + pcz - 2.0 * z;
+                    const double dr = fma(sx, ccx - pcx, fma(sy, ccy - pcy, sz * (ccz - pcz))) / (rc + rp);
+                    double sn, cs;
+                    sincos_bounded(k * dr, &sn, &cs);
+                    const double q1 = rp * inv_rc;
+                    ls = lc.ls;
+                    lt = lc.lt;
+                    lp = lc.lp;
+                    r1x = cs * q1;
+                    r1y = sn * q1;
+                    xf = CB::extra == RI ? inv_rc : q1;
+                }
+                double* row = geo + lane * kRow;
+                fill_row(ls, lt, lp, row);
+                row[kRowLen] = r1x;
+                row[kRowLen + 1] = r1y;
+                row[kRowLen + 2] = xf;
+                row[kRowLen + 3] = double(node);
             }
-            if constexpr (COMBO == 0) {  // child W2, W3 -> parent W4: sum across the quad
-                const double ox = __shfl_down_sync(0xffffffffu, ctb.x, 1);
-                const double oy = __shfl_down_sync(0xffffffffu, ctb.y, 1);
-                if (tig == 1) ctb = make_double2(ctb.x + ox, ctb.y + oy);
-            } else if constexpr (COMBO == 3) {
-                const double ox = __shfl_down_sync(0xffffffffu, ctb.x, 1);
-                const double oy = __shfl_down_sync(0xffffffffu, ctb.y, 1);
-                if (tig == 0) ctb = make_double2(ctb.x + ox, ctb.y + oy);
-            }
-            bool writer = valid && tig < NPC;
-            if constexpr (COMBO == 0) writer = writer && tig != 2;
-            if constexpr (COMBO == 3) writer = writer && tig == 0;
-            if (writer) {
-                int dst = 0;
+            __syncwarp();
+            // 2. 8-evaluation tensor-core tiles against the child block
+            for (int t0 = 0; t0 < cn; t0 += 8) {
+                const bool valid = t0 + r < cn;
+                const double* gp = geo + (valid ? t0 + r : 0) * kRow;
+                double d[LY::NQ][2];
+                tile_mma_row<NPC>(gp, valid, tig, bq, d);
+                const double2 val = tile_gather_row<NPC>(gp, lane, d);
+                // lanes tig < NPC now hold (re, im) of child pipe tig for evaluation row r
+                const double2 r1 = make_double2(gp[kRowLen], gp[kRowLen + 1]);
+                const double xf = gp[kRowLen + 2];
+                int fac = R1;
 #pragma unroll
                 for (int pc = 0; pc < NPC; ++pc)
-                    if (tig == pc) dst = CB::dst(pc);
-                double2& a = acc[int(gp[6]) * NPP + dst];
-                a = cadd(a, ctb);
+                    if (tig == pc) fac = CB::fac(pc);
+                double2 ctb;
+                if (fac == R1) {
+                    ctb = cmul(r1, val);
+                } else if (fac == MK) {
+                    const double2 w = cmul(r1, val);
+                    ctb = make_double2(k * w.y, -k * w.x);
+                } else {  // RI or RQ: ratio1 times the stored extra factor
+                    ctb = cmul(cscale(r1, xf), val);
+                }
+                if constexpr (COMBO == 0) {  // child W2, W3 -> parent W4: sum across the quad
+                    const double ox = __shfl_down_sync(0xffffffffu, ctb.x, 1);
+                    const double oy = __shfl_down_sync(0xffffffffu, ctb.y, 1);
+                    if (tig == 1) ctb = make_double2(ctb.x + ox, ctb.y + oy);
+                } else if constexpr (COMBO == 3) {
+                    const double ox = __shfl_down_sync(0xffffffffu, ctb.x, 1);
+                    const double oy = __shfl_down_sync(0xffffffffu, ctb.y, 1);
+                    if (tig == 0) ctb = make_double2(ctb.x + ox, ctb.y + oy);
+                }
+                bool writer = valid && tig < NPC;
+                if constexpr (COMBO == 0) writer = writer && tig != 2;
+                if constexpr (COMBO == 3) writer = writer && tig == 0;
+                if (writer) {
+                    int dst = 0;
+#pragma unroll
+                    for (int pc = 0; pc < NPC; ++pc)
+                        if (tig == pc) dst = CB::dst(pc);
+                    double2& a = acc[int(gp[kRowLen + 3]) * NPP + dst];
+                    a = cadd(a, ctb);
+                }
             }
+            __syncwarp();
         }
-        __syncwarp();
     }
     // values -> coefficients (transform3, ifgf.cpp:560-562), warp-local
     double2* v0 = acc;

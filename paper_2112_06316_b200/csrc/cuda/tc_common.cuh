@@ -147,5 +147,83 @@ __device__ __forceinline__ double2 tile_gather(double lp, int lane, const double
     return val;
 }
 
+// ---- precomputed evaluation rows: the geometry step of an evaluation writes, once, its
+// A operands in k-slot order and its T(phi) row, so the tiles only load them.
+constexpr int kRowA = 16;           // A slots: (j, tig) at 4 j + tig
+constexpr int kRowTq = kRowA;       // T_0..T_4(phi)
+constexpr int kRowLen = kRowA + kPA;
+
+__device__ __forceinline__ void fill_row(double ls, double lt, double lp, double* row) {
+    double ts[kPS], tt[kPA], tq[kPA];
+    dev::cheb_row<kPS>(ls, ts);
+    dev::cheb_row<kPA>(lt, tt);
+    dev::cheb_row<kPA>(lp, tq);
+#pragma unroll
+    for (int j = 0; j < kKS; ++j) {
+#pragma unroll
+        for (int tg = 0; tg < kPS; ++tg) row[4 * j + tg] = ts[tg] * tt[j];  // (is, it) = (tg, j)
+        row[4 * j + 3] = j < kPS ? ts[j] * tt[kPA - 1] : 0.0;              // (j, 4), (3, 3) padding
+    }
+#pragma unroll
+    for (int p = 0; p < kPA; ++p) row[kRowTq + p] = tq[p];
+}
+
+// tile from precomputed rows (row = this lane's row r, valid = false: zero row)
+template <int NPC>
+__device__ __forceinline__ void tile_mma_row(const double* row, bool valid, int tig, const double* bq,
+                                             double (&d)[Layout<NPC>::NQ][2]) {
+    using LY = Layout<NPC>;
+#pragma unroll
+    for (int q = 0; q < LY::NQ; ++q) d[q][0] = d[q][1] = 0.0;
+#pragma unroll
+    for (int j = 0; j < kKS; ++j) {
+        const double a = valid ? row[4 * j + tig] : 0.0;
+#pragma unroll
+        for (int q = 0; q < LY::NQ; ++q) dmma884(d[q][0], d[q][1], a, bq[q * kKS + j]);
+    }
+}
+
+template <int NPC>
+__device__ __forceinline__ double2 tile_gather_row(const double* row, int lane, const double (&d)[Layout<NPC>::NQ][2]) {
+    using LY = Layout<NPC>;
+    const int tig = lane & 3;
+    const double* tq = row + kRowTq;
+    double2 val = make_double2(0.0, 0.0);
+    if constexpr (NPC == 3) {
+#pragma unroll
+        for (int q = 0; q < LY::NQ; ++q) {
+            const double w = tq[q];
+            val.x = fma(w, d[q][0], val.x);
+            val.y = fma(w, d[q][1], val.y);
+        }
+        const double w4 = tq[kPA - 1];
+        const int src = (lane & ~3) | 3;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const double ex = __shfl_sync(0xffffffffu, d[q][0], src);
+            const double ey = __shfl_sync(0xffffffffu, d[q][1], src);
+            if (tig == q) {
+                val.x = fma(w4, ex, val.x);
+                val.y = fma(w4, ey, val.y);
+            }
+        }
+    } else {
+        const int sub = tig / NPC;
+#pragma unroll
+        for (int q = 0; q < LY::NQ; ++q) {
+            const int ip = LY::IPG * q + sub;
+            const double w = ip < kPA ? tq[ip < kPA ? ip : 0] : 0.0;
+            val.x = fma(w, d[q][0], val.x);
+            val.y = fma(w, d[q][1], val.y);
+        }
+#pragma unroll
+        for (int off = NPC; off < NPC * LY::IPG; off <<= 1) {
+            val.x += __shfl_down_sync(0xffffffffu, val.x, off);
+            val.y += __shfl_down_sync(0xffffffffu, val.y, off);
+        }
+    }
+    return val;
+}
+
 }  // namespace tc
 }  // namespace ifgfb200
