@@ -48,8 +48,11 @@ beta_kernel(BetaDev B, int TT, int max_dv, int max_nu, int max_nunv, int p_base,
     double* wv = wu + nb;
     double* Tu = wv + nb;                 // nb x TT, T_i(clamp(u_iu))
     double* Tv = Tu + nb * TT;            // nb x TT
-    double* Pu = Tv + nb * TT;            // 9 x nb x max_dv: u-contracted series
-    double2* fS = reinterpret_cast<double2*>(Pu + 9 * nb * max_dv);  // kJV x nb
+    // 9 x nb x (max_dv | 1): u-contracted series; odd row stride, the geometry step reads it
+    // across lanes by u node
+    const int pst = max_dv | 1;
+    double* Pu = Tv + nb * TT;
+    double2* fS = reinterpret_cast<double2*>(Pu + ((9 * nb * pst + 1) & ~1));  // kJV x nb, 16-byte aligned
     double2* fD = fS + nb * kJV;
     double2* rS = fD + nb * kJV;          // kJV x max_nu
     double2* rD = rS + kJV * max_nu;
@@ -95,7 +98,7 @@ beta_kernel(BetaDev B, int TT, int max_dv, int max_nu, int max_nunv, int p_base,
         const double* t = Tu + iu * TT;
         double acc = 0.0;
         for (int i = 0; i < du; ++i) acc += col[i] * t[i];
-        Pu[(s * nb + iu) * max_dv + j] = acc;
+        Pu[(s * nb + iu) * pst + j] = acc;
     }
     __syncthreads();
 
@@ -108,7 +111,7 @@ beta_kernel(BetaDev B, int TT, int max_dv, int max_nu, int max_nunv, int p_base,
             double g[9];
 #pragma unroll
             for (int s = 0; s < 9; ++s) {
-                const double* pp = Pu + (s * nb + iu) * max_dv;
+                const double* pp = Pu + (s * nb + iu) * pst;
                 double acc = 0.0;
                 for (int j = 0; j < dv; ++j) acc += pp[j] * t[j];
                 g[s] = acc;
@@ -182,7 +185,7 @@ beta_kernel(BetaDev B, int TT, int max_dv, int max_nu, int max_nunv, int p_base,
 }  // namespace
 
 std::size_t beta_smem_bytes(int nb, int TT, int max_dv, int max_nu, int max_nunv) {
-    return sizeof(double) * (4 * std::size_t(nb) + 2 * std::size_t(nb) * TT + 9 * std::size_t(nb) * max_dv) +
+    return sizeof(double) * (4 * std::size_t(nb) + 2 * std::size_t(nb) * TT + ((9 * std::size_t(nb) * (max_dv | 1) + 1) & ~std::size_t(1))) +
            sizeof(double2) * (2 * std::size_t(nb) * kJV + 2 * std::size_t(kJV) * max_nu + 2 * std::size_t(max_nunv));
 }
 

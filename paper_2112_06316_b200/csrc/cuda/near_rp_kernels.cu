@@ -70,7 +70,7 @@ __device__ __forceinline__ void pair_kernels(double x, double y, double z, doubl
     accD.y = fma(sg, da.y, accD.y);
 }
 
-__global__ void __launch_bounds__(kNearThreads)
+__global__ void __launch_bounds__(kNearThreads, 8)
 near_kernel(NearDev N, PointsDev P, const double2* __restrict__ a_p, double k,
             double2* __restrict__ Sp, double2* __restrict__ Dp) {
     const int c = blockIdx.x;
