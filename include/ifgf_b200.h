@@ -123,6 +123,9 @@ int ifgf_plan_diagnostics(const ifgf_plan* p, char* buf, size_t cap);
  * [3] near pairs (evaluated + corrections)  [4] RP pairs
  * [5..9]  flops of leaf, cousin, parent, near, RP (SURVEY.md §8(d) counting)
  * [10..14] algorithmic HBM bytes of leaf, cousin, parent, near, RP  [15] total flops */
+/* FNV-1a hash of a level's per-evaluation segment ordinals (cousin and parent) and the
+ * grouped parent permutation: compares plans built with and without the GPU decider */
+uint64_t ifgf_plan_decision_hash(const ifgf_plan* p, int level);
 int ifgf_plan_work(const ifgf_plan* p, double* work16);
 int ifgf_operator_work(const ifgf_operator* op, double* work16);
 

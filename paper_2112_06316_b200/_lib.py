@@ -76,6 +76,7 @@ _SIGS = {
     "ifgf_plan_beta_fingerprint": (C.c_uint64, [vp]),
     "ifgf_plan_diagnostics": (C.c_int, [vp, C.c_char_p, C.c_size_t]),
     "ifgf_plan_work": (C.c_int, [vp, d_p]),
+    "ifgf_plan_decision_hash": (C.c_uint64, [vp, C.c_int]),
     "ifgf_operator_work": (C.c_int, [vp, d_p]),
     "ifgf_operator_create": (C.c_int, [vp, C.POINTER(IfgfConfig), C.POINTER(vp)]),
     "ifgf_operator_from_plan": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(vp)]),

@@ -121,18 +121,23 @@ std::shared_ptr<ifgf_plan> make_plan(std::shared_ptr<const Surface> s, const ifg
     cp.n_s0 = c.n_s0;
     cp.ps = c.ps;
     cp.pang = c.pang;
-    p->cones = build_cone_plan(p->tree, p->rel, pts, cp, c.workers);
+    // segment decisions and closest-point searches batched on the GPU when one is there
+    // (decisions equal to the host's bit for bit; the host redoes the flagged ones)
+    int ndev = 0;
+    const bool gpu = c.device >= 0 && cudaGetDeviceCount(&ndev) == cudaSuccess && c.device < ndev;
+    if (!gpu) cudaGetLastError();  // clear a no-device error
+    const int dev = c.device;
+    const ConeDecider decider = [dev](const ConeDecisionJob& job, ConeLevel& L, std::vector<std::uint8_t>& marks,
+                                      std::vector<std::int64_t>& fc, std::vector<std::int64_t>& fp) {
+        gpu_cone_decisions(job, L, marks, fc, fp, dev);
+    };
+    p->cones = build_cone_plan(p->tree, p->rel, pts, cp, c.workers, gpu ? &decider : nullptr);
     p->t_cones = lap();
     RpParams rp;
     rp.delta_rel = c.delta_rel;
     rp.delta_abs = c.delta_abs;
     rp.n_beta = c.n_beta;
     rp.cov_d = c.cov_d;
-    // closest-point searches on the GPU when one is there (bitwise equal to the host's)
-    int ndev = 0;
-    const bool gpu = c.device >= 0 && cudaGetDeviceCount(&ndev) == cudaSuccess && c.device < ndev;
-    if (!gpu) cudaGetLastError();  // clear a no-device error
-    const int dev = c.device;
     const ClosestPointBatch batch = [dev](const Surface& sf, const std::vector<ClosestPointRequest>& rq,
                                           std::vector<ClosestPoint>& out) { gpu_closest_points(sf, rq, out, dev); };
     p->pairs = classify_pairs(*s, p->tree, p->rel, rp, c.workers, gpu ? &batch : nullptr);
@@ -442,6 +447,24 @@ int64_t ifgf_plan_level(const ifgf_plan* p, int level, int32_t* params4, double*
     if (seg_box) std::memcpy(seg_box, L.seg_box.data(), L.seg_box.size() * sizeof(int32_t));
     if (seg_gamma) std::memcpy(seg_gamma, L.seg_gamma.data(), L.seg_gamma.size() * sizeof(int32_t));
     return int64_t(L.nseg());
+}
+
+uint64_t ifgf_plan_decision_hash(const ifgf_plan* p, int level) {
+    if (!p || level < 3 || level > p->tree.depth) return 0;
+    const ConeLevel& L = p->cones.level[level - 1];
+    std::uint64_t h = 1469598103934665603ULL;
+    auto mix = [&](const void* data, std::size_t n) {
+        const auto* b = static_cast<const unsigned char*>(data);
+        for (std::size_t i = 0; i < n; ++i) {
+            h ^= b[i];
+            h *= 1099511628211ULL;
+        }
+    };
+    mix(L.cev_seg.data(), L.cev_seg.size() * sizeof(std::int32_t));
+    mix(L.pev_seg.data(), L.pev_seg.size() * sizeof(std::int32_t));
+    mix(L.pev_perm.data(), L.pev_perm.size() * sizeof(std::uint16_t));
+    mix(L.pgrp_seg.data(), L.pgrp_seg.size() * sizeof(std::int32_t));
+    return h;
 }
 
 int64_t ifgf_plan_evaluations(const ifgf_plan* p, int level, int which) {

@@ -5,6 +5,7 @@
 
 #include <vector>
 
+#include "host/coneplan.hpp"
 #include "host/fields.hpp"
 #include "host/proximity.hpp"
 
@@ -17,6 +18,9 @@ void gpu_far_field(const FineQuad& q, const std::vector<Vec3>& dirs, double k, d
 void gpu_near_field(const FineQuad& q, const std::vector<Vec3>& pts, double k, double gamma, int device,
                     cplx* scattered, double* dmin, double* gauss);
 // closest_point_on for every non-own request, bit for bit (ClosestPointBatch)
+// segment decisions of one plan level (ConeDecider); uncertain ones are flagged for the host
+void gpu_cone_decisions(const ConeDecisionJob& job, ConeLevel& L, std::vector<std::uint8_t>& marks,
+                        std::vector<std::int64_t>& flagged_cev, std::vector<std::int64_t>& flagged_pev, int device);
 void gpu_closest_points(const Surface& s, const std::vector<ClosestPointRequest>& req, std::vector<ClosestPoint>& res,
                         int device);
 

@@ -1,5 +1,9 @@
 #include "coneplan.hpp"
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <algorithm>
 #include <atomic>
 #include <exception>
@@ -187,7 +191,8 @@ std::vector<int> dl_pipes(const BoxTree& t, int level, DlStrategy s) {
 }
 
 ConePlanHost build_cone_plan(const BoxTree& t, const BoxRelations& rel,
-                             const std::vector<Vec3>& pts, const ConeParams& p, int workers) {
+                             const std::vector<Vec3>& pts, const ConeParams& p, int workers,
+                             const ConeDecider* decider) {
     if (p.ps < 1 || p.ps > kMaxOrder || p.pang < 1 || p.pang > kMaxOrder)
         throw InvalidArgument("plan_cones: interpolation orders must lie in [1,12]");
     if (p.n_s0 < 1 || p.n_c0 < 1) throw InvalidArgument("plan_cones: interval counts must be positive");
@@ -212,7 +217,11 @@ ConePlanHost build_cone_plan(const BoxTree& t, const BoxRelations& rel,
         }
     }
 
+    const bool timing = std::getenv("IFGF_PLAN_TIMING") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto secs = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
     for (int d = 3; d <= D; ++d) {
+        const auto T0 = now();
         ConeLevel& L = plan.level[d - 1];
         L = make_level(d, t.side(d), lambda, p);
         const BoxLevel& B = t.level[d - 1];
@@ -229,57 +238,117 @@ ConePlanHost build_cone_plan(const BoxTree& t, const BoxRelations& rel,
         for (std::size_t b = 0; b < nb; ++b)
             L.cev_begin[b + 1] = L.cev_begin[b] + std::int64_t(cz.count(b)) * (B.end[b] - B.begin[b]);
         L.cev_seg.assign(std::size_t(L.cev_begin[nb]), 0);
-        parallel_for(std::int64_t(nb), w, [&](std::int64_t tb) {
-            const std::uint32_t n_t = B.end[tb] - B.begin[tb];
-            std::int64_t at = L.cev_begin[tb];
-            for (std::int32_t j = cz.ptr[tb]; j < cz.ptr[tb + 1]; ++j) {
-                const std::int32_t sb = cz.idx[j];
-                for (std::uint32_t q = 0; q < n_t; ++q) {
-                    const int g = segment_gamma(L, to_cone(pts[B.begin[tb] + q], ctr[sb], h));
-                    L.cev_seg[at++] = g;
-                    mark(marks, std::size_t(sb) * spb + g);
-                }
-            }
-        });
-
+        auto cev_decide = [&](std::int64_t tb, std::int64_t off) {  // evaluation off of box tb
+            const std::int64_t n_t = B.end[tb] - B.begin[tb];
+            const std::int32_t sb = cz.idx[cz.ptr[tb] + off / n_t];
+            const int g = segment_gamma(L, to_cone(pts[B.begin[tb] + off % n_t], ctr[sb], h));
+            L.cev_seg[L.cev_begin[tb] + off] = g;
+            mark(marks, std::size_t(sb) * spb + g);
+        };
         // (2) interpolation nodes of every relevant parent segment, in each child's frame
-        if (d > 3) {
-            const ConeLevel& PL = plan.level[d - 2];
-            const double ph = t.half_diag(d - 1);
-            const auto& cptr = plan.child_ptr[d - 2];
-            const auto& cidx = plan.child_idx[d - 2];
-            const int P = PL.nodes_per_seg();
-            const std::size_t pseg = PL.nseg();
+        const ConeLevel* PLp = d > 3 ? &plan.level[d - 2] : nullptr;
+        const double ph = d > 3 ? t.half_diag(d - 1) : 0.0;
+        const std::vector<std::int32_t>* cptr = d > 3 ? &plan.child_ptr[d - 2] : nullptr;
+        const std::vector<std::int32_t>* cidx = d > 3 ? &plan.child_idx[d - 2] : nullptr;
+        if (PLp) {
+            const int P = PLp->nodes_per_seg();
+            const std::size_t pseg = PLp->nseg();
             L.pev_begin.assign(pseg + 1, 0);
             for (std::size_t so = 0; so < pseg; ++so) {
-                const std::int32_t pb = PL.seg_box[so];
-                L.pev_begin[so + 1] = L.pev_begin[so] + std::int64_t(P) * (cptr[pb + 1] - cptr[pb]);
+                const std::int32_t pb = PLp->seg_box[so];
+                L.pev_begin[so + 1] = L.pev_begin[so] + std::int64_t(P) * ((*cptr)[pb + 1] - (*cptr)[pb]);
             }
             L.pev_seg.assign(std::size_t(L.pev_begin[pseg]), 0);
-            parallel_for(std::int64_t(pseg), w, [&](std::int64_t so) {
-                const std::int32_t pb = PL.seg_box[so];
-                const int gam = PL.seg_gamma[so];
-                const int g1 = gam % PL.ns, g2 = (gam / PL.ns) % PL.nc, g3 = gam / PL.ns / PL.nc;
-                const Vec3 pc = t.center(d - 1, std::size_t(pb));
-                const int nch = cptr[pb + 1] - cptr[pb];
-                for (int ip = 0; ip < PL.pang; ++ip)
-                    for (int it = 0; it < PL.pang; ++it)
-                        for (int is = 0; is < PL.ps; ++is) {
-                            const Vec3 x = from_cone(PL.s_nodes[std::size_t(g1) * PL.ps + is],
-                                                     PL.th_nodes[std::size_t(g2) * PL.pang + it],
-                                                     PL.ph_nodes[std::size_t(g3) * PL.pang + ip], pc, ph);
-                            const int node = is + PL.ps * (it + PL.pang * ip);
-                            std::int64_t at = L.pev_begin[so] + std::int64_t(node) * nch;
-                            for (int c = 0; c < nch; ++c) {
-                                const std::int32_t ch = cidx[cptr[pb] + c];
-                                const int g = segment_gamma(L, to_cone(x, ctr[ch], h));
-                                L.pev_seg[at++] = g;
-                                mark(marks, std::size_t(ch) * spb + g);
-                            }
-                        }
+        }
+        auto pev_decide = [&](std::int64_t so, std::int64_t off) {  // evaluation off of parent segment so
+            const ConeLevel& PL = *PLp;
+            const std::int32_t pb = PL.seg_box[so];
+            const int gam = PL.seg_gamma[so];
+            const int g1 = gam % PL.ns, g2 = (gam / PL.ns) % PL.nc, g3 = gam / PL.ns / PL.nc;
+            const int nch = (*cptr)[pb + 1] - (*cptr)[pb];
+            const int node = int(off / nch), c = int(off % nch);
+            const int is = node % PL.ps, it = (node / PL.ps) % PL.pang, ip = node / (PL.ps * PL.pang);
+            const Vec3 x = from_cone(PL.s_nodes[std::size_t(g1) * PL.ps + is], PL.th_nodes[std::size_t(g2) * PL.pang + it],
+                                     PL.ph_nodes[std::size_t(g3) * PL.pang + ip], t.center(d - 1, std::size_t(pb)), ph);
+            const std::int32_t ch = (*cidx)[(*cptr)[pb] + c];
+            const int g = segment_gamma(L, to_cone(x, ctr[ch], h));
+            L.pev_seg[L.pev_begin[so] + off] = g;
+            mark(marks, std::size_t(ch) * spb + g);
+        };
+        if (decider) {
+            // batched decisions; the host redoes the ones the decider could not guarantee
+            ConeDecisionJob job;
+            job.L = &L;
+            job.h = h;
+            job.pts = &pts;
+            job.ctr = &ctr;
+            job.B = &B;
+            job.cz = &cz;
+            std::vector<Vec3> pctr;
+            if (PLp) {
+                job.PL = PLp;
+                job.ph = ph;
+                const BoxLevel& PB = t.level[d - 2];
+                pctr.resize(PB.size());
+                for (std::size_t b = 0; b < PB.size(); ++b) pctr[b] = t.center(d - 1, b);
+                job.pctr = &pctr;
+                job.cptr = cptr;
+                job.cidx = cidx;
+                for (double a : PLp->th_nodes) {
+                    job.th_sin.push_back(std::sin(a));
+                    job.th_cos.push_back(std::cos(a));
+                }
+                for (double a : PLp->ph_nodes) {
+                    job.ph_sin.push_back(std::sin(a));
+                    job.ph_cos.push_back(std::cos(a));
+                }
+            }
+            std::vector<std::int64_t> fl_cev, fl_pev;
+            (*decider)(job, L, marks, fl_cev, fl_pev);
+            parallel_for(std::int64_t(fl_cev.size()), w, [&](std::int64_t i) {
+                const std::int64_t at = fl_cev[i];
+                const std::int64_t tb =
+                    std::upper_bound(L.cev_begin.begin(), L.cev_begin.end(), at) - L.cev_begin.begin() - 1;
+                cev_decide(tb, at - L.cev_begin[tb]);
             });
+            parallel_for(std::int64_t(fl_pev.size()), w, [&](std::int64_t i) {
+                const std::int64_t at = fl_pev[i];
+                const std::int64_t so =
+                    std::upper_bound(L.pev_begin.begin(), L.pev_begin.end(), at) - L.pev_begin.begin() - 1;
+                pev_decide(so, at - L.pev_begin[so]);
+            });
+        } else {
+            parallel_for(std::int64_t(nb), w, [&](std::int64_t tb) {
+                const std::int64_t n = L.cev_begin[tb + 1] - L.cev_begin[tb];
+                for (std::int64_t off = 0; off < n; ++off) cev_decide(tb, off);
+            });
+            if (PLp)
+                parallel_for(std::int64_t(PLp->nseg()), w, [&](std::int64_t so) {  // x once per node
+                    const ConeLevel& PL = *PLp;
+                    const std::int32_t pb = PL.seg_box[so];
+                    const int gam = PL.seg_gamma[so];
+                    const int g1 = gam % PL.ns, g2 = (gam / PL.ns) % PL.nc, g3 = gam / PL.ns / PL.nc;
+                    const Vec3 pc = t.center(d - 1, std::size_t(pb));
+                    const int nch = (*cptr)[pb + 1] - (*cptr)[pb];
+                    for (int ip = 0; ip < PL.pang; ++ip)
+                        for (int it = 0; it < PL.pang; ++it)
+                            for (int is = 0; is < PL.ps; ++is) {
+                                const Vec3 x = from_cone(PL.s_nodes[std::size_t(g1) * PL.ps + is],
+                                                         PL.th_nodes[std::size_t(g2) * PL.pang + it],
+                                                         PL.ph_nodes[std::size_t(g3) * PL.pang + ip], pc, ph);
+                                const int node = is + PL.ps * (it + PL.pang * ip);
+                                std::int64_t at = L.pev_begin[so] + std::int64_t(node) * nch;
+                                for (int c = 0; c < nch; ++c) {
+                                    const std::int32_t ch = (*cidx)[(*cptr)[pb] + c];
+                                    const int g = segment_gamma(L, to_cone(x, ctr[ch], h));
+                                    L.pev_seg[at++] = g;
+                                    mark(marks, std::size_t(ch) * spb + g);
+                                }
+                            }
+                });
         }
 
+        const auto T1 = now();
         // relevant segments in (box, gamma) order
         L.box_seg_begin.assign(nb + 1, 0);
         for (std::size_t b = 0; b < nb; ++b) {
@@ -326,6 +395,9 @@ ConePlanHost build_cone_plan(const BoxTree& t, const BoxRelations& rel,
             });
             group_parent_evaluations(L, PL.nseg(), w, P);
         }
+        if (timing)
+            std::fprintf(stderr, "cone plan level %d: decisions %.3fs, segments/ordinals/groups %.3fs (cev %zu pev %zu)\n",
+                         d, secs(T0, T1), secs(T1, now()), L.cev_seg.size(), L.pev_seg.size());
     }
     return plan;
 }

@@ -11,6 +11,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <vector>
 
 #include "boxtree.hpp"
@@ -67,9 +68,32 @@ struct ConePlanHost {
 int cone_doublings(double side, double lambda);  // ifgf.cpp:18-25
 std::vector<int> dl_pipes(const BoxTree& t, int level, DlStrategy s);  // ifgf.cpp:193-207
 
+// Segment decisions of one level, for a batched (GPU) decider: every cousin evaluation
+// (cev, target-box major as ConeLevel::cev_seg) and every parent-node evaluation (pev) gets
+// the gamma of the segment it falls into, and marks[box * segs_per_box + gamma] is set.
+// A decider may leave decisions it cannot guarantee to equal glibc's acos/atan2 to the host:
+// it lists them in flagged_cev / flagged_pev (their gamma and marks are then ignored).
+struct ConeDecisionJob {
+    const ConeLevel* L = nullptr;        // this level (ns, nc, ds, dth, dph)
+    double h = 0;                        // half diagonal of this level's boxes
+    const std::vector<Vec3>* pts = nullptr;   // Morton-ordered points
+    const std::vector<Vec3>* ctr = nullptr;   // box centres of this level
+    const BoxLevel* B = nullptr;
+    const Adjacency* cz = nullptr;             // cousin lists
+    // parent part (level d - 1), absent at d = 3
+    const ConeLevel* PL = nullptr;
+    double ph = 0;                              // parent half diagonal
+    const std::vector<Vec3>* pctr = nullptr;    // parent centres (level d - 1)
+    const std::vector<std::int32_t>* cptr = nullptr;  // children of parent boxes (compacted)
+    const std::vector<std::int32_t>* cidx = nullptr;
+    std::vector<double> th_sin, th_cos, ph_sin, ph_cos;  // glibc sin/cos of the parent node tables
+};
+using ConeDecider = std::function<void(const ConeDecisionJob& job, ConeLevel& L, std::vector<std::uint8_t>& marks,
+                                       std::vector<std::int64_t>& flagged_cev, std::vector<std::int64_t>& flagged_pev)>;
+
 ConePlanHost build_cone_plan(const BoxTree& t, const BoxRelations& rel,
                              const std::vector<Vec3>& pts_morton, const ConeParams& p,
-                             int workers);
+                             int workers, const ConeDecider* decider = nullptr);
 
 // Parent-fill geometry templates (device data, not decisions). The position of a parent
 // interpolation node relative to a child box depends only on the parent cone cell, the

@@ -250,6 +250,10 @@ class HostPlan:
     def evaluations(self, d, which):
         return int(lib().ifgf_plan_evaluations(self._h, d, which))
 
+    def decision_hash(self, d):
+        """FNV-1a of level d's per-evaluation segment ordinals and parent groups."""
+        return int(lib().ifgf_plan_decision_hash(self._h, d))
+
     def proximity(self):
         L = lib()
         npairs = L.ifgf_plan_npairs(self._h)

@@ -69,3 +69,27 @@ def test_gpu_closest_points_bitwise(ref, mesh):
     for key in theirs:
         assert np.array_equal(gpu[key], theirs[key]), key
         assert np.array_equal(cpu[key], theirs[key]), key
+
+
+@pytest.mark.parametrize("mesh", ["sphere", "spheroid", "cfg1"])
+def test_gpu_cone_decisions_bitwise(ref, mesh):
+    # segment decisions batched on the GPU (uncertain ones redone on the host with glibc)
+    # give the reference's relevant segments, cousin / parent ordinals and groups bit for bit
+    if mesh == "sphere":
+        pm, rm, k = P.SurfaceMesh.sphere(1.0, 2, 10, 10), ref.RefMesh.sphere(1.0, 2, 10, 10), 8 * np.pi
+    elif mesh == "spheroid":
+        pm, rm, k = P.SurfaceMesh.spheroid(2, 8, 8, 4.0, 1.0, 1.0), ref.RefMesh.spheroid(2, 8, 8, 4.0, 1.0, 1.0), 2 * np.pi
+    else:
+        pm, rm, k = P.SurfaceMesh.sphere(1.0, 2, 16, 16), ref.RefMesh.sphere(1.0, 2, 16, 16), 4 * np.pi
+    gpu = P.HostPlan(pm, P.SolveConfig(k=k, device=0))
+    cpu = P.HostPlan(pm, P.SolveConfig(k=k, device=-1))
+    ro = ref.RefOperator(rm, k, n_beta=8)
+    assert gpu.depth == cpu.depth == ro.depth
+    for d in range(3, gpu.depth + 1):
+        A, B, C = gpu.level_cones(d), cpu.level_cones(d), ro.level_cones(d)
+        for key in ("seg_box", "seg_gamma"):
+            assert np.array_equal(A[key], C[key]) and np.array_equal(B[key], C[key]), (d, key)
+        for which in (0, 1):
+            assert gpu.evaluations(d, which) == cpu.evaluations(d, which)
+        assert gpu.decision_hash(d) == cpu.decision_hash(d), d
+    assert gpu.diagnostics() == cpu.diagnostics()
