@@ -1141,9 +1141,11 @@ PhaseTimes Engine::time_phases() {
 
 int Engine::kernels_per_apply() const {
     const Impl& e = *d_;
-    // weights + leaf + cousin per level + parent per level>3 + near + coeffs + rp_combine
-    if (e.depth < 3) return 4;
-    return 1 + 1 + (e.depth - 2) + (e.depth - 3) + 1 + 2;
+    if (e.kernels > 0) return e.kernels;  // counted by the last run_apply
+    // weights + leaf + cousin per level + parent per level > 3 + near + coeffs + rp + combine
+    // (+ the output un-permute under a communicator)
+    const int ifgf = e.depth < 3 ? 0 : 1 + (e.depth - 2) + (e.depth - 3);
+    return 1 + ifgf + 3 + 1 + (e.world > 1 ? 1 : 0);
 }
 
 std::string Engine::describe() const {
