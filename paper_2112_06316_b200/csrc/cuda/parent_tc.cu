@@ -79,7 +79,7 @@ struct Combo<5> {  // (W2,W3) <- (W2,W3)
 };
 
 template <int COMBO>
-__global__ void __launch_bounds__(32 * kWarps, 4)
+__global__ void __launch_bounds__(32 * kWarps, 5)
 parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, double k,
                  const double* __restrict__ Ms, const double* __restrict__ Ma,
                  double2* __restrict__ pstore) {
