@@ -8,8 +8,8 @@
 //   2. forms groups of lanes that evaluate the same segment (ballot on the ordinal), lists
 //      each group's lanes, loads the segment's B fragments once and runs 8-row DMMA tiles
 //      over the group (tc_common.cuh: 16 DMMAs per tile for 3 pipes, 12 for 2);
-//   3. applies the pipe factors (W1 -> S; W2 (1/r), W3 (-ik), W4 -> D), sums the pipes of
-//      each evaluation across the quad and adds into the target's shared accumulators.
+//   3. applies the pipe factors (W1 -> S; W2 (1/r), W3 (-ik), W4 -> D), adds the D pipes of
+//      each evaluation (one shuffle) and accumulates into the target's shared accumulators.
 // Every target gets its cousins' contributions in cousin-list order: deterministic.
 #include "ifgf_device.cuh"
 #include "kernels.cuh"
@@ -47,6 +47,13 @@ cousin_tc_kernel(LevelDev L, PointsDev P, const double2* __restrict__ store, dou
     const double h = L.h;
     sacc[warp][lane][0] = sacc[warp][lane][1] = make_double2(0.0, 0.0);
     const int fpipe = tig < NPC ? pp.f[tig] : 0;  // factor code of the pipe this lane gathers
+    // S comes from the W1 lane alone; D from the first D-pipe lane plus, for (W2, W3), its
+    // right neighbour (pipe lists keep W2, W3 adjacent)
+    int s_lane = -1, d_lane = -1, n_d = 0;
+    for (int i = 0; i < NPC; ++i) {
+        if (pp.f[i] == 1) s_lane = i;
+        else if (n_d++ == 0) d_lane = i;
+    }
     const int j0 = L.cz_ptr[tb], j1 = L.cz_ptr[tb + 1];
     const std::int64_t ev0 = L.cev_begin[tb] + q;
     double* mygeo = sgeo[warp] + lane * kCG;
@@ -94,17 +101,13 @@ cousin_tc_kernel(LevelDev L, PointsDev P, const double2* __restrict__ store, dou
                     case 4: cD = w; break;
                     default: break;
                 }
-#pragma unroll
-                for (int o = 1; o < 4; o <<= 1) {
-                    cS.x += __shfl_xor_sync(0xffffffffu, cS.x, o);
-                    cS.y += __shfl_xor_sync(0xffffffffu, cS.y, o);
-                    cD.x += __shfl_xor_sync(0xffffffffu, cD.x, o);
-                    cD.y += __shfl_xor_sync(0xffffffffu, cD.y, o);
+                if (n_d == 2) {
+                    const double ox = __shfl_down_sync(0xffffffffu, cD.x, 1);
+                    const double oy = __shfl_down_sync(0xffffffffu, cD.y, 1);
+                    cD = make_double2(cD.x + ox, cD.y + oy);
                 }
-                if (valid && tig == 0) {
-                    sacc[warp][src][0] = cadd(sacc[warp][src][0], cS);
-                    sacc[warp][src][1] = cadd(sacc[warp][src][1], cD);
-                }
+                if (valid && tig == s_lane) sacc[warp][src][0] = cadd(sacc[warp][src][0], cS);
+                if (valid && tig == d_lane) sacc[warp][src][1] = cadd(sacc[warp][src][1], cD);
             }
             __syncwarp();
         }
@@ -120,6 +123,7 @@ cousin_tc_kernel(LevelDev L, PointsDev P, const double2* __restrict__ store, dou
 bool launch_cousin_eval_tc(const LevelDev& L, const PointsDev& P, const double2* store, double k, const Pipes& pipes,
                            double2* Sp, double2* Dp, cudaStream_t st) {
     if (L.ps != kPS || L.pang != kPA || pipes.n < 1 || pipes.n > 3) return false;
+    if (pipes.n == 3 && pipes.f[1] == 1) return false;  // D pipes must be adjacent (epilogue shuffle)
     if (L.nwchunk == 0) return true;
     const int grid = (L.nwchunk + kWarps - 1) / kWarps;
     switch (pipes.n) {
