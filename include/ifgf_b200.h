@@ -196,6 +196,14 @@ int ifgf_gmres_solve(ifgf_operator* op, const double* rhs, double tol, int max_i
 int ifgf_solve(ifgf_operator* op, double theta, double phi, double tol, int max_iter,
                int restart, double* density, double* history, int history_cap,
                int* iterations, int* converged);
+/* solve(mesh, incident, cfg) for either IncidentField kind (solver.hpp:17-26): point sources
+ * src (3*nsrc) when nsrc > 0, else the plane wave (theta, phi) */
+int ifgf_solve_incident(ifgf_operator* op, double theta, double phi, const double* src, int64_t nsrc,
+                        double tol, int max_iter, int restart, double* density, double* history,
+                        int history_cap, int* iterations, int* converged);
+/* incident_trace (solver.hpp:28-30): u^i at the nodes, 2*N doubles */
+int ifgf_incident_trace(const ifgf_surface* s, double k, double theta, double phi,
+                        const double* src, int64_t nsrc, double* out);
 
 /* ---- fields after the solve (postprocess.cpp). The dense sums run on
  * GPU `device` over the oversampled per-patch Fejér quadrature of the density. ---- */

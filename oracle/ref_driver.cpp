@@ -507,4 +507,25 @@ int ref_mie_far_field(double radius, double k, const double* direction, const do
     }
 }
 
+int ref_solve_sources(void* mesh, double k, double gamma, const double* src, long nsrc, double tol, int max_iter,
+                      int restart, double* density_out, double* hist_out, int hist_cap) {
+    try {
+        SolveConfig cfg;
+        cfg.k = k;
+        cfg.gamma = gamma;
+        cfg.tol = tol;
+        cfg.max_iter = max_iter;
+        cfg.restart = restart;
+        IncidentField inc;
+        inc.kind = IncidentField::Kind::PointSources;
+        for (long j = 0; j < nsrc; ++j) inc.sources.push_back({src[3 * j], src[3 * j + 1], src[3 * j + 2]});
+        const auto res = solve(M(mesh), inc, cfg);
+        from_cplx(res.density, density_out);
+        for (int i = 0; i < int(res.residual_history.size()) && i < hist_cap; ++i) hist_out[i] = res.residual_history[i];
+        return res.iterations;
+    } catch (const std::exception& e) {
+        return -fail(e);
+    }
+}
+
 }  // extern "C"

@@ -5,14 +5,14 @@ operator API (solver.hpp / geometry.hpp / ifgf.hpp / rp.hpp)."""
 from ._lib import (ConvergenceFailure, DegenerateGeometry, DeviceError, IfgfError, InternalError,
                    InvalidArgument, ParseError, lib)
 from .operator import (CombinedOperator, ConeConfig, DlStrategy, Factor, GmresResult, HostPlan,
-                       IncidentField, RpConfig, SolveConfig, SurfaceMesh, gmres_solve, nccl_unique_id,
+                       IncidentField, RpConfig, SolveConfig, SurfaceMesh, gmres_solve, incident_trace, nccl_unique_id,
                        random_density, solve)
 from .postprocess import (FarFieldGrid, NearFieldGrid, eps_far, eps_near, far_field, mie_far_field,
                           near_field)
 
 __all__ = [
     "CombinedOperator", "ConeConfig", "DlStrategy", "Factor", "GmresResult", "HostPlan", "IncidentField",
-    "RpConfig", "SolveConfig", "SurfaceMesh", "gmres_solve", "nccl_unique_id", "random_density", "solve", "lib",
+    "RpConfig", "SolveConfig", "SurfaceMesh", "gmres_solve", "incident_trace", "nccl_unique_id", "random_density", "solve", "lib",
     "IfgfError", "InvalidArgument", "ParseError", "DegenerateGeometry", "ConvergenceFailure",
     "InternalError", "DeviceError", "FarFieldGrid", "NearFieldGrid", "far_field", "near_field",
     "mie_far_field", "eps_far", "eps_near",

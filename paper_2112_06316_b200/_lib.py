@@ -113,6 +113,9 @@ _SIGS = {
                                    C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "ifgf_solve": (C.c_int, [vp, C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, d_p, d_p, C.c_int,
                              C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "ifgf_solve_incident": (C.c_int, [vp, C.c_double, C.c_double, d_p, C.c_int64, C.c_double, C.c_int, C.c_int, d_p,
+                                      d_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "ifgf_incident_trace": (C.c_int, [vp, C.c_double, C.c_double, C.c_double, d_p, C.c_int64, d_p]),
     "ifgf_far_field": (C.c_int, [vp, d_p, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, d_p, d_p]),
     "ifgf_near_field": (C.c_int, [vp, d_p, C.c_double, C.c_double, C.c_double, C.c_double, d_p, C.c_int64, d_p,
                                   C.c_int64, C.c_double, C.c_int, d_p, d_p, C.POINTER(C.c_uint8)]),

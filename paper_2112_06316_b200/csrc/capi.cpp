@@ -957,16 +957,53 @@ int ifgf_gmres_solve(ifgf_operator* op, const double* rhs, double tol, int max_i
     });
 }
 
-int ifgf_solve(ifgf_operator* op, double theta, double phi, double tol, int max_iter, int restart, double* density,
-               double* history, int history_cap, int* iterations, int* converged) {
+namespace {
+// incident_at (solver.cpp:25-35): plane wave along (cos t sin p, sin t sin p, cos p), or the
+// sum of e^{ikr}/r over point sources when nsrc > 0
+cplx incident_value(const Vec3& x, double k, const Vec3& dir, const double* src, int64_t nsrc) {
+    if (nsrc <= 0) return std::polar(1.0, k * dot3(dir, x));
+    cplx acc{};
+    for (int64_t j = 0; j < nsrc; ++j) {
+        const Vec3 y{src[3 * j], src[3 * j + 1], src[3 * j + 2]};
+        const double r = len(x - y);
+        if (r < 1e-12) throw InvalidArgument("incident_at: point source coincides with node");
+        acc += std::polar(1.0 / r, k * r);
+    }
+    return acc;
+}
+Vec3 wave_direction(double theta, double phi) {
+    return {std::cos(theta) * std::sin(phi), std::sin(theta) * std::sin(phi), std::cos(phi)};
+}
+}  // namespace
+
+int ifgf_incident_trace(const ifgf_surface* s, double k, double theta, double phi, const double* src, int64_t nsrc,
+                        double* out) {
+    return guarded([&] {
+        need(s, "surface");
+        need(out, "out");
+        if (nsrc > 0) need(src, "point sources");
+        const Surface& S = *s->s;
+        const Vec3 dir = wave_direction(theta, phi);
+        for (std::size_t l = 0; l < S.size(); ++l) {
+            const cplx u = incident_value(S.pos[l], k, dir, src, nsrc);
+            out[2 * l] = u.real();
+            out[2 * l + 1] = u.imag();
+        }
+    });
+}
+
+int ifgf_solve_incident(ifgf_operator* op, double theta, double phi, const double* src, int64_t nsrc, double tol,
+                        int max_iter, int restart, double* density, double* history, int history_cap,
+                        int* iterations, int* converged) {
     return guarded([&] {
         need(op, "operator");
+        if (nsrc > 0) need(src, "point sources");
         const Surface& s = *op->plan->surf;
         const double k = op->plan->k;
-        const Vec3 dir{std::cos(theta) * std::sin(phi), std::sin(theta) * std::sin(phi), std::cos(phi)};
-        std::vector<double> rhs(2 * s.size());
+        const Vec3 dir = wave_direction(theta, phi);
+        std::vector<double> rhs(2 * s.size());  // -u^i on the nodes (solver.hpp:28-29)
         for (std::size_t l = 0; l < s.size(); ++l) {
-            const cplx ui = std::polar(1.0, k * dot3(dir, s.pos[l]));
+            const cplx ui = incident_value(s.pos[l], k, dir, src, nsrc);
             rhs[2 * l] = -ui.real();
             rhs[2 * l + 1] = -ui.imag();
         }
@@ -980,6 +1017,12 @@ int ifgf_solve(ifgf_operator* op, double theta, double phi, double tol, int max_
                                          std::to_string(it) + " iterations",
                                      {});
     });
+}
+
+int ifgf_solve(ifgf_operator* op, double theta, double phi, double tol, int max_iter, int restart, double* density,
+               double* history, int history_cap, int* iterations, int* converged) {
+    return ifgf_solve_incident(op, theta, phi, nullptr, 0, tol, max_iter, restart, density, history, history_cap,
+                               iterations, converged);
 }
 
 // ------------------------------------------------------------------ fields

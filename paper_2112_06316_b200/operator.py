@@ -470,19 +470,40 @@ def gmres_solve(op: CombinedOperator, rhs, tol: float, max_iter: int, restart: i
 
 
 @dataclass
-class IncidentField:  # solver.hpp:17-26 (plane wave)
+class IncidentField:  # solver.hpp:17-26: plane wave (theta, phi) or point sources
     theta: float = 0.0
     phi: float = float(np.pi)
+    sources: object = None  # (n, 3) point-source positions: Kind::PointSources when given
+
+    def wave_direction(self) -> np.ndarray:
+        return np.array([np.cos(self.theta) * np.sin(self.phi), np.sin(self.theta) * np.sin(self.phi),
+                         np.cos(self.phi)])
+
+    def _src(self):
+        if self.sources is None:
+            return np.zeros((0, 3))
+        return np.ascontiguousarray(self.sources, dtype=np.float64).reshape(-1, 3)
+
+
+def incident_trace(incident: IncidentField, mesh: SurfaceMesh, k: float) -> np.ndarray:
+    """u^i at the surface nodes (solver.hpp:28-30)."""
+    src = incident._src()
+    out = np.zeros(mesh.size(), dtype=np.complex128)
+    check(lib().ifgf_incident_trace(mesh._h, k, incident.theta, incident.phi, _ptr(src), src.shape[0], _ptr(out)),
+          "incident_trace")
+    return out
 
 
 def solve(op: CombinedOperator, incident: IncidentField, tol=None, max_iter=None, restart=None) -> GmresResult:
+    """solve(mesh, incident, cfg) (solver.hpp:111-112): GMRES on the device for -u^i."""
     tol = op.cfg.tol if tol is None else tol
     max_iter = op.cfg.max_iter if max_iter is None else max_iter
     restart = op.cfg.restart if restart is None else restart
+    src = incident._src()
     x = np.zeros(op.n, dtype=np.complex128)
     hist = np.zeros(max_iter + 1)
     it = C.c_int()
     cv = C.c_int()
-    check(lib().ifgf_solve(op._h, incident.theta, incident.phi, tol, max_iter, restart, _ptr(x), _ptr(hist),
-                           len(hist), C.byref(it), C.byref(cv)), "solve")
+    check(lib().ifgf_solve_incident(op._h, incident.theta, incident.phi, _ptr(src), src.shape[0], tol, max_iter,
+                                    restart, _ptr(x), _ptr(hist), len(hist), C.byref(it), C.byref(cv)), "solve")
     return GmresResult(x, hist[: it.value].tolist(), it.value, bool(cv.value))

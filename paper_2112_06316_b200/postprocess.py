@@ -54,6 +54,8 @@ def near_field(mesh: SurfaceMesh, density, gamma: float, k: float, incident: Inc
     (postprocess.cpp:106-139); `sources` switches the incidence to point sources."""
     phi = _cvec(density, mesh.size())
     pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    if sources is None and incident.sources is not None:
+        sources = incident.sources
     src = np.ascontiguousarray(sources if sources is not None else np.zeros((0, 3)), dtype=np.float64).reshape(-1, 3)
     npts = pts.shape[0]
     sc = np.zeros(npts, dtype=np.complex128)

@@ -79,3 +79,30 @@ def test_solved_sphere_far_field_against_mie(ref):
     _, rvals = _ref_far(ref, rm, dens.view(np.complex128), op.gamma, k, 21, 41)
     eps_ref, _ = P.eps_far(mie, rvals)
     assert abs(eps - eps_ref) <= 1e-6 * max(eps_ref, 1e-12) + 1e-9
+
+
+def test_point_source_solve_and_exterior_cancellation(ref):
+    # IncidentField::Kind::PointSources (solver.hpp:17-26): GMRES matches the reference's
+    # iterations, and for sources INSIDE the sound-soft sphere the exterior total field
+    # vanishes (scattered = -incident), a check of the whole solve + near-field chain
+    k = 2 * np.pi
+    pm = P.SurfaceMesh.sphere(1.0, 2, 10, 10)
+    op = P.CombinedOperator(pm, P.SolveConfig(k=k))
+    src = np.array([[0.1, -0.2, 0.15], [-0.3, 0.05, 0.0]])
+    inc = P.IncidentField(sources=src)
+    res = P.solve(op, inc, tol=1e-8, max_iter=200)
+    assert res.converged
+    rm = ref.RefMesh.sphere(1.0, 2, 10, 10)
+    dens = np.zeros(2 * pm.size())
+    hist = np.zeros(200)
+    it = ref.lib().ref_solve_sources(rm.h, k, -1.0, ref._p(np.ascontiguousarray(src)), len(src), 1e-8, 200, 0,
+                                     ref._p(dens), ref._p(hist), 200)
+    assert it == res.iterations
+    assert np.allclose(res.residual_history, hist[:it], rtol=1e-7, atol=0)
+    rng = np.random.default_rng(9)
+    d = rng.normal(size=(50, 3))
+    pts = d / np.linalg.norm(d, axis=1)[:, None] * rng.uniform(1.5, 3.0, size=(50, 1))
+    nf = P.near_field(pm, res.solution, op.gamma, k, inc, pts, 0.05)
+    assert not nf.flagged.any()
+    u_inc = nf.total - nf.scattered
+    assert np.max(np.abs(nf.total)) <= 1e-4 * np.max(np.abs(u_inc))
