@@ -29,6 +29,7 @@
  *   ifgf_far_field          far_field (+ FarFieldGrid::make)           postprocess.hpp:34-37
  *   ifgf_near_field         near_field                                 postprocess.hpp:39-41
  *   ifgf_mie_far_field      mie_far_field                              postprocess.hpp:44-45
+ *   ifgf_rp_regular_apply   rp_regular_apply                           rp.hpp:78-82
  *   ifgf_eps_metric         eps_far / eps_near                         postprocess.hpp:49-52
  */
 #ifndef IFGF_B200_H
@@ -218,6 +219,10 @@ int ifgf_near_field(const ifgf_surface* s, const double* density, double gamma, 
                     double inc_theta, double inc_phi, const double* src, int64_t nsrc,
                     const double* points, int64_t npts, double flag_distance, int device,
                     double* scattered, double* total, uint8_t* flagged);
+/* regular Fejér-rule S and D of the density at off-surface targets (3*n), ADDED into S / D
+ * (2*n each); a target within 1e-14 of a node is InvalidArgument (rp.cpp:453-479) */
+int ifgf_rp_regular_apply(const ifgf_surface* s, const double* density, const double* targets,
+                          int64_t ntargets, double k, int device, double* S, double* D);
 /* sound-soft sphere far field for a plane wave along direction (3) at n directions (3*n) */
 int ifgf_mie_far_field(double radius, double k, const double* direction, const double* dirs,
                        int64_t n, int extra_terms, double* values);

@@ -14,6 +14,7 @@
 //   gmres_solve / solve                   src/solver.cpp:270-340
 //   save_beta_cache                       src/rp.cpp:515-536
 //   far_field / near_field / mie_far_field src/postprocess.cpp:83-205
+//   rp_regular_apply                      src/rp.cpp:453-479
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -523,6 +524,22 @@ int ref_solve_sources(void* mesh, double k, double gamma, const double* src, lon
         from_cplx(res.density, density_out);
         for (int i = 0; i < int(res.residual_history.size()) && i < hist_cap; ++i) hist_out[i] = res.residual_history[i];
         return res.iterations;
+    } catch (const std::exception& e) {
+        return -fail(e);
+    }
+}
+
+int ref_rp_regular_apply(void* mesh, const double* density, const double* targets, long n, double k, double* S,
+                         double* D) {
+    try {
+        const auto dens = to_cplx(density, M(mesh).size());
+        std::vector<Vec3> t(n);
+        for (long i = 0; i < n; ++i) t[i] = {targets[3 * i], targets[3 * i + 1], targets[3 * i + 2]};
+        std::vector<cplx> s(n), d(n);
+        rp_regular_apply(M(mesh), dens, t, k, s, d, 0);
+        from_cplx(s, S);
+        from_cplx(d, D);
+        return 0;
     } catch (const std::exception& e) {
         return -fail(e);
     }

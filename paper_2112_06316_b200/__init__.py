@@ -8,12 +8,12 @@ from .operator import (CombinedOperator, ConeConfig, DlStrategy, Factor, GmresRe
                        IncidentField, RpConfig, SolveConfig, SurfaceMesh, gmres_solve, incident_trace, nccl_unique_id,
                        random_density, solve)
 from .postprocess import (FarFieldGrid, NearFieldGrid, eps_far, eps_near, far_field, mie_far_field,
-                          near_field)
+                          near_field, rp_regular_apply)
 
 __all__ = [
     "CombinedOperator", "ConeConfig", "DlStrategy", "Factor", "GmresResult", "HostPlan", "IncidentField",
     "RpConfig", "SolveConfig", "SurfaceMesh", "gmres_solve", "incident_trace", "nccl_unique_id", "random_density", "solve", "lib",
     "IfgfError", "InvalidArgument", "ParseError", "DegenerateGeometry", "ConvergenceFailure",
     "InternalError", "DeviceError", "FarFieldGrid", "NearFieldGrid", "far_field", "near_field",
-    "mie_far_field", "eps_far", "eps_near",
+    "mie_far_field", "eps_far", "eps_near", "rp_regular_apply",
 ]

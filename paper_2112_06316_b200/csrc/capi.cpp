@@ -1092,6 +1092,47 @@ int ifgf_near_field(const ifgf_surface* s, const double* density, double gamma, 
     });
 }
 
+int ifgf_rp_regular_apply(const ifgf_surface* s, const double* density, const double* targets, int64_t ntargets,
+                          double k, int device, double* S, double* D) {
+    return guarded([&] {
+        need(s, "surface");
+        need(density, "density");
+        if (ntargets > 0) {
+            need(targets, "targets");
+            need(S, "out_single");
+            need(D, "out_dbl");
+        }
+        const Surface& sf = *s->s;
+        // the nodal Fejer rule itself (rp.cpp:453-479): nodes, normals, J w, density
+        FineQuad q;
+        const auto phi = as_cplx(density, sf.size());
+        for (std::size_t m = 0; m < sf.size(); ++m) {
+            q.x.push_back(sf.pos[m].x);
+            q.y.push_back(sf.pos[m].y);
+            q.z.push_back(sf.pos[m].z);
+            q.nx.push_back(sf.nrm[m].x);
+            q.ny.push_back(sf.nrm[m].y);
+            q.nz.push_back(sf.nrm[m].z);
+            q.jw.push_back(sf.jac[m] * sf.wt[m]);
+            q.density.push_back(phi[m]);
+        }
+        const std::size_t n = std::size_t(std::max<int64_t>(ntargets, 0));
+        std::vector<Vec3> pts(n);
+        for (std::size_t i = 0; i < n; ++i) pts[i] = {targets[3 * i], targets[3 * i + 1], targets[3 * i + 2]};
+        std::vector<cplx> s_out(n), d_out(n);
+        std::vector<double> dmin(n), gauss(n);
+        gpu_layer_potentials_at(q, pts, k, device, s_out.data(), d_out.data(), dmin.data(), gauss.data());
+        for (std::size_t i = 0; i < n; ++i)
+            if (dmin[i] < 1e-14) throw InvalidArgument("rp_regular_apply: target coincides with a node");
+        for (std::size_t i = 0; i < n; ++i) {  // accumulated into the outputs, like the reference
+            S[2 * i] += s_out[i].real();
+            S[2 * i + 1] += s_out[i].imag();
+            D[2 * i] += d_out[i].real();
+            D[2 * i + 1] += d_out[i].imag();
+        }
+    });
+}
+
 int ifgf_mie_far_field(double radius, double k, const double* direction, const double* dirs, int64_t n,
                        int extra_terms, double* values) {
     return guarded([&] {

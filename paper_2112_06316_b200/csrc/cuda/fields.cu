@@ -64,9 +64,9 @@ __global__ void __launch_bounds__(kT) far_field_kernel(QuadDev Q, int nd, const 
 
 __global__ void __launch_bounds__(kT) near_field_kernel(QuadDev Q, int np, const double* __restrict__ px,
                                                         const double* __restrict__ py,
-                                                        const double* __restrict__ pz, double k, double gamma,
-                                                        double2* __restrict__ scat, double* __restrict__ dmin_out,
-                                                        double* __restrict__ gauss_out) {
+                                                        const double* __restrict__ pz, double k,
+                                                        double2* __restrict__ S_out, double2* __restrict__ D_out,
+                                                        double* __restrict__ dmin_out, double* __restrict__ gauss_out) {
     __shared__ double sx[kT], sy[kT], sz[kT], snx[kT], sny[kT], snz[kT], sw[kT];
     __shared__ double2 sa[kT];
     const int t = blockIdx.x * kT + threadIdx.x;
@@ -112,8 +112,8 @@ __global__ void __launch_bounds__(kT) near_field_kernel(QuadDev Q, int np, const
         }
     }
     if (!act) return;
-    // scattered = D - i gamma S
-    scat[t] = make_double2(accd.x + gamma * accs.y, accd.y - gamma * accs.x);
+    S_out[t] = accs;
+    D_out[t] = accd;
     dmin_out[t] = dmin;
     gauss_out[t] = gauss;
 }
@@ -182,11 +182,11 @@ void gpu_far_field(const FineQuad& q, const std::vector<Vec3>& dirs, double k, d
     o.get(reinterpret_cast<double2*>(out), nd);
 }
 
-void gpu_near_field(const FineQuad& q, const std::vector<Vec3>& pts, double k, double gamma, int device,
-                    cplx* scattered, double* dmin, double* gauss) {
+void gpu_layer_potentials_at(const FineQuad& q, const std::vector<Vec3>& pts, double k, int device, cplx* S, cplx* D,
+                             double* dmin, double* gauss) {
     IFGF_CUDA(cudaSetDevice(device));
     if (q.size() > std::size_t(0x7fffffff) || pts.size() > std::size_t(0x7fffffff))
-        throw InvalidArgument("near_field: too many nodes or points");
+        throw InvalidArgument("layer potentials: too many nodes or points");
     QuadBufs Q(q);
     const std::size_t np = pts.size();
     std::vector<double> hx(np), hy(np), hz(np);
@@ -196,18 +196,26 @@ void gpu_near_field(const FineQuad& q, const std::vector<Vec3>& pts, double k, d
         hz[i] = pts[i].z;
     }
     Buf<double> px(np), py(np), pz(np), dm(np), ga(np);
-    Buf<double2> sc(np);
+    Buf<double2> s_out(np), d_out(np);
     px.put(hx.data(), np);
     py.put(hy.data(), np);
     pz.put(hz.data(), np);
     if (np)
-        near_field_kernel<<<int((np + kT - 1) / kT), kT>>>(Q.dev, int(np), px.p, py.p, pz.p, k, gamma, sc.p, dm.p,
+        near_field_kernel<<<int((np + kT - 1) / kT), kT>>>(Q.dev, int(np), px.p, py.p, pz.p, k, s_out.p, d_out.p, dm.p,
                                                             ga.p);
     IFGF_CUDA(cudaGetLastError());
     IFGF_CUDA(cudaDeviceSynchronize());
-    sc.get(reinterpret_cast<double2*>(scattered), np);
+    s_out.get(reinterpret_cast<double2*>(S), np);
+    d_out.get(reinterpret_cast<double2*>(D), np);
     dm.get(dmin, np);
     ga.get(gauss, np);
+}
+
+void gpu_near_field(const FineQuad& q, const std::vector<Vec3>& pts, double k, double gamma, int device,
+                    cplx* scattered, double* dmin, double* gauss) {
+    std::vector<cplx> S(pts.size()), D(pts.size());
+    gpu_layer_potentials_at(q, pts, k, device, S.data(), D.data(), dmin, gauss);
+    for (std::size_t i = 0; i < pts.size(); ++i) scattered[i] = D[i] - cplx(0.0, gamma) * S[i];  // D - i gamma S
 }
 
 }  // namespace ifgfb200

@@ -17,6 +17,10 @@ void gpu_far_field(const FineQuad& q, const std::vector<Vec3>& dirs, double k, d
 // (postprocess.cpp:106-139; the caller adds the incident field and sets the flags)
 void gpu_near_field(const FineQuad& q, const std::vector<Vec3>& pts, double k, double gamma, int device,
                     cplx* scattered, double* dmin, double* gauss);
+// S and D of the quadrature's density at `pts` (zero contribution from nodes within 1e-14),
+// with the closest-node distance and the unit-density static double layer
+void gpu_layer_potentials_at(const FineQuad& q, const std::vector<Vec3>& pts, double k, int device, cplx* S, cplx* D,
+                             double* dmin, double* gauss);
 // closest_point_on for every non-own request, bit for bit (ClosestPointBatch)
 // segment decisions of one plan level (ConeDecider); uncertain ones are flagged for the host
 void gpu_cone_decisions(const ConeDecisionJob& job, ConeLevel& L, std::vector<std::uint8_t>& marks,

@@ -67,6 +67,19 @@ def near_field(mesh: SurfaceMesh, density, gamma: float, k: float, incident: Inc
     return NearFieldGrid(pts, sc, tot, flg)
 
 
+def rp_regular_apply(mesh: SurfaceMesh, density, targets, k: float, out_single=None, out_dbl=None,
+                     device: int = 0):
+    """S and D of the density at off-surface targets by the nodal Fejér rule (rp.hpp:78-82),
+    added into out_single / out_dbl (new zero arrays when not given); returns both."""
+    phi = _cvec(density, mesh.size())
+    t = np.ascontiguousarray(targets, dtype=np.float64).reshape(-1, 3)
+    S = np.zeros(t.shape[0], dtype=np.complex128) if out_single is None else _cvec(out_single, t.shape[0])
+    D = np.zeros(t.shape[0], dtype=np.complex128) if out_dbl is None else _cvec(out_dbl, t.shape[0])
+    check(lib().ifgf_rp_regular_apply(mesh._h, _ptr(phi), _ptr(t), t.shape[0], k, device, _ptr(S), _ptr(D)),
+          "rp_regular_apply")
+    return S, D
+
+
 def mie_far_field(radius: float, k: float, direction, eval_directions, extra_terms: int = 0) -> np.ndarray:
     """Sound-soft sphere far field for plane-wave incidence along `direction`
     (postprocess.cpp:176-205)."""

@@ -106,3 +106,28 @@ def test_point_source_solve_and_exterior_cancellation(ref):
     assert not nf.flagged.any()
     u_inc = nf.total - nf.scattered
     assert np.max(np.abs(nf.total)) <= 1e-4 * np.max(np.abs(u_inc))
+
+
+def test_rp_regular_apply_matches_reference(ref):
+    # regular Fejer-rule S and D at off-surface targets (rp.hpp:78-82), accumulated into the
+    # outputs; a target on a node is InvalidArgument like the reference
+    k = 3 * np.pi
+    pm = P.SurfaceMesh.sphere(1.0, 1, 8, 8)
+    rm = ref.RefMesh.sphere(1.0, 1, 8, 8)
+    dens = P.random_density(pm.size(), 4)
+    rng = np.random.default_rng(2)
+    d = rng.normal(size=(60, 3))
+    t = d / np.linalg.norm(d, axis=1)[:, None] * rng.uniform(0.2, 3.0, size=(60, 1))
+    S0 = np.full(60, 0.5 + 0.25j)
+    S, D = P.rp_regular_apply(pm, dens, t, k, out_single=S0.copy())
+    rs = np.zeros(120)
+    rd = np.zeros(120)
+    dd = np.ascontiguousarray(dens).view(np.float64)
+    assert ref.lib().ref_rp_regular_apply(rm.h, ref._p(dd), ref._p(np.ascontiguousarray(t)), 60, k, ref._p(rs),
+                                          ref._p(rd)) == 0
+    rs = rs.view(np.complex128)
+    rd = rd.view(np.complex128)
+    assert np.max(np.abs(S - S0 - rs)) <= 1e-12 * np.max(np.abs(rs))
+    assert np.max(np.abs(D - rd)) <= 1e-12 * np.max(np.abs(rd))
+    with pytest.raises(P.InvalidArgument):
+        P.rp_regular_apply(pm, dens, pm.nodes()["pos"][:2], k)
