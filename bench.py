@@ -36,11 +36,22 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
-    # name: (splits, nodes per patch side, k, gamma, description)
+    # name: (splits, nodes per patch side, k, gamma, description); SPHEROIDS adds the axes
     "cfg1": (2, 16, 4 * np.pi, 4 * np.pi, "sphere r=1, 4 wavelengths, 96 patches x 16^2, k=4pi, gamma=k"),
     "cfg2": (4, 16, 16 * np.pi, -1.0, "sphere r=1, 16 wavelengths, 1536 patches x 16^2, k=16pi"),
     "cfg3": (6, 16, 64 * np.pi, -1.0, "sphere r=1, 64 wavelengths, 24576 patches x 16^2, k=64pi"),
+    "cfg4": (6, 16, 2 * np.pi, -1.0, "spheroid (40,4,4) lambda=1, 24576 patches x 16^2, k=2pi"),
 }
+SPHEROIDS = {"cfg4": (40.0, 4.0, 4.0)}  # cube-sphere coefficients scaled
+
+
+def make_mesh(cfg_name, module):
+    """the config's surface from the product (paper_2112_06316_b200) or the oracle (oracle.ref)"""
+    splits, nu = CONFIGS[cfg_name][:2]
+    cls = module.SurfaceMesh if hasattr(module, "SurfaceMesh") else module.RefMesh
+    if cfg_name in SPHEROIDS:
+        return cls.spheroid(splits, nu, nu, *SPHEROIDS[cfg_name])
+    return cls.sphere(1.0, splits, nu, nu)
 
 
 def peaks():
@@ -132,7 +143,7 @@ def reference_apply_time(cfg_name, phi, beta_cache=None, applies=1, warmup=0):
     from oracle import ref as R
 
     splits, nu, k, gamma, _ = CONFIGS[cfg_name]
-    rm = R.RefMesh.sphere(1.0, splits, nu, nu)
+    rm = make_mesh(cfg_name, R)
     t0 = time.perf_counter()
     ro = R.RefOperator(rm, k, gamma=gamma, beta_cache=beta_cache or "")
     setup = time.perf_counter() - t0
@@ -235,7 +246,7 @@ def run_b200(args, ws, rank, local):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     splits, nu, k, gamma, desc = CONFIGS[args.config]
     t0 = time.perf_counter()
-    mesh = P.SurfaceMesh.sphere(1.0, splits, nu, nu)
+    mesh = make_mesh(args.config, P)
     cfg = P.SolveConfig(k=k, gamma=gamma, device=local)
     if ws > 1:  # one operator per GPU, Morton-partitioned, NCCL exchange inside the engine
         from paper_2112_06316_b200.distributed import DistributedCombinedOperator

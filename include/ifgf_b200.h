@@ -182,6 +182,9 @@ int ifgf_operator_set_comm(ifgf_operator* op, int rank, int world, const void* i
 int ifgf_operator_partition(const ifgf_operator* op, int parts, uint32_t* bounds);
 int ifgf_plan_partition(const ifgf_plan* p, int parts, uint32_t* bounds);
 /* own [lo, hi) without a communicator (single-GPU emulation of one rank) */
+/* (re)compute the beta tables on the GPU: all pairs, or — after set_partition / set_comm — only
+ * the pairs whose target this operator owns (target-sharded tables) */
+int ifgf_operator_compute_beta(ifgf_operator* op);
 int ifgf_operator_set_partition(ifgf_operator* op, uint32_t lo, uint32_t hi);
 /* near field + RP + combine for the owned targets given the full far field S, D
  * (original order, e.g. the sum of every rank's ifgf_operator_ifgf_apply); out is zero

@@ -108,6 +108,7 @@ _SIGS = {
     "ifgf_operator_partition": (C.c_int, [vp, C.c_int, u32_p]),
     "ifgf_plan_partition": (C.c_int, [vp, C.c_int, u32_p]),
     "ifgf_operator_set_partition": (C.c_int, [vp, C.c_uint32, C.c_uint32]),
+    "ifgf_operator_compute_beta": (C.c_int, [vp]),
     "ifgf_operator_finish_owned": (C.c_int, [vp, d_p, d_p, d_p, d_p]),
     "ifgf_gmres_solve": (C.c_int, [vp, d_p, C.c_double, C.c_int, C.c_int, d_p, d_p, C.c_int,
                                    C.POINTER(C.c_int), C.POINTER(C.c_int)]),

@@ -646,6 +646,15 @@ int ifgf_operator_from_plan(ifgf_plan* p, int device, int compute_beta, ifgf_ope
     });
 }
 
+int ifgf_operator_compute_beta(ifgf_operator* op) {
+    return guarded([&] {
+        need(op, "operator");
+        const auto t = std::chrono::steady_clock::now();
+        op->eng->compute_beta();
+        op->t_beta = std::chrono::duration<double>(std::chrono::steady_clock::now() - t).count();
+    });
+}
+
 void ifgf_operator_free(ifgf_operator* op) { delete op; }
 int64_t ifgf_operator_size(const ifgf_operator* op) { return op ? int64_t(op->eng->size()) : -1; }
 double ifgf_operator_gamma(const ifgf_operator* op) { return op ? op->plan->gamma : 0.0; }

@@ -29,8 +29,8 @@ __global__ void __launch_bounds__(kBetaThreads)
 beta_kernel(BetaDev B, int TT, int max_dv, int max_nu, int max_nunv, int p_base,
             double2* __restrict__ bs_out, double2* __restrict__ bd_out) {
     extern __shared__ double sm[];
-    const int pl = blockIdx.x;       // pair within the batch
-    const int p = p_base + pl;       // global pair
+    const int pl = blockIdx.x;            // pair within the batch
+    const int p = int(B.pidx[p_base + pl]);  // global pair
     const int nb = B.n_beta;
     const int q = B.patch[p];
     const int nu = B.nu[q], nv = B.nv[q], du = B.du[q], dv = B.dv[q];

@@ -118,6 +118,35 @@ struct Engine::Impl {
     RpDev rp;
     std::size_t beta_entries = 0;
     bool beta_ready = false;
+    bool beta_sharded = false;              // tables hold only the owned targets' pairs
+    std::vector<std::uint64_t> beta_off_full;  // per pair offsets of the full tables (host)
+
+    // storage for the pairs in `pairs_idx` (all pairs when empty list means full), offsets
+    // compacted; non-stored pairs get offset 0 and are never read (their targets are not owned)
+    void alloc_beta(const std::vector<std::uint32_t>* owned) {
+        std::vector<std::uint64_t> off;
+        std::size_t entries;
+        if (!owned) {
+            off = beta_off_full;
+            entries = beta_off_full.back();
+        } else {
+            off.assign(beta_off_full.size(), 0);
+            std::uint64_t acc = 0;
+            for (std::uint32_t p : *owned) {
+                off[p] = acc;
+                acc += beta_off_full[p + 1] - beta_off_full[p];
+            }
+            entries = acc;
+        }
+        beta_off.upload(off);
+        beta_s.alloc(std::max<std::size_t>(entries, 1) * sizeof(double2));
+        beta_d.alloc(std::max<std::size_t>(entries, 1) * sizeof(double2));
+        rp.beta_off = beta_off.as<std::uint64_t>();
+        rp.beta_s = beta_s.as<double2>();
+        rp.beta_d = beta_d.as<double2>();
+        beta_sharded = owned != nullptr;
+        drop_graph();
+    }
     // beta inputs
     DevBuf b_target, b_ubar, b_vbar, b_du, b_dv, b_orient, b_series_off, b_series, b_cutoff,
         b_gu, b_gwu, b_gv, b_gwv;
@@ -212,6 +241,7 @@ struct Engine::Impl {
 
     // ---- multi-GPU: source ownership by Morton ranges of leaf boxes
     std::uint32_t own_lo = 0, own_hi = 0;
+    bool partitioned = false;
     std::vector<DevBuf> active;  // per level, uint8 per box
     int rank = 0, world = 1;
     std::vector<std::uint32_t> bounds;  // world + 1 Morton boundaries
@@ -229,6 +259,7 @@ struct Engine::Impl {
         if (lo > hi || hi > n) throw InvalidArgument("partition: bad Morton range");
         own_lo = lo;
         own_hi = hi;
+        partitioned = !(lo == 0 && hi == n);
         const bool all = lo == 0 && hi == n;
         active.resize(depth);
         for (int d = 3; d <= depth; ++d) {
@@ -658,10 +689,8 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
             const Patch& p = S.patches[PL.patch[i]];
             boff[i + 1] = boff[i] + std::uint64_t(p.nu) * p.nv;
         }
-        e.beta_entries = boff.back();
-        e.beta_off.upload(boff);
-        e.beta_s.alloc(std::max<std::size_t>(e.beta_entries, 1) * sizeof(double2));
-        e.beta_d.alloc(std::max<std::size_t>(e.beta_entries, 1) * sizeof(double2));
+        e.beta_entries = boff.back();  // full tables; storage comes with compute/upload_beta
+        e.beta_off_full = std::move(boff);
         e.coeffs.alloc(std::max<std::size_t>(n, 1) * sizeof(double2));
         RpDev& rp = e.rp;
         rp.n = int(n);
@@ -673,9 +702,7 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         rp.mats = e.mats.as<double>();
         rp.tpb = e.tpb.as<std::uint32_t>();
         rp.pair_patch = e.pair_patch.as<std::int32_t>();
-        rp.beta_off = e.beta_off.as<std::uint64_t>();
-        rp.beta_s = e.beta_s.as<double2>();
-        rp.beta_d = e.beta_d.as<double2>();
+        // rp.beta_off / beta_s / beta_d are set when the tables are allocated (alloc_beta)
         rp.pos = e.pos.as<std::uint32_t>();
         rp.max_nn = max_nn;
         // beta inputs
@@ -732,7 +759,6 @@ void Engine::compute_beta() {
     B.patch = e.pair_patch.as<std::int32_t>();
     B.ubar = e.b_ubar.as<double>();
     B.vbar = e.b_vbar.as<double>();
-    B.offset = e.beta_off.as<std::uint64_t>();
     B.tx = e.ox.as<double>();
     B.ty = e.oy.as<double>();
     B.tz = e.oz.as<double>();
@@ -744,10 +770,26 @@ void Engine::compute_beta() {
     B.series_off = e.b_series_off.as<std::int64_t>();
     B.series = e.b_series.as<double>();
     B.cutoff = e.b_cutoff.as<double>();
+    // the pairs to compute: all, or (under a partition) those whose target this engine owns
+    const bool shard = e.partitioned;
+    std::vector<std::uint32_t> idx;
+    {
+        std::vector<std::uint32_t> pos(e.n);
+        for (std::size_t t = 0; t < e.n; ++t) pos[e.tree->perm[t]] = std::uint32_t(t);
+        for (std::size_t p = 0; p < e.pairs->size(); ++p) {
+            const std::uint32_t m = pos[e.pairs->target[p]];
+            if (!shard || (m >= e.own_lo && m < e.own_hi)) idx.push_back(std::uint32_t(p));
+        }
+    }
+    e.alloc_beta(shard ? &idx : nullptr);
+    B.offset = e.beta_off.as<std::uint64_t>();
+    DevBuf d_idx;
+    d_idx.upload(idx);
+    B.pidx = d_idx.as<std::uint32_t>();
     // graded rules on the host (glibc pow, bit-identical to the reference), in batches
-    const std::size_t np = e.pairs->size();
+    const std::size_t np = idx.size();
     const int nb = B.n_beta;
-    const std::size_t batch = std::min<std::size_t>(np, std::size_t(1) << 17);
+    const std::size_t batch = std::min<std::size_t>(std::max<std::size_t>(np, 1), std::size_t(1) << 17);
     std::vector<double> hu(batch * nb), hwu(batch * nb), hv(batch * nb), hwv(batch * nb);
     for (DevBuf* b : {&e.b_gu, &e.b_gwu, &e.b_gv, &e.b_gwv}) b->alloc(std::max<std::size_t>(batch * nb, 1) * sizeof(double));
     B.grid_u = e.b_gu.as<double>();
@@ -756,7 +798,8 @@ void Engine::compute_beta() {
     B.grid_wv = e.b_gwv.as<double>();
     for (std::size_t p0 = 0; p0 < np; p0 += batch) {
         const std::size_t cnt = std::min(batch, np - p0);
-        graded_rules(*e.pairs, p0, p0 + cnt, e.rule_x, e.rule_w, hu.data(), hwu.data(), hv.data(), hwv.data(), 0);
+        graded_rules(*e.pairs, idx.data() + p0, cnt, e.rule_x, e.rule_w, hu.data(), hwu.data(), hv.data(), hwv.data(),
+                     0);
         IFGF_CUDA(cudaStreamSynchronize(e.st));  // previous batch done with the device buffers
         const std::size_t bytes = cnt * nb * sizeof(double);
         IFGF_CUDA(cudaMemcpyAsync(e.b_gu.as<void>(), hu.data(), bytes, cudaMemcpyHostToDevice, e.st));
@@ -777,6 +820,7 @@ void Engine::upload_beta(const std::vector<std::uint64_t>& offset, const cplx* b
     IFGF_CUDA(cudaSetDevice(e.dev));
     if (offset.size() != e.pairs->size() + 1 || offset.back() != e.beta_entries)
         throw InvalidArgument("upload_beta: table layout does not match the pair list");
+    e.alloc_beta(nullptr);
     IFGF_CUDA(cudaMemcpy(e.beta_s.as<void>(), bs, e.beta_entries * sizeof(double2), cudaMemcpyHostToDevice));
     IFGF_CUDA(cudaMemcpy(e.beta_d.as<void>(), bd, e.beta_entries * sizeof(double2), cudaMemcpyHostToDevice));
     e.beta_ready = true;
@@ -787,6 +831,7 @@ void Engine::download_beta(std::vector<std::uint64_t>& offset, std::vector<cplx>
     Impl& e = *d_;
     std::lock_guard<std::mutex> g(e.mu);
     e.ensure_beta();
+    if (e.beta_sharded) throw InvalidArgument("beta tables are target-sharded under a partition (no full tables here)");
     IFGF_CUDA(cudaSetDevice(e.dev));
     offset.resize(e.pairs->size() + 1);
     IFGF_CUDA(cudaMemcpy(offset.data(), e.beta_off.as<void>(), offset.size() * 8, cudaMemcpyDeviceToHost));

@@ -130,9 +130,11 @@ struct BetaDev {
     const double* cutoff = nullptr;            // per patch: max(1e-14, 1e-8 spacing)
     // graded nodes/weights of the current batch (host-computed, glibc pow): batch x n_beta
     const double *grid_u = nullptr, *grid_wu = nullptr, *grid_v = nullptr, *grid_wv = nullptr;
+    // pairs to compute, by position (all pairs, or the owned ones of a target-sharded operator)
+    const std::uint32_t* pidx = nullptr;
 };
 std::size_t beta_smem_bytes(int nb, int TT, int max_dv, int max_nu, int max_nunv);
-// pairs [p_base, p_base + count) of the batch whose graded rules are in B.grid_*
+// pairs B.pidx[p_base .. p_base + count) of the batch whose graded rules are in B.grid_*
 void launch_beta_batch(const BetaDev& B, int p_base, int count, double2* bs, double2* bd, int TT,
                        int max_dv, int max_nu, int max_nunv, cudaStream_t st);
 

@@ -220,6 +220,23 @@ void graded_rules(const PairList& pl, std::size_t p0, std::size_t p1, const std:
     }
 }
 
+void graded_rules(const PairList& pl, const std::uint32_t* idx, std::size_t count, const std::vector<double>& rx,
+                  const std::vector<double>& rw, double* u, double* wu, double* v, double* wv, int workers) {
+    const int nb = int(rx.size());
+    const int d = pl.cfg.cov_d;
+    const int w = worker_count(workers);
+#pragma omp parallel for schedule(static) num_threads(w)
+    for (std::int64_t i = 0; i < std::int64_t(count); ++i) {
+        const std::size_t p = idx[i], o = std::size_t(i) * nb;
+        for (int j = 0; j < nb; ++j) {
+            u[o + j] = grade_xi(pl.ubar[p], rx[j], d);
+            wu[o + j] = grade_xi_deriv(pl.ubar[p], rx[j], d) * rw[j];
+            v[o + j] = grade_xi(pl.vbar[p], rx[j], d);
+            wv[o + j] = grade_xi_deriv(pl.vbar[p], rx[j], d) * rw[j];
+        }
+    }
+}
+
 std::uint64_t beta_key(const Surface& s, const PairList& pl, double k) {
     std::uint64_t h = 14695981039346656037ULL;
     h = fnv(&k, sizeof k, h);

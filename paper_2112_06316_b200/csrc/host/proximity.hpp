@@ -64,6 +64,9 @@ double grade_xi_deriv(double alpha, double tau, int d);
 void graded_rules(const PairList& pl, std::size_t p0, std::size_t p1, const std::vector<double>& rx,
                   const std::vector<double>& rw, double* u, double* wu, double* v, double* wv,
                   int workers);
+// the same for the pairs idx[0 .. count) (output row i = pair idx[i])
+void graded_rules(const PairList& pl, const std::uint32_t* idx, std::size_t count, const std::vector<double>& rx,
+                  const std::vector<double>& rw, double* u, double* wu, double* v, double* wv, int workers);
 
 // FNV-1a fingerprint of everything the beta tables depend on (rp.cpp:291-307), so beta
 // caches written here and by the reference are interchangeable.

@@ -5,7 +5,8 @@ Each rank owns the sources and targets of a cost-balanced, leaf-aligned Morton r
   1. IFGF far field of the owned sources onto ALL targets (leaf fill of owned leaves,
      parent fill and cousin evaluation only for boxes holding owned sources);
   2. grouped ncclReduce of the far-field partials to the owner of each target range;
-  3. near field + RP + combine for the owned targets (every rank holds the full phi);
+  3. near field + RP + combine for the owned targets (every rank holds the full phi; the
+     beta tables hold only the owned targets' pairs);
   4. grouped ncclBroadcast of each owner's outputs, so every rank returns the full out.
 The host plan is built identically on every rank (deterministic), so the partition
 needs no communication; only the 128-byte ncclUniqueId is broadcast.
@@ -48,10 +49,12 @@ class DistributedCombinedOperator(CombinedOperator):
 
         self.rank = dist.get_rank()
         self.world = dist.get_world_size()
-        super().__init__(mesh, cfg)
+        # beta tables sharded by target owner: built after the partition is known
+        super().__init__(mesh, cfg, compute_beta=False)
         uid = broadcast_unique_id(self.rank)
         if self.world > 1:
             self.set_comm(self.rank, self.world, uid)
+        self.compute_beta()
         self.bounds = self.partition(self.world)
 
     @property

@@ -382,6 +382,11 @@ class CombinedOperator:
         d = _cvec(bd)
         check(lib().ifgf_operator_set_beta(self._h, _ptr(off, u64_p), _ptr(s), _ptr(d)), "set_beta")
 
+    def compute_beta(self):
+        """(Re)compute the beta tables on the GPU: all pairs, or after set_partition /
+        set_comm only the owned targets' pairs (target-sharded)."""
+        check(lib().ifgf_operator_compute_beta(self._h), "compute_beta")
+
     def save_beta_cache(self, path: str):
         check(lib().ifgf_operator_save_beta_cache(self._h, path.encode()), "save_beta_cache")
 

@@ -46,3 +46,29 @@ def test_partitioned_apply_equals_full(world):
     assert rel(out, full) <= 1e-13
     op.set_partition(0, n)
     assert np.array_equal(op.apply(phi), full)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_target_sharded_beta(world):
+    # SURVEY.md §8(e) "partition beta by target": each rank's operator holds only the owned
+    # targets' beta tables (built after the partition), and the owned outputs assembled over
+    # ranks still equal the single-GPU apply
+    mesh = P.SurfaceMesh.sphere(1.0, 2, 16, 16)
+    k = 4 * np.pi
+    cfg = P.SolveConfig(k=k, gamma=k)
+    full_op = P.CombinedOperator(mesh, cfg)
+    n = mesh.size()
+    phi = P.random_density(n, 3)
+    full = full_op.apply(phi)
+    nd = mesh.nodes()
+    S, D = full_op.ifgf_apply(phi * nd["jac"] * nd["weight"])
+    bounds = full_op.partition(world)
+    out = np.zeros(n, complex)
+    for r in range(world):
+        op = P.CombinedOperator(mesh, cfg, compute_beta=False)
+        op.set_partition(int(bounds[r]), int(bounds[r + 1]))
+        op.compute_beta()  # owned pairs only
+        out += op.finish_owned(phi, S, D)
+        with pytest.raises(P.InvalidArgument):
+            op.beta()  # no full tables on a sharded operator
+    assert rel(out, full) <= 1e-13

@@ -4,13 +4,13 @@ import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_2112_06316_b200 as P
-from bench import CONFIGS
+from bench import CONFIGS, make_mesh
 
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 applies = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 splits, nu, k, gamma, desc = CONFIGS[name]
 t = time.perf_counter()
-mesh = P.SurfaceMesh.sphere(1.0, splits, nu, nu)
+mesh = make_mesh(name, P)
 op = P.CombinedOperator(mesh, P.SolveConfig(k=k, gamma=gamma))
 print(f"setup {time.perf_counter() - t:.1f}s N={mesh.size()}", flush=True)
 op.upload_density(P.random_density(mesh.size(), 1))

@@ -2,12 +2,12 @@
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2112_06316_b200 as P
-from bench import CONFIGS
+from bench import CONFIGS, make_mesh
 
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 splits, nu, k, gamma, desc = CONFIGS[name]
 t = time.perf_counter()
-mesh = P.SurfaceMesh.sphere(1.0, splits, nu, nu)
+mesh = make_mesh(name, P)
 t1 = time.perf_counter()
 op = P.CombinedOperator(mesh, P.SolveConfig(k=k, gamma=gamma))
 t2 = time.perf_counter()
