@@ -46,12 +46,13 @@ beta_kernel(BetaDev B, int TT, int max_dv, int max_nu, int max_nunv, int p_base,
     double* vs = us + nb;
     double* wu = vs + nb;
     double* wv = wu + nb;
-    double* Tu = wv + nb;                 // nb x TT, T_i(clamp(u_iu))
-    double* Tv = Tu + nb * TT;            // nb x TT
+    const int tts = TT | 1;               // odd row stride: rows read across lanes by node
+    double* Tu = wv + nb;                 // nb x tts, T_i(clamp(u_iu))
+    double* Tv = Tu + nb * tts;           // nb x tts
     // 9 x nb x (max_dv | 1): u-contracted series; odd row stride, the geometry step reads it
     // across lanes by u node
     const int pst = max_dv | 1;
-    double* Pu = Tv + nb * TT;
+    double* Pu = Tv + nb * tts;
     double2* fS = reinterpret_cast<double2*>(Pu + ((9 * nb * pst + 1) & ~1));  // kJV x nb, 16-byte aligned
     double2* fD = fS + nb * kJV;
     double2* rS = fD + nb * kJV;          // kJV x max_nu
@@ -73,8 +74,8 @@ beta_kernel(BetaDev B, int TT, int max_dv, int max_nu, int max_nunv, int p_base,
     const int tmax = max(max(du, nu), max(dv, nv));
     for (int i = threadIdx.x; i < nb; i += blockDim.x) {
         const double u = fmin(fmax(us[i], -1.0), 1.0), v = fmin(fmax(vs[i], -1.0), 1.0);
-        double* tu = Tu + i * TT;
-        double* tv = Tv + i * TT;
+        double* tu = Tu + i * tts;
+        double* tv = Tv + i * tts;
         tu[0] = 1.0;
         tv[0] = 1.0;
         if (tmax > 1) {
@@ -92,10 +93,10 @@ beta_kernel(BetaDev B, int TT, int max_dv, int max_nu, int max_nunv, int p_base,
     }
     __syncthreads();
     // partial[s][iu][j] = sum_i series_s[i + du j] T_i(u_iu)   (eval_series_grid, rp.cpp:57-66)
-    for (int e = threadIdx.x; e < 9 * nb * dv; e += blockDim.x) {
-        const int j = e % dv, rest = e / dv, iu = rest % nb, s = rest / nb;
+    for (int e = threadIdx.x; e < 9 * nb * dv; e += blockDim.x) {  // lanes run over u nodes
+        const int iu = e % nb, rest = e / nb, j = rest % dv, s = rest / dv;
         const double* col = ser + std::size_t(s) * du * dv + std::size_t(du) * j;
-        const double* t = Tu + iu * TT;
+        const double* t = Tu + iu * tts;
         double acc = 0.0;
         for (int i = 0; i < du; ++i) acc += col[i] * t[i];
         Pu[(s * nb + iu) * pst + j] = acc;
@@ -107,7 +108,7 @@ beta_kernel(BetaDev B, int TT, int max_dv, int max_nu, int max_nunv, int p_base,
         // geometry + kernels at the slab's nodes (rp.cpp:67-75, 100-107, 366-379)
         for (int e = threadIdx.x; e < nb * jn; e += blockDim.x) {
             const int iu = e % nb, jj = e / nb;
-            const double* t = Tv + (j0 + jj) * TT;
+            const double* t = Tv + (j0 + jj) * tts;
             double g[9];
 #pragma unroll
             for (int s = 0; s < 9; ++s) {
@@ -151,7 +152,7 @@ beta_kernel(BetaDev B, int TT, int max_dv, int max_nu, int max_nunv, int p_base,
             const double2* f = (tab == 0 ? fS : fD) + jj * nb;
             double ax = 0.0, ay = 0.0;
             for (int iu = 0; iu < nb; ++iu) {
-                const double tn = Tu[iu * TT + n];
+                const double tn = Tu[iu * tts + n];
                 ax += f[iu].x * tn;
                 ay += f[iu].y * tn;
             }
@@ -163,7 +164,7 @@ beta_kernel(BetaDev B, int TT, int max_dv, int max_nu, int max_nunv, int p_base,
             const int n = e % nu, m = e / nu;
             double2 s = aS[e], d = aD[e];
             for (int jj = 0; jj < jn; ++jj) {
-                const double t = Tv[(j0 + jj) * TT + m];
+                const double t = Tv[(j0 + jj) * tts + m];
                 const double2 a = rS[jj * max_nu + n], b = rD[jj * max_nu + n];
                 s.x += a.x * t;
                 s.y += a.y * t;
@@ -185,7 +186,7 @@ beta_kernel(BetaDev B, int TT, int max_dv, int max_nu, int max_nunv, int p_base,
 }  // namespace
 
 std::size_t beta_smem_bytes(int nb, int TT, int max_dv, int max_nu, int max_nunv) {
-    return sizeof(double) * (4 * std::size_t(nb) + 2 * std::size_t(nb) * TT + ((9 * std::size_t(nb) * (max_dv | 1) + 1) & ~std::size_t(1))) +
+    return sizeof(double) * (4 * std::size_t(nb) + 2 * std::size_t(nb) * (TT | 1) + ((9 * std::size_t(nb) * (max_dv | 1) + 1) & ~std::size_t(1))) +
            sizeof(double2) * (2 * std::size_t(nb) * kJV + 2 * std::size_t(kJV) * max_nu + 2 * std::size_t(max_nunv));
 }
 
