@@ -25,3 +25,20 @@ def test_eps_metric_semantics():
     assert skipped == 1 and abs(eps - 0.1) < 1e-15
     with pytest.raises(P.InvalidArgument):
         P.eps_near(np.array([1.0]), np.array([1.0, 2.0]))
+
+
+def test_incident_trace_kinds():
+    # incident_at (solver.cpp:25-35): plane wave along (cos t sin p, sin t sin p, cos p) and
+    # the point-source sum of e^{ikr}/r; a source on a node is InvalidArgument
+    mesh = P.SurfaceMesh.sphere(1.0, 1, 6, 6)
+    pos = mesh.nodes()["pos"]
+    k = 3.0
+    inc = P.IncidentField(theta=0.3, phi=2.0)
+    d = inc.wave_direction()
+    assert np.allclose(P.incident_trace(inc, mesh, k), np.exp(1j * k * pos @ d), rtol=0, atol=1e-14)
+    src = np.array([[0.1, 0.2, -0.1], [0.0, -0.3, 0.2]])
+    r = np.linalg.norm(pos[:, None, :] - src[None], axis=2)
+    want = (np.exp(1j * k * r) / r).sum(axis=1)
+    assert np.allclose(P.incident_trace(P.IncidentField(sources=src), mesh, k), want, rtol=1e-14, atol=0)
+    with pytest.raises(P.InvalidArgument):
+        P.incident_trace(P.IncidentField(sources=pos[:1]), mesh, k)
