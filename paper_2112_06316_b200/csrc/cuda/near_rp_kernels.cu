@@ -58,16 +58,15 @@ __device__ __forceinline__ void pair_kernels(double x, double y, double z, doubl
     double sn, cs;
     sincos_bounded(k * r, &sn, &cs);
     const double g = kInv4PiD * inv;
-    const double2 ga = cmul(make_double2(cs * g, sn * g), a);
+    const double2 ga = cmul(make_double2(cs * g, sn * g), a);  // G a = e^{ikr} a / (4 pi r)
     accS.x = fma(sg, ga.x, accS.x);
     accS.y = fma(sg, ga.y, accS.y);
+    // dG/dnu_y a = (1 - ikr) G a <x - y, nu> / r^2
     const double dn = fma(dx, nx, fma(dy, ny, dz * nz));
     const double kr = k * r;
-    const double f = dn * kInv4PiD * inv * inv * inv;
-    const double2 e = make_double2(fma(kr, sn, cs) * f, fma(-kr, cs, sn) * f);  // e^{ikr}(1-ikr) f
-    const double2 da = cmul(e, a);
-    accD.x = fma(sg, da.x, accD.x);
-    accD.y = fma(sg, da.y, accD.y);
+    const double f = sg * dn * (inv * inv);
+    accD.x = fma(fma(kr, ga.y, ga.x), f, accD.x);
+    accD.y = fma(fma(-kr, ga.x, ga.y), f, accD.y);
 }
 
 __global__ void __launch_bounds__(kNearThreads, 8)
