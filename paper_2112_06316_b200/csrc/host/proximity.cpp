@@ -191,6 +191,9 @@ PairList classify_pairs(const Surface& s, const BoxTree& t, const BoxRelations& 
             out.patch.push_back(f.q);
             out.ubar.push_back(f.u);
             out.vbar.push_back(f.v);
+            if (out.far_nodes.size() + f.far.size() > std::size_t(0xffffffffu) ||
+                out.target.size() >= std::size_t(0xffffffffu))
+                throw InternalError("classify_targets: more than 2^32 far-node entries or pairs (32-bit offsets)");
             out.far_begin.push_back(std::uint32_t(out.far_nodes.size()));
             out.far_nodes.insert(out.far_nodes.end(), f.far.begin(), f.far.end());
             out.far_end.push_back(std::uint32_t(out.far_nodes.size()));
