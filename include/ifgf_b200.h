@@ -57,6 +57,8 @@ typedef struct {
     int32_t n_beta, cov_d;          /* 96, 6 */
     int32_t workers;          /* host setup threads, <= 0: all */
     int32_t device;           /* CUDA device ordinal */
+    int32_t part_rank, part_world;  /* per-rank plan of a multi-GPU run (0, 1: the full plan):
+                                       only boxes with sources of rank part_rank's Morton range */
 } ifgf_config;
 
 const char* ifgf_last_error(void);

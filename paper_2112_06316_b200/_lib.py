@@ -36,6 +36,8 @@ class IfgfConfig(C.Structure):
         ("cov_d", C.c_int32),
         ("workers", C.c_int32),
         ("device", C.c_int32),
+        ("part_rank", C.c_int32),
+        ("part_world", C.c_int32),
     ]
 
 

@@ -131,7 +131,17 @@ std::shared_ptr<ifgf_plan> make_plan(std::shared_ptr<const Surface> s, const ifg
                                       std::vector<std::int64_t>& fc, std::vector<std::int64_t>& fp) {
         gpu_cone_decisions(job, L, marks, fc, fp, dev);
     };
-    p->cones = build_cone_plan(p->tree, p->rel, pts, cp, c.workers, gpu ? &decider : nullptr);
+    if (c.part_world > 1) {  // per-rank plan: partition first (plan-free cost model), then prune
+        if (c.part_rank < 0 || c.part_rank >= c.part_world) throw InvalidArgument("plan: bad part_rank / part_world");
+        const auto bounds = partition_sources_light(p->tree, p->rel, c.part_world);
+        const auto act = active_boxes(p->tree, bounds[c.part_rank], bounds[c.part_rank + 1]);
+        p->cones = build_cone_plan(p->tree, p->rel, pts, cp, c.workers, gpu ? &decider : nullptr, &act);
+        p->cones.rank = c.part_rank;
+        p->cones.world = c.part_world;
+        p->cones.bounds = bounds;
+    } else {
+        p->cones = build_cone_plan(p->tree, p->rel, pts, cp, c.workers, gpu ? &decider : nullptr);
+    }
     p->t_cones = lap();
     RpParams rp;
     rp.delta_rel = c.delta_rel;
@@ -140,7 +150,14 @@ std::shared_ptr<ifgf_plan> make_plan(std::shared_ptr<const Surface> s, const ifg
     rp.cov_d = c.cov_d;
     const ClosestPointBatch batch = [dev](const Surface& sf, const std::vector<ClosestPointRequest>& rq,
                                           std::vector<ClosestPoint>& out) { gpu_closest_points(sf, rq, out, dev); };
-    p->pairs = classify_pairs(*s, p->tree, p->rel, rp, c.workers, gpu ? &batch : nullptr);
+    std::vector<std::uint8_t> owned;  // per-rank plan: pairs of the owned targets only
+    if (p->cones.world > 1) {
+        owned.assign(s->size(), 0);
+        for (std::uint32_t m = p->cones.bounds[p->cones.rank]; m < p->cones.bounds[p->cones.rank + 1]; ++m)
+            owned[p->tree.perm[m]] = 1;
+    }
+    p->pairs = classify_pairs(*s, p->tree, p->rel, rp, c.workers, gpu ? &batch : nullptr,
+                              owned.empty() ? nullptr : &owned);
     p->t_pairs = lap();
     p->strategy = c.strategy == 0 ? DlStrategy::W4 : (c.strategy == 1 ? DlStrategy::W2W3 : DlStrategy::Hybrid);
     if (p->strategy == DlStrategy::Hybrid) {  // solver.cpp:55-62
@@ -203,6 +220,8 @@ void ifgf_config_default(ifgf_config* c) {
     c->cov_d = 6;
     c->workers = 0;
     c->device = 0;
+    c->part_rank = 0;
+    c->part_world = 1;
 }
 
 // ------------------------------------------------------------------ surfaces
@@ -918,7 +937,9 @@ int ifgf_plan_partition(const ifgf_plan* p, int parts, uint32_t* bounds) {
     return guarded([&] {
         need(p, "plan");
         need(bounds, "bounds");
-        const auto b = partition_sources(p->tree, p->rel, p->cones, parts);
+        const auto b = p->cones.world > 1 ? p->cones.bounds : partition_sources(p->tree, p->rel, p->cones, parts);
+        if (p->cones.world > 1 && parts != p->cones.world)
+            throw InvalidArgument("partition: a per-rank plan is partitioned " + std::to_string(p->cones.world) + " ways");
         std::memcpy(bounds, b.data(), b.size() * sizeof(uint32_t));
     });
 }

@@ -285,7 +285,13 @@ struct Engine::Impl {
         drop_graph();
     }
 
-    std::vector<std::uint32_t> partition(int parts) const { return partition_sources(*tree, *rel, *cones, parts); }
+    std::vector<std::uint32_t> partition(int parts) const {
+        if (cones->world > 1) {  // a per-rank plan carries its partition
+            if (parts != cones->world) throw InvalidArgument("partition: the plan is per rank of a different world");
+            return cones->bounds;
+        }
+        return partition_sources(*tree, *rel, *cones, parts);
+    }
 
     void reduce_far_to_owners() {
         IFGF_NCCL(ncclGroupStart());
@@ -433,14 +439,14 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         }
         std::vector<std::int32_t> chunk_box, chunk_q0;
         for (std::size_t i = 0; i < nb; ++i)
-            if (R.cousin[d - 1].count(i) > 0)
+            if (CL.cz.count(i) > 0)
                 for (std::uint32_t q = 0; q < B.end[i] - B.begin[i]; q += kChunk) {
                     chunk_box.push_back(std::int32_t(i));
                     chunk_q0.push_back(std::int32_t(q));
                 }
         std::vector<std::int32_t> wchunk_box, wchunk_q0;  // one warp per 32 targets
         for (std::size_t i = 0; i < nb; ++i)
-            if (R.cousin[d - 1].count(i) > 0)
+            if (CL.cz.count(i) > 0)
                 for (std::uint32_t q = 0; q < B.end[i] - B.begin[i]; q += 32) {
                     wchunk_box.push_back(std::int32_t(i));
                     wchunk_q0.push_back(std::int32_t(q));
@@ -455,8 +461,8 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         b.cz.upload(cz);
         b.beg.upload(B.begin);
         b.end.upload(B.end);
-        b.cz_ptr.upload(R.cousin[d - 1].ptr);
-        b.cz_idx.upload(R.cousin[d - 1].idx);
+        b.cz_ptr.upload(CL.cz.ptr);  // the plan's cousin lists (pruned in a per-rank plan)
+        b.cz_idx.upload(CL.cz.idx);
         b.cev_begin.upload(CL.cev_begin);
         b.cev_seg.upload(CL.cev_seg);
         b.seg_box.upload(CL.seg_box);

@@ -192,7 +192,7 @@ std::vector<int> dl_pipes(const BoxTree& t, int level, DlStrategy s) {
 
 ConePlanHost build_cone_plan(const BoxTree& t, const BoxRelations& rel,
                              const std::vector<Vec3>& pts, const ConeParams& p, int workers,
-                             const ConeDecider* decider) {
+                             const ConeDecider* decider, const std::vector<std::vector<std::uint8_t>>* active) {
     if (p.ps < 1 || p.ps > kMaxOrder || p.pang < 1 || p.pang > kMaxOrder)
         throw InvalidArgument("plan_cones: interpolation orders must lie in [1,12]");
     if (p.n_s0 < 1 || p.n_c0 < 1) throw InvalidArgument("plan_cones: interval counts must be positive");
@@ -212,7 +212,7 @@ ConePlanHost build_cone_plan(const BoxTree& t, const BoxRelations& rel,
         cp.assign(B.size() + 1, 0);
         for (std::size_t b = 0; b < B.size(); ++b) {
             for (std::int32_t ch : B.child[b])
-                if (ch >= 0) ci.push_back(ch);
+                if (ch >= 0 && (!active || d >= D || (*active)[d][ch])) ci.push_back(ch);
             cp[b + 1] = std::int32_t(ci.size());
         }
     }
@@ -233,7 +233,21 @@ ConePlanHost build_cone_plan(const BoxTree& t, const BoxRelations& rel,
         std::vector<std::uint8_t> marks(nb * spb, 0);
 
         // (1) cousin target points, evaluated in the frame of each cousin source box
-        const Adjacency& cz = rel.cousin[d - 1];
+        // cousin pairs evaluated by this plan (all, or those whose source box is active)
+        if (!active) {
+            L.cz = rel.cousin[d - 1];
+        } else {
+            const Adjacency& full = rel.cousin[d - 1];
+            const auto& act = (*active)[d - 1];
+            L.cz.ptr.assign(nb + 1, 0);
+            L.cz.idx.clear();
+            for (std::size_t b = 0; b < nb; ++b) {
+                for (std::int32_t j = full.ptr[b]; j < full.ptr[b + 1]; ++j)
+                    if (act[full.idx[j]]) L.cz.idx.push_back(full.idx[j]);
+                L.cz.ptr[b + 1] = std::int32_t(L.cz.idx.size());
+            }
+        }
+        const Adjacency& cz = L.cz;
         L.cev_begin.assign(nb + 1, 0);
         for (std::size_t b = 0; b < nb; ++b)
             L.cev_begin[b + 1] = L.cev_begin[b] + std::int64_t(cz.count(b)) * (B.end[b] - B.begin[b]);
@@ -444,6 +458,46 @@ void parent_templates(const BoxTree& t, const ConePlanHost& plan, int d, const s
                     }
         }
     });
+}
+
+std::vector<std::vector<std::uint8_t>> active_boxes(const BoxTree& t, std::uint32_t lo, std::uint32_t hi) {
+    std::vector<std::vector<std::uint8_t>> a(t.depth);
+    for (int d = 1; d <= t.depth; ++d) {
+        const BoxLevel& B = t.level[d - 1];
+        a[d - 1].resize(B.size());
+        for (std::size_t b = 0; b < B.size(); ++b) a[d - 1][b] = (B.begin[b] < hi && B.end[b] > lo) ? 1 : 0;
+    }
+    return a;
+}
+
+std::vector<std::uint32_t> partition_sources_light(const BoxTree& t, const BoxRelations& rel, int parts) {
+    if (parts < 1) throw InvalidArgument("partition: need at least one part");
+    const std::size_t n = t.perm.size();
+    const int D = t.depth;
+    const BoxLevel& leaves = t.level[D - 1];
+    const Adjacency& nbr = rel.nbr[D - 1];
+    const Adjacency& cz = rel.cousin[D - 1];
+    std::vector<double> cost(leaves.size(), 0.0);
+    for (std::size_t b = 0; b < leaves.size(); ++b) {
+        const double np = double(leaves.end[b] - leaves.begin[b]);
+        double nn = 0, ce = 0;
+        for (int j = nbr.ptr[b]; j < nbr.ptr[b + 1]; ++j) nn += leaves.end[nbr.idx[j]] - leaves.begin[nbr.idx[j]];
+        for (int j = cz.ptr[b]; j < cz.ptr[b + 1]; ++j) ce += leaves.end[cz.idx[j]] - leaves.begin[cz.idx[j]];
+        // near pairs, leaf fill over ~40 relevant segments x 75 nodes, cousin evaluations
+        cost[b] = 47.0 * np * nn + 47.0 * 75.0 * 40.0 * np + 1358.0 * ce;
+    }
+    double total = 0;
+    for (double c : cost) total += c;
+    std::vector<std::uint32_t> out(parts + 1, 0);
+    double acc = 0;
+    int r = 1;
+    for (std::size_t b = 0; b < leaves.size() && r < parts; ++b) {
+        acc += cost[b];
+        while (r < parts && acc >= total * r / parts) out[r++] = leaves.end[b];
+    }
+    for (; r < parts; ++r) out[r] = std::uint32_t(n);
+    out[parts] = std::uint32_t(n);
+    return out;
 }
 
 // cost-balanced leaf-aligned boundaries: per leaf box, near pairs + leaf-fill

@@ -33,6 +33,9 @@ struct ConeLevel {
 
     std::vector<std::int32_t> seg_box, seg_gamma;  // relevant segments, (box, gamma) order
     std::vector<std::int32_t> box_seg_begin;       // nboxes + 1
+    // cousin lists the plan evaluates (BoxRelations::cousin, restricted to source boxes with
+    // owned sources in a per-rank plan)
+    Adjacency cz;
 
     // cousin evaluations, target-box major: for box tb, cousin j (ascending cousin list),
     // point t of tb -> segment ordinal of the cousin box at this level
@@ -63,6 +66,10 @@ struct ConePlanHost {
     std::vector<ConeLevel> level;  // level[d-1], valid for 3 <= d <= depth
     // per leaf/coarse level: children lists compacted in slot order (nch <= 8)
     std::vector<std::vector<std::int32_t>> child_ptr, child_idx;  // [d-1] over boxes of level d
+    // per-rank plan (multi-GPU): only boxes holding sources of the Morton range
+    // [bounds[rank], bounds[rank + 1]) carry segments; world == 1: the full plan
+    int rank = 0, world = 1;
+    std::vector<std::uint32_t> bounds;
 };
 
 int cone_doublings(double side, double lambda);  // ifgf.cpp:18-25
@@ -91,9 +98,17 @@ struct ConeDecisionJob {
 using ConeDecider = std::function<void(const ConeDecisionJob& job, ConeLevel& L, std::vector<std::uint8_t>& marks,
                                        std::vector<std::int64_t>& flagged_cev, std::vector<std::int64_t>& flagged_pev)>;
 
+// active: per level [d-1], per box, 1 if the box holds sources this plan covers (null = all)
 ConePlanHost build_cone_plan(const BoxTree& t, const BoxRelations& rel,
                              const std::vector<Vec3>& pts_morton, const ConeParams& p,
-                             int workers, const ConeDecider* decider = nullptr);
+                             int workers, const ConeDecider* decider = nullptr,
+                             const std::vector<std::vector<std::uint8_t>>* active = nullptr);
+
+// leaf-aligned Morton boundaries from a plan-free cost model (points, neighbour and cousin
+// point counts per leaf), for building per-rank plans before any cone plan exists
+std::vector<std::uint32_t> partition_sources_light(const BoxTree& t, const BoxRelations& rel, int parts);
+// per level, per box: 1 if the box holds sources of the Morton range [lo, hi)
+std::vector<std::vector<std::uint8_t>> active_boxes(const BoxTree& t, std::uint32_t lo, std::uint32_t hi);
 
 // Parent-fill geometry templates (device data, not decisions). The position of a parent
 // interpolation node relative to a child box depends only on the parent cone cell, the

@@ -79,7 +79,8 @@ double grade_xi_deriv(double alpha, double tau, int d) {
 }
 
 PairList classify_pairs(const Surface& s, const BoxTree& t, const BoxRelations& rel,
-                        const RpParams& cfg, int workers, const ClosestPointBatch* batch) {
+                        const RpParams& cfg, int workers, const ClosestPointBatch* batch,
+                        const std::vector<std::uint8_t>* owned) {
     if (cfg.n_beta < 2 || cfg.cov_d < 2)
         throw InvalidArgument("classify_targets: n_beta >= 2 and cov_d >= 2 required");
     const std::size_t n = s.size();
@@ -115,6 +116,7 @@ PairList classify_pairs(const Surface& s, const BoxTree& t, const BoxRelations& 
     std::vector<std::vector<ClosestPointRequest>> req(n);
 #pragma omp parallel for schedule(dynamic, 64) num_threads(w)
     for (std::int64_t l = 0; l < std::int64_t(n); ++l) {
+        if (owned && !(*owned)[l]) continue;  // another rank's target
         const std::int32_t tb = t.leaf_of[l];
         const auto nb0 = nbr.idx.begin() + nbr.ptr[tb], nb1 = nbr.idx.begin() + nbr.ptr[tb + 1];
         std::vector<std::int32_t> cand;

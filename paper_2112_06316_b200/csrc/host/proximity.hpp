@@ -50,8 +50,10 @@ struct ClosestPointRequest {
 using ClosestPointBatch = std::function<void(const Surface&, const std::vector<ClosestPointRequest>&,
                                              std::vector<ClosestPoint>&)>;
 
+// owned (per original node, optional): only those targets get pairs (per-rank plans)
 PairList classify_pairs(const Surface& s, const BoxTree& t, const BoxRelations& rel,
-                        const RpParams& cfg, int workers, const ClosestPointBatch* batch = nullptr);
+                        const RpParams& cfg, int workers, const ClosestPointBatch* batch = nullptr,
+                        const std::vector<std::uint8_t>* owned = nullptr);
 
 // graded change of variables (rp.cpp:139-192)
 double grade_w(double tau, int d);

@@ -8,12 +8,14 @@ Each rank owns the sources and targets of a cost-balanced, leaf-aligned Morton r
   3. near field + RP + combine for the owned targets (every rank holds the full phi; the
      beta tables hold only the owned targets' pairs);
   4. grouped ncclBroadcast of each owner's outputs, so every rank returns the full out.
-The host plan is built identically on every rank (deterministic), so the partition
-needs no communication; only the 128-byte ncclUniqueId is broadcast.
+Each rank partitions with the same deterministic, plan-free cost model and then builds
+only its share of the cone plan, so the partition needs no communication; only the
+128-byte ncclUniqueId is broadcast.
 """
 from __future__ import annotations
 
 import ctypes as C
+import dataclasses
 
 import numpy as np
 
@@ -49,7 +51,10 @@ class DistributedCombinedOperator(CombinedOperator):
 
         self.rank = dist.get_rank()
         self.world = dist.get_world_size()
-        # beta tables sharded by target owner: built after the partition is known
+        # per-rank plan (only boxes holding this rank's sources) and beta tables sharded by
+        # target owner, built once the partition is set
+        if self.world > 1:
+            cfg = dataclasses.replace(cfg, part_rank=self.rank, part_world=self.world)
         super().__init__(mesh, cfg, compute_beta=False)
         uid = broadcast_unique_id(self.rank)
         if self.world > 1:

@@ -59,6 +59,9 @@ class SolveConfig:  # solver.hpp:32-45 (+ device)
     rp: RpConfig = field(default_factory=RpConfig)
     workers: int = 0
     device: int = 0
+    # per-rank plan of a multi-GPU run: only boxes with sources of this rank's Morton range
+    part_rank: int = 0
+    part_world: int = 1
 
     def to_c(self) -> IfgfConfig:
         c = IfgfConfig()
@@ -72,6 +75,8 @@ class SolveConfig:  # solver.hpp:32-45 (+ device)
         c.n_beta, c.cov_d = self.rp.n_beta, self.rp.cov_d
         c.workers = self.workers
         c.device = self.device
+        c.part_rank = self.part_rank
+        c.part_world = self.part_world
         return c
 
 

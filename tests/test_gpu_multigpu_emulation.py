@@ -72,3 +72,48 @@ def test_target_sharded_beta(world):
         with pytest.raises(P.InvalidArgument):
             op.beta()  # no full tables on a sharded operator
     assert rel(out, full) <= 1e-13
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_per_rank_plans(world):
+    # per-rank plans (SolveConfig.part_rank / part_world): each holds only the boxes with its
+    # sources; the ranks' far fields sum to the full far field and the owned outputs
+    # assemble the single-GPU apply
+    mesh = P.SurfaceMesh.sphere(1.0, 2, 16, 16)
+    k = 4 * np.pi
+    full_op = P.CombinedOperator(mesh, P.SolveConfig(k=k, gamma=k))
+    n = mesh.size()
+    phi = P.random_density(n, 5)
+    full = full_op.apply(phi)
+    nd = mesh.nodes()
+    a = phi * nd["jac"] * nd["weight"]
+    S_full, D_full = full_op.ifgf_apply(a)
+    S = np.zeros(n, complex)
+    D = np.zeros(n, complex)
+    out = np.zeros(n, complex)
+    segs = 0
+    full_plan = P.HostPlan(mesh, P.SolveConfig(k=k, gamma=k))
+    for r in range(world):
+        cfg = P.SolveConfig(k=k, gamma=k, part_rank=r, part_world=world)
+        plan = P.HostPlan(mesh, cfg)
+        segs += sum(len(plan.level_cones(d)["seg_box"]) for d in range(3, plan.depth + 1))
+        op = P.CombinedOperator(mesh, cfg, plan=plan, compute_beta=False)
+        bounds = op.partition(world)
+        op.set_partition(int(bounds[r]), int(bounds[r + 1]))
+        op.compute_beta()
+        s, d = op.ifgf_apply(a)
+        S += s
+        D += d
+    assert rel(S, S_full) <= 1e-13 and rel(D, D_full) <= 1e-13
+    # pruning: the ranks together hold about one plan's worth of segments, not world plans
+    full_segs = sum(len(full_plan.level_cones(d)["seg_box"]) for d in range(3, full_plan.depth + 1))
+    assert segs < 1.6 * full_segs
+    # owned outputs from the per-rank operators
+    for r in range(world):
+        cfg = P.SolveConfig(k=k, gamma=k, part_rank=r, part_world=world)
+        op = P.CombinedOperator(mesh, cfg, compute_beta=False)
+        bounds = op.partition(world)
+        op.set_partition(int(bounds[r]), int(bounds[r + 1]))
+        op.compute_beta()
+        out += op.finish_owned(phi, S_full, D_full)
+    assert rel(out, full) <= 1e-13
