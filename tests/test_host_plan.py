@@ -107,3 +107,31 @@ def test_diagnostics_text():
     assert "level 4: boxes=272 segments=9424 interp_points=706800 ns=2 nc=4" in txt
     assert "level 3: boxes=56 segments=4432" in txt
     assert hp.evaluations(4, 0) == 1071192 and hp.evaluations(4, 1) == 1646400
+
+
+def test_per_rank_plans_partition_the_full_plan():
+    # a per-rank plan keeps exactly the full plan's relevant segments of the boxes holding its
+    # sources (same evaluations reach them), so the ranks' segment sets cover the full plan
+    pm = P.SurfaceMesh.sphere(1.0, 2, 10, 10)
+    k = 8 * np.pi
+    full = P.HostPlan(pm, P.SolveConfig(k=k, device=-1))
+    world = 3
+    parts = [P.HostPlan(pm, P.SolveConfig(k=k, device=-1, part_rank=r, part_world=world)) for r in range(world)]
+    for d in range(3, full.depth + 1):
+        F = full.level_cones(d)
+        fset = set(zip(F["seg_box"].tolist(), F["seg_gamma"].tolist()))
+        union = set()
+        for hp in parts:
+            A = hp.level_cones(d)
+            aset = set(zip(A["seg_box"].tolist(), A["seg_gamma"].tolist()))
+            assert aset <= fset, d
+            union |= aset
+        assert union == fset, d
+    # the plan-free partition is leaf aligned, covers all points and is the same on every rank
+    n = pm.size()
+    from paper_2112_06316_b200.distributed import plan_partition
+    bounds = [plan_partition(hp, world) for hp in parts]
+    assert all(np.array_equal(bounds[0], x) for x in bounds)
+    assert bounds[0][0] == 0 and bounds[0][-1] == n
+    with pytest.raises(P.InvalidArgument):
+        plan_partition(parts[0], world + 1)
