@@ -27,7 +27,7 @@ constexpr int kJV = 8;
 
 __global__ void __launch_bounds__(kBetaThreads)
 beta_kernel(BetaDev B, int TT, int max_dv, int max_nu, int max_nunv, int p_base,
-            double2* __restrict__ bs_out, double2* __restrict__ bd_out) {
+            double2* __restrict__ bs_out, double2* __restrict__ bd_out, double* __restrict__ gPu) {
     extern __shared__ double sm[];
     const int pl = blockIdx.x;            // pair within the batch
     const int p = int(B.pidx[p_base + pl]);  // global pair
@@ -51,9 +51,12 @@ beta_kernel(BetaDev B, int TT, int max_dv, int max_nu, int max_nunv, int p_base,
     double* Tv = Tu + nb * tts;           // nb x tts
     // 9 x nb x (max_dv | 1): u-contracted series; odd row stride, the geometry step reads it
     // across lanes by u node
+    // (in global scratch, gPu, when the patch series are too long for shared memory)
     const int pst = max_dv | 1;
-    double* Pu = Tv + nb * tts;
-    double2* fS = reinterpret_cast<double2*>(Pu + ((9 * nb * pst + 1) & ~1));  // kJV x nb, 16-byte aligned
+    double* const after_T = Tv + nb * tts;
+    double* Pu = gPu ? gPu + std::size_t(blockIdx.x) * 9 * nb * pst : after_T;
+    // (the head, 4 nb + 2 nb tts doubles, is even: fS stays 16-byte aligned)
+    double2* fS = reinterpret_cast<double2*>(after_T + (gPu ? 0 : ((9 * nb * pst + 1) & ~1)));
     double2* fD = fS + nb * kJV;
     double2* rS = fD + nb * kJV;          // kJV x max_nu
     double2* rD = rS + kJV * max_nu;
@@ -185,21 +188,53 @@ beta_kernel(BetaDev B, int TT, int max_dv, int max_nu, int max_nunv, int p_base,
 
 }  // namespace
 
-std::size_t beta_smem_bytes(int nb, int TT, int max_dv, int max_nu, int max_nunv) {
-    return sizeof(double) * (4 * std::size_t(nb) + 2 * std::size_t(nb) * (TT | 1) + ((9 * std::size_t(nb) * (max_dv | 1) + 1) & ~std::size_t(1))) +
+namespace {
+std::size_t beta_smem(int nb, int TT, int max_dv, int max_nu, int max_nunv, bool pu_shared) {
+    const std::size_t head = 4 * std::size_t(nb) + 2 * std::size_t(nb) * (TT | 1);
+    const std::size_t pu = pu_shared ? ((9 * std::size_t(nb) * (max_dv | 1) + 1) & ~std::size_t(1)) : 0;
+    return sizeof(double) * (head + pu) +
            sizeof(double2) * (2 * std::size_t(nb) * kJV + 2 * std::size_t(kJV) * max_nu + 2 * std::size_t(max_nunv));
+}
+}  // namespace
+
+std::size_t beta_smem_bytes(int nb, int TT, int max_dv, int max_nu, int max_nunv) {
+    return beta_smem(nb, TT, max_dv, max_nu, max_nunv, true);
 }
 
 void launch_beta_batch(const BetaDev& B, int p_base, int count, double2* bs, double2* bd, int TT, int max_dv,
                        int max_nu, int max_nunv, cudaStream_t st) {
     if (count == 0) return;
-    const std::size_t smem = beta_smem_bytes(B.n_beta, TT, max_dv, max_nu, max_nunv);
-    if (smem > 227 * 1024)
+    constexpr std::size_t kSmemMax = 227 * 1024;
+    const std::size_t smem = beta_smem(B.n_beta, TT, max_dv, max_nu, max_nunv, true);
+    if (smem <= kSmemMax) {
+        IFGF_CUDA(cudaFuncSetAttribute(beta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        beta_kernel<<<count, kBetaThreads, smem, st>>>(B, TT, max_dv, max_nu, max_nunv, p_base, bs, bd, nullptr);
+        IFGF_CUDA(cudaGetLastError());
+        return;
+    }
+    // long patch series (few large patches): the u-contracted series live in a global scratch
+    // buffer, pairs in sub-batches that bound it (~256 MB)
+    const std::size_t smem2 = beta_smem(B.n_beta, TT, max_dv, max_nu, max_nunv, false);
+    if (smem2 > kSmemMax)
         throw InvalidArgument("beta tables: graded rule too large for shared memory (n_beta=" +
                               std::to_string(B.n_beta) + ")");
-    IFGF_CUDA(cudaFuncSetAttribute(beta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    beta_kernel<<<count, kBetaThreads, smem, st>>>(B, TT, max_dv, max_nu, max_nunv, p_base, bs, bd);
-    IFGF_CUDA(cudaGetLastError());
+    const std::size_t per_pair = 9 * std::size_t(B.n_beta) * std::size_t(max_dv | 1) * sizeof(double);
+    const int sub = int(std::max<std::size_t>(1, std::min<std::size_t>(std::size_t(count), (std::size_t(256) << 20) / per_pair)));
+    double* scratch = nullptr;
+    IFGF_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), std::size_t(sub) * per_pair, st));
+    IFGF_CUDA(cudaFuncSetAttribute(beta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
+    for (int p0 = 0; p0 < count; p0 += sub) {
+        const int cnt = std::min(sub, count - p0);
+        BetaDev Bs = B;  // the graded rules of the batch are indexed by block: shift them
+        const std::size_t go = std::size_t(p0) * B.n_beta;
+        Bs.grid_u += go;
+        Bs.grid_wu += go;
+        Bs.grid_v += go;
+        Bs.grid_wv += go;
+        beta_kernel<<<cnt, kBetaThreads, smem2, st>>>(Bs, TT, max_dv, max_nu, max_nunv, p_base + p0, bs, bd, scratch);
+        IFGF_CUDA(cudaGetLastError());
+    }
+    IFGF_CUDA(cudaFreeAsync(scratch, st));
 }
 
 }  // namespace ifgfb200

@@ -79,6 +79,7 @@ near_kernel(NearDev N, PointsDev P, const double2* __restrict__ a_p, double k,
     const int n_t = int(N.end[tb]) - tbeg;
     const int q = N.chunk_q0[c] + threadIdx.x;
     const bool act = q < n_t;
+    if (__all_sync(0xffffffffu, !act)) return;  // whole warp past the box's targets (no barriers here)
     const int t = act ? tbeg + q : tbeg;
     const std::uint32_t l = N.perm[t];
     const double x = P.x[t], y = P.y[t], z = P.z[t];

@@ -93,3 +93,18 @@ def test_gpu_cone_decisions_bitwise(ref, mesh):
             assert gpu.evaluations(d, which) == cpu.evaluations(d, which)
         assert gpu.decision_hash(d) == cpu.decision_hash(d), d
     assert gpu.diagnostics() == cpu.diagnostics()
+
+
+@pytest.mark.parametrize("splits,nu,k", [(0, 4, 2 * np.pi), (0, 6, np.pi), (1, 4, 4.0)])
+def test_tiny_meshes_without_far_levels(ref, splits, nu, k):
+    # depth < 3: no cone levels at all, the apply is near field + RP only (solver.cpp:78-147);
+    # the smallest geometries the reference accepts
+    pm = P.SurfaceMesh.sphere(1.0, splits, nu, nu)
+    rm = ref.RefMesh.sphere(1.0, splits, nu, nu)
+    op = P.CombinedOperator(pm, P.SolveConfig(k=k))
+    ro = ref.RefOperator(rm, k)
+    phi = P.random_density(pm.size(), 6)
+    assert rel_l2(op.apply(phi), ro.apply(phi)) <= TOL
+    S, D = op.layer_potentials(phi)
+    rS, rD = ro.layer_potentials(phi)
+    assert rel_l2(S, rS) <= TOL and rel_l2(D, rD) <= TOL
