@@ -108,3 +108,27 @@ def test_tiny_meshes_without_far_levels(ref, splits, nu, k):
     S, D = op.layer_potentials(phi)
     rS, rD = ro.layer_potentials(phi)
     assert rel_l2(S, rS) <= TOL and rel_l2(D, rD) <= TOL
+
+
+@pytest.mark.parametrize("kw", [
+    dict(n_c0=3, n_s0=2),
+    dict(finest_box_lambda=0.25),
+    dict(finest_box_lambda=1.0),
+    dict(n_beta=48, cov_d=4),
+    dict(n_beta=128, cov_d=8),
+])
+def test_configuration_knobs(ref, kw):
+    # ConeConfig / SolveConfig / RpConfig knobs (ifgf.hpp:12-17, solver.hpp:32-45,
+    # rp.hpp:14-19) against the reference built with the same values
+    pm = P.SurfaceMesh.sphere(1.0, 2, 8, 8)
+    rm = ref.RefMesh.sphere(1.0, 2, 8, 8)
+    k = 4 * np.pi
+    cone = P.ConeConfig(n_c0=kw.get("n_c0", 2), n_s0=kw.get("n_s0", 1))
+    rp = P.RpConfig(n_beta=kw.get("n_beta", 96), cov_d=kw.get("cov_d", 6))
+    cfg = P.SolveConfig(k=k, cone=cone, rp=rp, finest_box_lambda=kw.get("finest_box_lambda", 0.5))
+    op = P.CombinedOperator(pm, cfg)
+    ro = ref.RefOperator(rm, k, n_c0=kw.get("n_c0", 0), n_s0=kw.get("n_s0", 0),
+                         finest_box_lambda=kw.get("finest_box_lambda", 0.0), n_beta=kw.get("n_beta", 0),
+                         cov_d=kw.get("cov_d", 0))
+    phi = P.random_density(pm.size(), 8)
+    assert rel_l2(op.apply(phi), ro.apply(phi)) <= TOL
