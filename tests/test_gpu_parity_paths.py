@@ -132,3 +132,16 @@ def test_configuration_knobs(ref, kw):
                          cov_d=kw.get("cov_d", 0))
     phi = P.random_density(pm.size(), 8)
     assert rel_l2(op.apply(phi), ro.apply(phi)) <= TOL
+
+
+@pytest.mark.parametrize("nu,nv", [(6, 9), (12, 5)])
+def test_rectangular_patch_grids(ref, nu, nv):
+    # nu != nv node grids per patch (geometry.hpp:16-34): RP coefficient transforms, beta
+    # table extents and the leaf / near field all see rectangular patches
+    pm = P.SurfaceMesh.sphere(1.0, 1, nu, nv)
+    rm = ref.RefMesh.sphere(1.0, 1, nu, nv)
+    k = 3 * np.pi
+    op = P.CombinedOperator(pm, P.SolveConfig(k=k))
+    ro = ref.RefOperator(rm, k)
+    phi = P.random_density(pm.size(), 10)
+    assert rel_l2(op.apply(phi), ro.apply(phi)) <= TOL
