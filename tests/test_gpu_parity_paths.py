@@ -145,3 +145,15 @@ def test_rectangular_patch_grids(ref, nu, nv):
     ro = ref.RefOperator(rm, k)
     phi = P.random_density(pm.size(), 10)
     assert rel_l2(op.apply(phi), ro.apply(phi)) <= TOL
+
+
+def test_largest_patch_resolution(ref):
+    # 48 x 48 nodes per patch, the reference's limit (geometry.cpp:33): the paper's smallest
+    # sphere (6 x 48^2 = 13,824 unknowns, 4 lambda); beta rows of 2,304 entries per pair
+    pm = P.SurfaceMesh.sphere(1.0, 0, 48, 48)
+    rm = ref.RefMesh.sphere(1.0, 0, 48, 48)
+    k = 4 * np.pi
+    op = P.CombinedOperator(pm, P.SolveConfig(k=k))
+    ro = ref.RefOperator(rm, k)
+    phi = P.random_density(pm.size(), 12)
+    assert rel_l2(op.apply(phi), ro.apply(phi)) <= TOL
