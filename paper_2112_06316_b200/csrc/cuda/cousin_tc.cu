@@ -65,7 +65,7 @@ cousin_tc_kernel(LevelDev L, PointsDev P, const double2* __restrict__ store, dou
             const double vx = x - L.cx[sb], vy = y - L.cy[sb], vz = z - L.cz[sb];
             const double r2 = fma(vx, vx, fma(vy, vy, vz * vz));
             const double inv_r = rsqrt(r2);
-            const LocalCoords lc = local_coords(vx, vy, vz, inv_r, h, L.seg_gamma[so], L);
+            const LocalCoords lc = local_coords_seg(vx, vy, vz, inv_r, h, so, L);
             double sn, cs;
             sincos_bounded(k * (r2 * inv_r), &sn, &cs);
             const double f1 = kInv4PiD * inv_r;

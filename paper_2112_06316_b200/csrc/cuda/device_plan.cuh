@@ -25,6 +25,9 @@ struct LevelDev {
     const std::int64_t* cev_begin = nullptr;                  // per target box
     const std::int32_t* cev_seg = nullptr;                    // per cousin evaluation
     const std::int32_t *seg_box = nullptr, *seg_gamma = nullptr, *box_seg_begin = nullptr;
+    // per segment: (g1, g2, g3) of its cell packed as g1 | g2 << 8 | g3 << 19 (no integer
+    // division on the device); null when the grid is too large to pack
+    const std::uint32_t* seg_code = nullptr;
     const std::int64_t* pev_begin = nullptr;  // per parent (level d-1) segment
     const std::int32_t* pev_seg = nullptr;    // per parent-node evaluation into this level
     const std::uint16_t* pev_perm = nullptr;  // evaluations grouped by child segment

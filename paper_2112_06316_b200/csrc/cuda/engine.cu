@@ -72,7 +72,7 @@ class DevBuf {
 struct LevelBufs {
     DevBuf cx, cy, cz, beg, end, cz_ptr, cz_idx, cev_begin, cev_seg, seg_box, seg_gamma,
         box_seg_begin, pev_begin, pev_seg, pev_perm, pgrp_begin, pgrp_seg, pgrp_start, pgrp_count, ch_ptr, ch_idx, s_nodes, th_nodes, ph_nodes, th_sin, th_cos, ph_sin, ph_cos, thc_cos, thc_sin, phc_cos, phc_sin,
-        chunk_box, chunk_q0, wchunk_box, wchunk_q0, tmpl_slot, tmpl, tmpl_gc;
+        chunk_box, chunk_q0, wchunk_box, wchunk_q0, tmpl_slot, tmpl, tmpl_gc, seg_code;
 };
 
 Pipes make_pipes(const std::vector<int>& f) {
@@ -467,6 +467,16 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         b.cev_seg.upload(CL.cev_seg);
         b.seg_box.upload(CL.seg_box);
         b.seg_gamma.upload(CL.seg_gamma);
+        if (CL.ns <= 256 && CL.nc <= 2048 && 2 * CL.nc <= 8192) {  // packed cells (no device division)
+            std::vector<std::uint32_t> code(CL.seg_gamma.size());
+            for (std::size_t i = 0; i < code.size(); ++i) {
+                const int g = CL.seg_gamma[i];
+                const int g1 = g % CL.ns, rest = g / CL.ns, g2 = rest % CL.nc, g3 = rest / CL.nc;
+                code[i] = std::uint32_t(g1) | (std::uint32_t(g2) << 8) | (std::uint32_t(g3) << 19);
+            }
+            b.seg_code.upload(code);
+            L.seg_code = b.seg_code.as<std::uint32_t>();
+        }
         b.box_seg_begin.upload(CL.box_seg_begin);
         b.pev_begin.upload(CL.pev_begin);
         // per-evaluation child ordinals are only read by the generic-order parent kernel;

@@ -127,6 +127,28 @@ __device__ __forceinline__ LocalCoords local_coords(double vx, double vy, double
     return o;
 }
 
+// local_coords for the segment with ordinal so, its cell decoded from the packed code
+__device__ __forceinline__ LocalCoords local_coords_seg(double vx, double vy, double vz, double inv_r, double h,
+                                                        int so, const LevelDev& L) {
+    if (!L.thc_cos || !L.seg_code) return local_coords(vx, vy, vz, inv_r, h, L.seg_gamma[so], L);
+    const unsigned code = L.seg_code[so];
+    const int g1 = int(code & 0xffu), g2 = int((code >> 8) & 0x7ffu), g3 = int(code >> 19);
+    const double rho = sqrt(fma(vx, vx, vy * vy));
+    const double ctc = L.thc_cos[g2], stc = L.thc_sin[g2];
+    const double cpc = L.phc_cos[g3], spc = L.phc_sin[g3];
+    const double tn = fma(rho, ctc, -vz * stc), td = fma(vz, ctc, rho * stc);
+    const double pn = fma(vy, cpc, -vx * spc), pd = fma(vx, cpc, vy * spc);
+    const double inv = 1.0 / (td * pd);  // one division for both tangents
+    const double tt = tn * pd * inv, tp = pn * td * inv;
+    if (!(fabs(tt) <= 0.4225 && fabs(tp) <= 0.4225 && td > 0.0 && pd > 0.0))
+        return local_coords_lib(vx, vy, vz, inv_r, h, L.seg_gamma[so], L);
+    LocalCoords o;
+    o.ls = fma(h * inv_r, 2.0 * L.inv_ds, -(2 * g1 + 1.0));
+    o.lt = atan_small(tt) * (2.0 * L.inv_dth);
+    o.lp = atan_small(tp) * (2.0 * L.inv_dph);
+    return o;
+}
+
 // sum_{ip,it,is} c[is + ps*(it + pa*ip)] T_is(ls) T_it(lt) T_ip(lp)
 template <int PS, int PA>
 __device__ __forceinline__ double2 eval_series(const double2* __restrict__ c, const double* ts,
