@@ -52,6 +52,11 @@ struct LevelDev {
     int nchunk = 0;
     const std::int32_t *wchunk_box = nullptr, *wchunk_q0 = nullptr;  // 32-target warp items
     int nwchunk = 0;
+    // leaf-fill work items (leaf level): consecutive segments [seg0, seg0 + nseg) of box0
+    // (the first `split`) and box1 (the rest; -1: none)
+    const std::int32_t *litem_seg0 = nullptr, *litem_nseg = nullptr, *litem_split = nullptr;
+    const std::int32_t *litem_box0 = nullptr, *litem_box1 = nullptr;
+    int n_litem = 0;
     int max_pts = 0;  // largest box
 };
 

@@ -72,7 +72,8 @@ class DevBuf {
 struct LevelBufs {
     DevBuf cx, cy, cz, beg, end, cz_ptr, cz_idx, cev_begin, cev_seg, seg_box, seg_gamma,
         box_seg_begin, pev_begin, pev_seg, pev_perm, pgrp_begin, pgrp_seg, pgrp_start, pgrp_count, ch_ptr, ch_idx, s_nodes, th_nodes, ph_nodes, th_sin, th_cos, ph_sin, ph_cos, thc_cos, thc_sin, phc_cos, phc_sin,
-        chunk_box, chunk_q0, wchunk_box, wchunk_q0, tmpl_slot, tmpl, tmpl_gc, seg_code;
+        chunk_box, chunk_q0, wchunk_box, wchunk_q0, tmpl_slot, tmpl, tmpl_gc, seg_code, litem_seg0,
+        litem_nseg, litem_split, litem_box0, litem_box1;
 };
 
 Pipes make_pipes(const std::vector<int>& f) {
@@ -456,6 +457,57 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         L.wchunk_box = b.wchunk_box.as<std::int32_t>();
         L.wchunk_q0 = b.wchunk_q0.as<std::int32_t>();
         L.nwchunk = int(wchunk_box.size());
+        if (d == T.depth) {  // leaf-fill items: <= G consecutive segments of at most two boxes
+            const int G = leaf_item_segments(CL.pang), tile = leaf_item_tile();
+            std::vector<std::int32_t> i_s0, i_n, i_split, i_b0, i_b1;
+            int cs0 = 0, cn = 0, cb0 = -1, cb1 = -1, csplit = 0;
+            auto flush = [&] {
+                if (cn == 0) return;
+                i_s0.push_back(cs0);
+                i_n.push_back(cn);
+                i_split.push_back(cb1 < 0 ? cn : csplit);
+                i_b0.push_back(cb0);
+                i_b1.push_back(cb1);
+                cn = 0;
+                cb0 = cb1 = -1;
+            };
+            for (std::size_t bx = 0; bx < nb; ++bx) {
+                int s = CL.box_seg_begin[bx];
+                int S = CL.box_seg_begin[bx + 1] - s;
+                if (S == 0) continue;
+                const bool big = int(B.end[bx] - B.begin[bx]) > tile;
+                if (big) flush();  // a box streaming its sources in tiles gets items of its own
+                while (S > 0) {
+                    if (cn > 0 && cb0 != int(bx) && cb1 < 0 && !big) {  // second box of the item
+                        cb1 = int(bx);
+                        csplit = cn;
+                    } else if (cn > 0 && cb0 != int(bx) && cb1 != int(bx)) {
+                        flush();
+                    }
+                    if (cn == 0) {
+                        cs0 = s;
+                        cb0 = int(bx);
+                    }
+                    const int take = std::min(G - cn, S);
+                    cn += take;
+                    s += take;
+                    S -= take;
+                    if (cn == G || big) flush();
+                }
+            }
+            flush();
+            b.litem_seg0.upload(i_s0);
+            b.litem_nseg.upload(i_n);
+            b.litem_split.upload(i_split);
+            b.litem_box0.upload(i_b0);
+            b.litem_box1.upload(i_b1);
+            L.litem_seg0 = b.litem_seg0.as<std::int32_t>();
+            L.litem_nseg = b.litem_nseg.as<std::int32_t>();
+            L.litem_split = b.litem_split.as<std::int32_t>();
+            L.litem_box0 = b.litem_box0.as<std::int32_t>();
+            L.litem_box1 = b.litem_box1.as<std::int32_t>();
+            L.n_litem = int(i_s0.size());
+        }
         b.cx.upload(cx);
         b.cy.upload(cy);
         b.cz.upload(cz);

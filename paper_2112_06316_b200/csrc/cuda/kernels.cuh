@@ -29,6 +29,9 @@ void launch_parent_fill(const LevelDev& Lp, const LevelDev& Lc, const double2* c
 // tensor-core cousin evaluation (cousin_tc.cu); false when the orders are not (3, 5)
 bool launch_cousin_eval_tc(const LevelDev& L, const PointsDev& P, const double2* store, double k, const Pipes& pipes,
                            double2* Sp, double2* Dp, cudaStream_t st);
+// leaf-fill work items: segments per item for an angular order, sources per staged tile
+int leaf_item_segments(int pang);
+int leaf_item_tile();
 bool launch_leaf_fill_ray(const LevelDev& L, const PointsDev& P, const double2* a_p, double k, const Pipes& pipes,
                           const double* Ms, const double* Ma, double2* store, cudaStream_t st);
 // FP64 tensor-core parent fill (parent_tc.cu) for ps = 3, pang = 5; false if not applicable
