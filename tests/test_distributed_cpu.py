@@ -68,3 +68,51 @@ def test_partition_balance_single_process():
         sizes = np.diff(b)
         assert b[0] == 0 and b[-1] == mesh.size() and np.all(sizes > 0)
         assert sizes.max() <= 2.0 * sizes.mean()  # cost-balanced, so roughly point-balanced
+
+
+def _worker_per_rank(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2112_06316_b200 as P
+    from paper_2112_06316_b200.distributed import plan_partition
+
+    mesh = P.SurfaceMesh.sphere(1.0, 2, 16, 16)
+    cfg = P.SolveConfig(k=4 * np.pi, gamma=4 * np.pi, device=-1, part_rank=rank, part_world=world)
+    plan = P.HostPlan(mesh, cfg)  # this rank's share only
+    b = plan_partition(plan, world)
+    segs = {d: sorted(zip(plan.level_cones(d)["seg_box"].tolist(), plan.level_cones(d)["seg_gamma"].tolist()))
+            for d in range(3, plan.depth + 1)}
+    npairs = len(plan.proximity()["target"])
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (b.tolist(), segs, npairs))
+    q.put((rank, gathered))
+    dist.destroy_process_group()
+
+
+def test_per_rank_plans_over_gloo():
+    # each rank builds only its share of the plan (SolveConfig.part_rank / part_world) with a
+    # partition derived identically on every rank; together the shares cover the full plan
+    import paper_2112_06316_b200 as P
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_per_rank, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    gathered = res[0][1]
+    assert gathered[0][0] == gathered[1][0]  # same partition on both ranks
+    mesh = P.SurfaceMesh.sphere(1.0, 2, 16, 16)
+    full = P.HostPlan(mesh, P.SolveConfig(k=4 * np.pi, gamma=4 * np.pi, device=-1))
+    for d in range(3, full.depth + 1):
+        F = set(zip(full.level_cones(d)["seg_box"].tolist(), full.level_cones(d)["seg_gamma"].tolist()))
+        union = set(gathered[0][1][d]) | set(gathered[1][1][d])
+        assert union == F, d
+    # pairs are classified for the owned targets only: the shares add up to the full list
+    assert gathered[0][2] + gathered[1][2] == len(full.proximity()["target"])
