@@ -30,6 +30,8 @@
  *   ifgf_near_field         near_field                                 postprocess.hpp:39-41
  *   ifgf_mie_far_field      mie_far_field                              postprocess.hpp:44-45
  *   ifgf_rp_regular_apply   rp_regular_apply                           rp.hpp:78-82
+ *   ifgf_closest_point      closest_point                              rp.hpp:49-51
+ *   ifgf_graded             cov_w / cov_w_deriv / cov_xi / cov_xi_deriv rp.hpp:53-57
  *   ifgf_eps_metric         eps_far / eps_near                         postprocess.hpp:49-52
  */
 #ifndef IFGF_B200_H
@@ -210,6 +212,12 @@ int ifgf_solve_incident(ifgf_operator* op, double theta, double phi, const doubl
 /* incident_trace (solver.hpp:28-30): u^i at the nodes, 2*N doubles */
 int ifgf_incident_trace(const ifgf_surface* s, double k, double theta, double phi,
                         const double* src, int64_t nsrc, double* out);
+
+/* closest point on patch q to x (3) from (u0, v0): alternating golden-section sweeps
+ * (rp.hpp:49-51); out = (u, v, dist), bit-identical to the reference */
+int ifgf_closest_point(const ifgf_surface* s, int q, const double* x, double u0, double v0, double* out);
+/* graded change of variables around alpha (rp.hpp:53-57): which = 0 w, 1 w', 2 xi, 3 xi' */
+double ifgf_graded(int which, double alpha, double tau, int d);
 
 /* ---- fields after the solve (postprocess.cpp). The dense sums run on
  * GPU `device` over the oversampled per-patch Fejér quadrature of the density. ---- */

@@ -83,6 +83,8 @@ def lib():
                                     C.c_int, C.c_int, C.c_int, d_p, d_p, C.c_int]),
             "ref_solve_sources": (C.c_int, [vp, C.c_double, C.c_double, d_p, C.c_long, C.c_double, C.c_int, C.c_int,
                                             d_p, d_p, C.c_int]),
+            "ref_closest_point": (C.c_int, [vp, C.c_int, d_p, C.c_double, C.c_double, d_p]),
+            "ref_graded": (C.c_double, [C.c_int, C.c_double, C.c_double, C.c_int]),
             "ref_rp_regular_apply": (C.c_int, [vp, d_p, d_p, C.c_long, C.c_double, d_p, d_p]),
             "ref_far_field": (C.c_int, [vp, d_p, C.c_double, C.c_double, C.c_int, C.c_int, d_p, d_p]),
             "ref_near_field": (C.c_int, [vp, d_p, C.c_double, C.c_double, C.c_double, C.c_double, d_p, C.c_long,

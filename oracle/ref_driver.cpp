@@ -18,6 +18,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <limits>
 #include <memory>
 #include <numbers>
 #include <random>
@@ -542,6 +543,32 @@ int ref_rp_regular_apply(void* mesh, const double* density, const double* target
         return 0;
     } catch (const std::exception& e) {
         return -fail(e);
+    }
+}
+
+int ref_closest_point(void* mesh, int q, const double* x, double u0, double v0, double* out) {
+    try {
+        const auto c = closest_point(M(mesh).patches[q], {x[0], x[1], x[2]}, u0, v0);
+        out[0] = c.u;
+        out[1] = c.v;
+        out[2] = c.dist;
+        return 0;
+    } catch (const std::exception& e) {
+        return -fail(e);
+    }
+}
+
+double ref_graded(int which, double alpha, double tau, int d) {
+    try {
+        switch (which) {
+            case 0: return cov_w(tau, d);
+            case 1: return cov_w_deriv(tau, d);
+            case 2: return cov_xi(alpha, tau, d);
+            default: return cov_xi_deriv(alpha, tau, d);
+        }
+    } catch (const std::exception& e) {
+        fail(e);
+        return std::numeric_limits<double>::quiet_NaN();
     }
 }
 

@@ -122,6 +122,8 @@ _SIGS = {
     "ifgf_far_field": (C.c_int, [vp, d_p, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, d_p, d_p]),
     "ifgf_near_field": (C.c_int, [vp, d_p, C.c_double, C.c_double, C.c_double, C.c_double, d_p, C.c_int64, d_p,
                                   C.c_int64, C.c_double, C.c_int, d_p, d_p, C.POINTER(C.c_uint8)]),
+    "ifgf_closest_point": (C.c_int, [vp, C.c_int, d_p, C.c_double, C.c_double, d_p]),
+    "ifgf_graded": (C.c_double, [C.c_int, C.c_double, C.c_double, C.c_int]),
     "ifgf_rp_regular_apply": (C.c_int, [vp, d_p, d_p, C.c_int64, C.c_double, C.c_int, d_p, d_p]),
     "ifgf_mie_far_field": (C.c_int, [C.c_double, C.c_double, d_p, d_p, C.c_int64, C.c_int, d_p]),
     "ifgf_eps_metric": (C.c_int, [d_p, d_p, C.c_int64, d_p, C.POINTER(C.c_int)]),

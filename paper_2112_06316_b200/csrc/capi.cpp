@@ -15,6 +15,8 @@
 #include "host/chebyshev.hpp"
 #include <cuda_runtime.h>
 
+#include <limits>
+
 #include "fields_gpu.hpp"
 #include "host/gmres.hpp"
 
@@ -1161,6 +1163,34 @@ int ifgf_rp_regular_apply(const ifgf_surface* s, const double* density, const do
             D[2 * i + 1] += d_out[i].imag();
         }
     });
+}
+
+int ifgf_closest_point(const ifgf_surface* s, int q, const double* x, double u0, double v0, double* out) {
+    return guarded([&] {
+        need(s, "surface");
+        need(x, "x");
+        need(out, "out");
+        if (q < 0 || q >= int(s->s->patches.size())) throw InvalidArgument("closest_point: patch index out of range");
+        const ClosestPoint c = closest_point_on(s->s->patches[q], {x[0], x[1], x[2]}, u0, v0);
+        out[0] = c.u;
+        out[1] = c.v;
+        out[2] = c.dist;
+    });
+}
+
+double ifgf_graded(int which, double alpha, double tau, int d) {
+    try {
+        switch (which) {
+            case 0: return grade_w(tau, d);
+            case 1: return grade_w_deriv(tau, d);
+            case 2: return grade_xi(alpha, tau, d);
+            case 3: return grade_xi_deriv(alpha, tau, d);
+            default: throw InvalidArgument("graded: which must be 0..3");
+        }
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return std::numeric_limits<double>::quiet_NaN();
+    }
 }
 
 int ifgf_mie_far_field(double radius, double k, const double* direction, const double* dirs, int64_t n,

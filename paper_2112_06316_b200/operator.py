@@ -98,6 +98,30 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def closest_point(mesh: "SurfaceMesh", q: int, x, u0: float, v0: float):
+    """(u, v, dist) of the closest point of patch q to x (rp.hpp:49-51)."""
+    out = np.zeros(3)
+    check(lib().ifgf_closest_point(mesh._h, int(q), _ptr(np.ascontiguousarray(x, dtype=np.float64)), u0, v0,
+                                   _ptr(out)), "closest_point")
+    return float(out[0]), float(out[1]), float(out[2])
+
+
+def cov_w(tau: float, d: int) -> float:  # rp.hpp:53-57, graded change of variables
+    return float(lib().ifgf_graded(0, 0.0, tau, d))
+
+
+def cov_w_deriv(tau: float, d: int) -> float:
+    return float(lib().ifgf_graded(1, 0.0, tau, d))
+
+
+def cov_xi(alpha: float, tau: float, d: int) -> float:
+    return float(lib().ifgf_graded(2, alpha, tau, d))
+
+
+def cov_xi_deriv(alpha: float, tau: float, d: int) -> float:
+    return float(lib().ifgf_graded(3, alpha, tau, d))
+
+
 def random_density(n: int, seed: int) -> np.ndarray:
     """U(-1,1) + i U(-1,1) from std::mt19937_64(seed), in the reference harness's draw order."""
     out = np.zeros(n, dtype=np.complex128)

@@ -42,3 +42,31 @@ def test_incident_trace_kinds():
     assert np.allclose(P.incident_trace(P.IncidentField(sources=src), mesh, k), want, rtol=1e-14, atol=0)
     with pytest.raises(P.InvalidArgument):
         P.incident_trace(P.IncidentField(sources=pos[:1]), mesh, k)
+
+
+def test_closest_point_and_graded_rules_bitwise(ref):
+    # proximity building blocks (rp.hpp:44-57) equal the reference's bit for bit
+    pm = P.SurfaceMesh.sphere(1.0, 1, 8, 8)
+    rm = ref.RefMesh.sphere(1.0, 1, 8, 8)
+    rng = np.random.default_rng(1)
+    for _ in range(20):
+        q = int(rng.integers(0, 24))
+        x = rng.normal(size=3)
+        x *= rng.uniform(0.9, 1.3) / np.linalg.norm(x)
+        u0, v0 = rng.uniform(-1, 1, size=2)
+        ours = P.closest_point(pm, q, x, u0, v0)
+        theirs = np.zeros(3)
+        assert ref.lib().ref_closest_point(rm.h, q, ref._p(np.ascontiguousarray(x)), u0, v0, ref._p(theirs)) == 0
+        assert ours == tuple(theirs)
+    def same(a, b):  # bitwise, or both refused (NaN)
+        return a == b or (np.isnan(a) and np.isnan(b))
+
+    for d in (2, 4, 6, 9):
+        for tau in np.linspace(0, 2 * np.pi, 17):
+            for alpha in (-0.7, 0.0, 0.3, 1.0, 1.5):
+                assert same(P.cov_xi(alpha, tau, d), ref.lib().ref_graded(2, alpha, tau, d))
+                assert same(P.cov_xi_deriv(alpha, tau, d), ref.lib().ref_graded(3, alpha, tau, d))
+            assert same(P.cov_w(tau, d), ref.lib().ref_graded(0, 0.0, tau, d))
+            assert same(P.cov_w_deriv(tau, d), ref.lib().ref_graded(1, 0.0, tau, d))
+    with pytest.raises(P.InvalidArgument):
+        P.closest_point(pm, 99, [1.0, 0.0, 0.0], 0.0, 0.0)
