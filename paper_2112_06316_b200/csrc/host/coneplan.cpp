@@ -129,13 +129,48 @@ void group_parent_evaluations(ConeLevel& L, std::size_t pseg, int w, int P) {
         const std::int64_t b = L.pev_begin[so], n = L.pev_begin[so + 1] - b;
         if (n > 65535) throw InternalError("cone plan: too many evaluations per parent segment");
         std::uint16_t* perm = L.pev_perm.data() + b;
-        for (std::int64_t i = 0; i < n; ++i) perm[i] = std::uint16_t(i);
         const std::int32_t* seg = L.pev_seg.data() + b;
-        std::stable_sort(perm, perm + n, [&](std::uint16_t x, std::uint16_t y) { return seg[x] < seg[y]; });
-        int g = 0;
-        for (std::int64_t i = 0; i < n; ++i)
-            if (i == 0 || seg[perm[i]] != seg[perm[i - 1]]) ++g;
-        ngroups[so + 1] = g;
+        // stable bucketing by child segment: few distinct values per parent segment
+        constexpr int kMaxU = 64;
+        std::int32_t val[kMaxU];
+        int cnt[kMaxU], u = 0;
+        bool many = false;
+        for (std::int64_t i = 0; i < n && !many; ++i) {
+            int j = 0;
+            while (j < u && val[j] != seg[i]) ++j;
+            if (j == u) {
+                if (u == kMaxU) {
+                    many = true;
+                    break;
+                }
+                val[u] = seg[i];
+                cnt[u++] = 0;
+            }
+            ++cnt[j];
+        }
+        if (many) {
+            for (std::int64_t i = 0; i < n; ++i) perm[i] = std::uint16_t(i);
+            std::stable_sort(perm, perm + n, [&](std::uint16_t x, std::uint16_t y) { return seg[x] < seg[y]; });
+            int g = 0;
+            for (std::int64_t i = 0; i < n; ++i)
+                if (i == 0 || seg[perm[i]] != seg[perm[i - 1]]) ++g;
+            ngroups[so + 1] = g;
+            return;
+        }
+        int order[kMaxU], start[kMaxU];
+        for (int j = 0; j < u; ++j) order[j] = j;
+        std::sort(order, order + u, [&](int x, int y) { return val[x] < val[y]; });
+        int acc = 0;
+        for (int r = 0; r < u; ++r) {
+            start[order[r]] = acc;
+            acc += cnt[order[r]];
+        }
+        for (std::int64_t i = 0; i < n; ++i) {
+            int j = 0;
+            while (val[j] != seg[i]) ++j;
+            perm[start[j]++] = std::uint16_t(i);
+        }
+        ngroups[so + 1] = u;
     });
     L.pgrp_begin.assign(pseg + 1, 0);
     for (std::size_t so = 0; so < pseg; ++so) L.pgrp_begin[so + 1] = L.pgrp_begin[so] + ngroups[so + 1];
@@ -375,11 +410,24 @@ ConePlanHost build_cone_plan(const BoxTree& t, const BoxRelations& rel,
                 }
         }
         L.box_seg_begin[nb] = std::int32_t(L.seg_box.size());
+        // gamma -> ordinal of (box, gamma) among the relevant segments: segments are in (box,
+        // gamma) order, so the ordinal is the exclusive prefix count of the marks (a table
+        // lookup; binary search per box when the candidate grid is too large for a table)
+        std::vector<std::int32_t> ordtab;
+        if (nb * spb <= (std::size_t(1) << 29)) {
+            ordtab.assign(nb * spb, -1);
+            std::int32_t o = 0;
+            for (std::size_t i = 0; i < nb * spb; ++i)
+                if (marks[i]) ordtab[i] = o++;
+        }
         marks.clear();
         marks.shrink_to_fit();
-
-        // gamma -> ordinal of (box, gamma) among the relevant segments
         auto ordinal = [&](std::int32_t box, int g) {
+            if (!ordtab.empty()) {
+                const std::int32_t o = ordtab[std::size_t(box) * spb + std::size_t(g)];
+                if (o < 0) throw InternalError("cone plan: unmarked segment");
+                return o;
+            }
             const auto b0 = L.seg_gamma.begin() + L.box_seg_begin[box];
             const auto b1 = L.seg_gamma.begin() + L.box_seg_begin[box + 1];
             const auto it = std::lower_bound(b0, b1, g);
