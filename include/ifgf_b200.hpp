@@ -16,6 +16,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <span>
 #include <vector>
 
 #include "ifgf_b200.h"
@@ -176,6 +177,32 @@ class GpuCombinedOperator {
 
     ifgf_operator* handle() const { return op_; }
 
+#ifdef IFGF_B200_WITH_REFERENCE
+    // solve(mesh, incident, cfg) (solver.hpp:111-112) on this operator: rhs = -u^i for either
+    // IncidentField kind, restarted MGS-GMRES with the Krylov basis in HBM
+    ifgf::SolveResult solve(const ifgf::IncidentField& inc, const ifgf::SolveConfig& sc) const {
+        std::vector<double> src;
+        if (inc.kind == ifgf::IncidentField::Kind::PointSources)
+            for (const auto& y : inc.sources) src.insert(src.end(), {y.x, y.y, y.z});
+        ifgf::SolveResult r;
+        r.density.resize(n_);
+        r.residual_history.resize(std::size_t(sc.max_iter) + 1);
+        int it = 0, cv = 0;
+        const int rc = ifgf_solve_incident(op_, inc.theta, inc.phi, src.empty() ? nullptr : src.data(),
+                                           int64_t(src.size() / 3), sc.tol, sc.max_iter, sc.restart,
+                                           reinterpret_cast<double*>(r.density.data()), r.residual_history.data(),
+                                           int(r.residual_history.size()), &it, &cv);
+        r.iterations = it;
+        r.converged = cv != 0;
+        r.residual_history.resize(std::size_t(std::max(it, 0)));
+        r.gamma = gamma();
+        r.k = sc.k;
+        if (rc == 4) return r;  // not converged: the reference reports it in the result
+        check(rc, "solve");
+        return r;
+    }
+#endif
+
   private:
     void build(const Surface& s, const ifgf_config& c) {
         check(ifgf_operator_create(s.get(), &c, &op_), "GpuCombinedOperator");
@@ -185,5 +212,20 @@ class GpuCombinedOperator {
     ifgf_operator* op_ = nullptr;
     std::size_t n_ = 0;
 };
+
+#ifdef IFGF_B200_WITH_REFERENCE
+// far_field(mesh, density, gamma, k, n_phi, n_theta) (postprocess.hpp:34-37), the dense sum
+// on GPU `device`
+inline ifgf::FarFieldGrid gpu_far_field(const ifgf::SurfaceMesh& mesh, std::span<const cplx> density, double gamma,
+                                       double k, int n_phi, int n_theta, int device = 0) {
+    Surface s = Surface::from_reference(mesh);
+    ifgf::FarFieldGrid g = ifgf::FarFieldGrid::make(n_phi, n_theta);
+    std::vector<double> dirs(3 * g.directions.size());
+    check(ifgf_far_field(s.get(), reinterpret_cast<const double*>(density.data()), gamma, k, n_phi, n_theta, device,
+                         dirs.data(), reinterpret_cast<double*>(g.values.data())),
+          "far_field");
+    return g;
+}
+#endif
 
 }  // namespace ifgfb200

@@ -8,6 +8,7 @@
 #include <numbers>
 #include <random>
 
+#include "ifgf/postprocess.hpp"
 #include "ifgf/solver.hpp"
 #include "../../include/ifgf_b200.hpp"
 
@@ -70,6 +71,25 @@ int main() {
     check("gmres iterations equal", res_gpu.iterations == res_ref.iterations, res_gpu.iterations);
     check("gmres solution", rel_l2(res_gpu.solution, res_ref.solution) <= 1e-8,
           rel_l2(res_gpu.solution, res_ref.solution));
+
+    // solve() and far_field() through the header, against the reference's own
+    SolveConfig scfg = cfg;
+    scfg.tol = 1e-6;
+    const auto sol_ref = solve(mesh, inc, scfg);
+    const auto sol_gpu = gpu.solve(inc, scfg);
+    check("solve iterations equal", sol_gpu.iterations == sol_ref.iterations && sol_gpu.converged, sol_gpu.iterations);
+    check("solve density", rel_l2(sol_gpu.density, sol_ref.density) <= 1e-8, rel_l2(sol_gpu.density, sol_ref.density));
+    const auto ff_ref = far_field(mesh, sol_ref.density, sol_ref.gamma, cfg.k, 9, 17);
+    const auto ff_gpu = ifgfb200::gpu_far_field(mesh, sol_ref.density, sol_ref.gamma, cfg.k, 9, 17);
+    check("far field", rel_l2(ff_gpu.values, ff_ref.values) <= 1e-12, rel_l2(ff_gpu.values, ff_ref.values));
+    IncidentField pts;
+    pts.kind = IncidentField::Kind::PointSources;
+    pts.sources = {{0.1, 0.2, -0.1}};
+    const auto ps_ref = solve(mesh, pts, scfg);
+    const auto ps_gpu = gpu.solve(pts, scfg);
+    check("point-source solve", ps_gpu.iterations == ps_ref.iterations &&
+                                    rel_l2(ps_gpu.density, ps_ref.density) <= 1e-8,
+          rel_l2(ps_gpu.density, ps_ref.density));
     std::printf("%d failure(s)\n", failures);
     return failures == 0 ? 0 : 1;
 }
