@@ -169,6 +169,8 @@ int ifgf_operator_load_beta_cache(ifgf_operator* op, const char* path);
 int ifgf_operator_upload_density(ifgf_operator* op, const double* phi);
 int ifgf_operator_time_applies(ifgf_operator* op, int iters, int flush_l2, double* ms_per_apply);
 /* ms for {weights, leaf, cousin, parent, near, rp, total} of one instrumented apply */
+/* device time of each of iters graph applies (ms_each: iters entries) */
+int ifgf_operator_time_applies_each(ifgf_operator* op, int iters, int flush_l2, double* ms_each);
 int ifgf_operator_time_phases(ifgf_operator* op, double* ms7);
 int ifgf_operator_kernels_per_apply(const ifgf_operator* op);
 void* ifgf_operator_device_phi(ifgf_operator* op);

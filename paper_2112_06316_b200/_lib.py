@@ -102,6 +102,7 @@ _SIGS = {
     "ifgf_operator_upload_density": (C.c_int, [vp, d_p]),
     "ifgf_operator_time_applies": (C.c_int, [vp, C.c_int, C.c_int, d_p]),
     "ifgf_operator_time_phases": (C.c_int, [vp, d_p]),
+    "ifgf_operator_time_applies_each": (C.c_int, [vp, C.c_int, C.c_int, d_p]),
     "ifgf_operator_kernels_per_apply": (C.c_int, [vp]),
     "ifgf_operator_device_phi": (vp, [vp]),
     "ifgf_operator_device_out": (vp, [vp]),

@@ -882,6 +882,15 @@ int ifgf_operator_time_applies(ifgf_operator* op, int iters, int flush_l2, doubl
     });
 }
 
+int ifgf_operator_time_applies_each(ifgf_operator* op, int iters, int flush_l2, double* ms_each) {
+    return guarded([&] {
+        need(op, "operator");
+        need(ms_each, "ms_each");
+        const auto v = op->eng->time_device_applies_each(iters, flush_l2 != 0);
+        for (std::size_t i = 0; i < v.size(); ++i) ms_each[i] = v[i];
+    });
+}
+
 int ifgf_operator_time_phases(ifgf_operator* op, double* ms7) {
     return guarded([&] {
         need(op, "operator");

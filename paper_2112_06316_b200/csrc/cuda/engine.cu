@@ -1154,6 +1154,13 @@ void Engine::upload_density(const cplx* phi) {
 }
 
 double Engine::time_device_applies(int iters, bool flush_l2) {
+    const std::vector<double> each = time_device_applies_each(iters, flush_l2);
+    double total = 0;
+    for (double t : each) total += t;
+    return each.empty() ? 0.0 : total / double(each.size());
+}
+
+std::vector<double> Engine::time_device_applies_each(int iters, bool flush_l2) {
     Impl& e = *d_;
     std::lock_guard<std::mutex> g(e.mu);
     e.ensure_beta();
@@ -1165,7 +1172,7 @@ double Engine::time_device_applies(int iters, bool flush_l2) {
     cudaEvent_t a, b;
     IFGF_CUDA(cudaEventCreate(&a));
     IFGF_CUDA(cudaEventCreate(&b));
-    float total = 0.f;
+    std::vector<double> each;
     for (int i = 0; i < iters; ++i) {
         if (flush_l2) IFGF_CUDA(cudaMemsetAsync(e.flush.as<void>(), i & 0xff, flush_bytes, e.st));
         IFGF_CUDA(cudaEventRecord(a, e.st));
@@ -1174,11 +1181,11 @@ double Engine::time_device_applies(int iters, bool flush_l2) {
         IFGF_CUDA(cudaEventSynchronize(b));
         float ms = 0.f;
         IFGF_CUDA(cudaEventElapsedTime(&ms, a, b));
-        total += ms;
+        each.push_back(double(ms));
     }
     cudaEventDestroy(a);
     cudaEventDestroy(b);
-    return iters > 0 ? double(total) / iters : 0.0;
+    return each;
 }
 
 PhaseTimes Engine::time_phases() {

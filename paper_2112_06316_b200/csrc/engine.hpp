@@ -83,6 +83,7 @@ class Engine {
     // benchmark helpers: graph replays with device-resident phi (no host copies)
     void upload_density(const cplx* phi);
     double time_device_applies(int iters, bool flush_l2);   // mean ms per apply
+    std::vector<double> time_device_applies_each(int iters, bool flush_l2);  // ms of each apply
     PhaseTimes time_phases();                               // one instrumented apply
     int kernels_per_apply() const;
     std::string describe() const;

@@ -435,6 +435,12 @@ class CombinedOperator:
         check(lib().ifgf_operator_time_applies(self._h, iters, int(flush_l2), C.byref(ms)), "time_applies")
         return ms.value
 
+    def time_applies_each(self, iters: int, flush_l2: bool = True) -> np.ndarray:
+        """Device time (ms) of each of `iters` graph applies (CUDA events, engine stream)."""
+        out = np.zeros(max(iters, 1))
+        check(lib().ifgf_operator_time_applies_each(self._h, iters, int(flush_l2), _ptr(out)), "time_applies_each")
+        return out[:iters]
+
     def time_phases(self) -> dict:
         v = np.zeros(7)
         check(lib().ifgf_operator_time_phases(self._h, _ptr(v)), "time_phases")
