@@ -10,6 +10,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 #include <string>
 #include <cstring>
@@ -112,7 +113,7 @@ struct Engine::Impl {
     DevBuf storeA, storeB;
     std::size_t store_elems = 0;
     // near field
-    DevBuf nb_ptr, nb_idx, tpb, pair_patch, far_begin, far_end, far_pos, near_chunk_box, near_chunk_q0;
+    DevBuf nb_ptr, nb_idx, leaf_of_m, tpb, pair_patch, far_begin, far_end, far_pos, near_chunk_box, near_chunk_q0;
     NearDev near;
     // rp
     DevBuf patch_nu, patch_nv, patch_start, mat_off, mats, beta_off, beta_s, beta_d, coeffs;
@@ -173,15 +174,22 @@ struct Engine::Impl {
     }
 
     // the IFGF far field on a_p (Morton) into Sp/Dp (accumulated)
-    int run_ifgf(bool single, bool dbl, DlStrategy s, cudaEvent_t* ev = nullptr) {
+    // after_leaf (optional) is issued right after the leaf-fill launch: side-stream work then
+    // queues behind the leaf's CTAs and fills the room they leave
+    template <class F = void (*)()>
+    int run_ifgf(bool single, bool dbl, DlStrategy s, cudaEvent_t* ev = nullptr, F after_leaf = nullptr) {
         int launches = 0;
-        if (depth < 3 || (!single && !dbl)) return 0;
+        if (depth < 3 || (!single && !dbl)) {
+            if constexpr (!std::is_same_v<F, void (*)()>) after_leaf();
+            return 0;
+        }
         double2* cur = storeA.as<double2>();
         double2* nxt = storeB.as<double2>();
         auto pipes_d = make_pipes(pipes_at(depth, single, dbl, s));
         launch_leaf_fill(L[depth - 1], P, a_p.as<double2>(), k, pipes_d, Ms.as<double>(),
                          Ma.as<double>(), cur, st);
         ++launches;
+        if constexpr (!std::is_same_v<F, void (*)()>) after_leaf();
         if (ev) IFGF_CUDA(cudaEventRecord(ev[0], st));
         for (int d = depth; d >= 3; --d) {
             const Pipes pc = make_pipes(pipes_at(d, single, dbl, s));
@@ -210,14 +218,34 @@ struct Engine::Impl {
         IFGF_CUDA(cudaMemsetAsync(Dn.as<void>(), 0, vb, st));
         launch_weights(int(n), perm.as<std::uint32_t>(), phi, jw_p.as<double>(), a_p.as<double2>(), st);
         ++launches;
-        IFGF_CUDA(cudaEventRecord(ev_fork, st));
-        IFGF_CUDA(cudaStreamWaitEvent(st2, ev_fork, 0));
-        launch_near_field(near, P, a_p.as<double2>(), k, Sn.as<double2>(), Dn.as<double2>(), st2);
-        launch_density_coeffs(rp, phi, coeffs.as<double2>(), st2);
-        launch_rp_accum(rp, coeffs.as<double2>(), Sn.as<double2>(), Dn.as<double2>(), st2);
+        static const bool one_stream = [] {
+            const char* e = std::getenv("IFGF_SIDE_STREAM");
+            return e && e[0] == '0';
+        }();
+        cudaStream_t side = one_stream ? st : st2;
+        if (!one_stream) {
+            IFGF_CUDA(cudaEventRecord(ev_fork, st));
+            IFGF_CUDA(cudaStreamWaitEvent(st2, ev_fork, 0));
+        }
+        auto side_work = [&] {
+            launch_near_field(near, P, a_p.as<double2>(), k, Sn.as<double2>(), Dn.as<double2>(), side);
+            launch_density_coeffs(rp, phi, coeffs.as<double2>(), side);
+            launch_rp_accum(rp, coeffs.as<double2>(), Sn.as<double2>(), Dn.as<double2>(), side);
+            IFGF_CUDA(cudaEventRecord(ev_join, side));
+        };
+        // measured (cfg2): side work issued before the leaf fill is fastest with the warp-per-
+        // target near kernel; IFGF_SIDE_ORDER=after_leaf queues it behind the leaf instead
+        static const bool side_first = [] {
+            const char* e = std::getenv("IFGF_SIDE_ORDER");
+            return !(e && std::string(e) == "after_leaf");
+        }();
         launches += 3;
-        IFGF_CUDA(cudaEventRecord(ev_join, st2));
-        launches += run_ifgf(true, true, strategy);
+        if (side_first || one_stream) {
+            side_work();
+            launches += run_ifgf(true, true, strategy);
+        } else {
+            launches += run_ifgf(true, true, strategy, nullptr, side_work);
+        }
         if (world > 1) reduce_far_to_owners();  // far-field partials -> target owners
         IFGF_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
         RpDev r = rp;
@@ -680,6 +708,12 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
             e.lb[D - 1].beg.upload(B.begin);
             e.lb[D - 1].end.upload(B.end);
         }
+        {
+            std::vector<std::int32_t> lom(n, 0);
+            for (std::size_t b = 0; b < B.size(); ++b)
+                for (std::uint32_t t = B.begin[b]; t < B.end[b]; ++t) lom[t] = std::int32_t(b);
+            e.leaf_of_m.upload(lom);
+        }
         e.nb_ptr.upload(R.nbr[D - 1].ptr);
         e.nb_idx.upload(R.nbr[D - 1].idx);
         e.tpb.upload(PL.target_pair_begin);
@@ -698,6 +732,7 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         N.nb_ptr = e.nb_ptr.as<std::int32_t>();
         N.nb_idx = e.nb_idx.as<std::int32_t>();
         N.patch_p = e.patch_p.as<std::int32_t>();
+        N.leaf_of_m = e.leaf_of_m.as<std::int32_t>();
         N.tpb = e.tpb.as<std::uint32_t>();
         N.pair_patch = e.pair_patch.as<std::int32_t>();
         N.far_begin = e.far_begin.as<std::uint32_t>();

@@ -55,6 +55,7 @@ struct NearDev {
     const std::int32_t *chunk_box = nullptr, *chunk_q0 = nullptr;
     int nchunk = 0;
     const std::uint8_t* leaf_active = nullptr;  // owned target leaves (null = all)
+    const std::int32_t* leaf_of_m = nullptr;    // leaf box of each Morton point (warp kernel)
 };
 void launch_weights(int n, const std::uint32_t* perm, const double2* phi, const double* jw_p,
                     double2* a_p, cudaStream_t st);

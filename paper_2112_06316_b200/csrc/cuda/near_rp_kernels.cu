@@ -11,6 +11,9 @@
 //                   fused with 1/2 phi + D - i gamma S (solver.cpp:152-156) and the
 //                   Morton un-permute (ifgf.cpp:603-606).
 //  * direct       : layer_potential_direct's regular part (rp.cpp:481-513), O(N^2).
+#include <cstdlib>
+#include <string>
+
 #include "dev_common.cuh"
 #include "kernels.cuh"
 
@@ -115,6 +118,80 @@ near_kernel(NearDev N, PointsDev P, const double2* __restrict__ a_p, double k,
         }
     Sp[t] = cadd(Sp[t], accS);
     Dp[t] = cadd(Dp[t], accD);
+}
+
+// Warp per target, lanes over sources: each warp screens its target's neighbourhood 32
+// candidates at a time (self and singular-patch exclusions, solver.cpp:117-124), appends the
+// valid sources to a per-warp queue (ballot) and evaluates full 32-lane batches of pairs, so
+// excluded pairs cost no lane time; the far-node corrections (solver.cpp:131-139) run
+// lane-parallel, and a fixed shuffle tree sums the lanes (deterministic).
+constexpr int kNearWarps = 4;
+__global__ void __launch_bounds__(32 * kNearWarps, 8)
+near_warp_kernel(NearDev N, PointsDev P, const double2* __restrict__ a_p, double k, double2* __restrict__ Sp,
+                 double2* __restrict__ Dp) {
+    __shared__ int queue[kNearWarps][64];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int t = blockIdx.x * kNearWarps + w;  // Morton target
+    if (t >= N.n) return;
+    const int tb = N.leaf_of_m[t];
+    if (N.leaf_active && !N.leaf_active[tb]) return;  // target owned by another rank
+    const std::uint32_t l = N.perm[t];
+    const double x = P.x[t], y = P.y[t], z = P.z[t];
+    const int p0 = int(N.tpb[l]), p1 = int(N.tpb[l + 1]);
+    const int nsing = p1 - p0;
+    int sing[kMaxSing];
+#pragma unroll
+    for (int i = 0; i < kMaxSing; ++i) sing[i] = (i < nsing) ? N.pair_patch[p0 + i] : -1;
+    int* q = queue[w];
+    int qn = 0;
+    double2 accS = make_double2(0.0, 0.0), accD = make_double2(0.0, 0.0);
+    for (int j = N.nb_ptr[tb]; j < N.nb_ptr[tb + 1]; ++j) {
+        const int nb = N.nb_idx[j];
+        const int u1 = int(N.end[nb]);
+        for (int ub = int(N.beg[nb]); ub < u1; ub += 32) {
+            const int u = ub + lane;
+            bool ok = u < u1 && u != t;
+            if (ok) {
+                const int pq = N.patch_p[u];
+#pragma unroll
+                for (int i = 0; i < kMaxSing; ++i) ok &= (sing[i] != pq);
+                if (nsing > kMaxSing)
+                    for (int i = kMaxSing; i < nsing; ++i) ok &= (N.pair_patch[p0 + i] != pq);
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, ok);
+            if (ok) q[qn + __popc(m & ((1u << lane) - 1u))] = u;
+            qn += __popc(m);
+            __syncwarp();
+            if (qn >= 32) {
+                const int v = q[lane];
+                pair_kernels(x, y, z, P.x[v], P.y[v], P.z[v], P.nx[v], P.ny[v], P.nz[v], a_p[v], k, 1.0, accS, accD);
+                __syncwarp();
+                if (lane < qn - 32) q[lane] = q[lane + 32];
+                qn -= 32;
+                __syncwarp();
+            }
+        }
+    }
+    if (lane < qn) {
+        const int v = q[lane];
+        pair_kernels(x, y, z, P.x[v], P.y[v], P.z[v], P.nx[v], P.ny[v], P.nz[v], a_p[v], k, 1.0, accS, accD);
+    }
+    for (int p = p0; p < p1; ++p)
+        for (std::uint32_t f = N.far_begin[p] + lane; f < N.far_end[p]; f += 32) {
+            const int u = int(N.far_pos[f]);
+            pair_kernels(x, y, z, P.x[u], P.y[u], P.z[u], P.nx[u], P.ny[u], P.nz[u], a_p[u], k, -1.0, accS, accD);
+        }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        accS.x += __shfl_xor_sync(0xffffffffu, accS.x, o);
+        accS.y += __shfl_xor_sync(0xffffffffu, accS.y, o);
+        accD.x += __shfl_xor_sync(0xffffffffu, accD.x, o);
+        accD.y += __shfl_xor_sync(0xffffffffu, accD.y, o);
+    }
+    if (lane == 0) {
+        Sp[t] = cadd(Sp[t], accS);
+        Dp[t] = cadd(Dp[t], accD);
+    }
 }
 
 // one CTA per patch: a^q = Mv (Mu phi_q) along u then v (chebyshev.cpp:43-61)
@@ -323,7 +400,14 @@ void launch_unpermute1(int n, const std::uint32_t* perm, const double2* in_m, do
 void launch_near_field(const NearDev& N, const PointsDev& P, const double2* a_p, double k,
                        double2* Sp, double2* Dp, cudaStream_t st) {
     if (N.nchunk == 0) return;
-    near_kernel<<<N.nchunk, kNearThreads, 0, st>>>(N, P, a_p, k, Sp, Dp);
+    static const bool per_thread = [] {
+        const char* e = std::getenv("IFGF_NEAR");
+        return e && std::string(e) == "thread";
+    }();
+    if (per_thread || !N.leaf_of_m)
+        near_kernel<<<N.nchunk, kNearThreads, 0, st>>>(N, P, a_p, k, Sp, Dp);
+    else
+        near_warp_kernel<<<(N.n + kNearWarps - 1) / kNearWarps, 32 * kNearWarps, 0, st>>>(N, P, a_p, k, Sp, Dp);
     IFGF_CUDA(cudaGetLastError());
 }
 
