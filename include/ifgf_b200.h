@@ -114,6 +114,9 @@ int64_t ifgf_plan_level(const ifgf_plan* p, int level, int32_t* params4, double*
                         int32_t* seg_box, int32_t* seg_gamma);
 /* number of cousin / parent-node evaluations planned at a level */
 int64_t ifgf_plan_evaluations(const ifgf_plan* p, int level, int which);
+/* cousin DMMA tile statistics of a level for warp items of `items_of` targets:
+ * out3 = (evaluations, segment groups, 8-row tiles) (kernel design diagnostics) */
+int ifgf_plan_cousin_tile_stats(const ifgf_plan* p, int level, int items_of, int64_t* out3);
 int64_t ifgf_plan_npairs(const ifgf_plan* p);
 /* {groups, evaluations, 8-row tensor-core tiles} of the parent-node evaluations into level */
 int ifgf_plan_tile_stats(const ifgf_plan* p, int level, int64_t* out3);

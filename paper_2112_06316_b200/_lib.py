@@ -73,6 +73,7 @@ _SIGS = {
     "ifgf_plan_evaluations": (C.c_int64, [vp, C.c_int, C.c_int]),
     "ifgf_plan_npairs": (C.c_int64, [vp]),
     "ifgf_plan_tile_stats": (C.c_int, [vp, C.c_int, C.POINTER(C.c_int64)]),
+    "ifgf_plan_cousin_tile_stats": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(C.c_int64)]),
     "ifgf_plan_nfar": (C.c_int64, [vp]),
     "ifgf_plan_pairs": (C.c_int, [vp, u32_p, i32_p, d_p, d_p, u32_p, u32_p, u32_p, u32_p]),
     "ifgf_plan_beta_fingerprint": (C.c_uint64, [vp]),

@@ -508,6 +508,40 @@ int ifgf_plan_tile_stats(const ifgf_plan* p, int level, int64_t* out3) {
     });
 }
 
+int ifgf_plan_cousin_tile_stats(const ifgf_plan* p, int level, int items_of, int64_t* out3) {
+    return guarded([&] {
+        need(p, "plan");
+        need(out3, "out");
+        if (level < 3 || level > p->tree.depth || items_of < 1) throw InvalidArgument("cousin tile stats: bad level");
+        const ConeLevel& L = p->cones.level[level - 1];
+        const BoxLevel& B = p->tree.level[level - 1];
+        int64_t evals = 0, groups = 0, tiles = 0;
+        std::vector<std::int32_t> segs;
+        for (std::size_t tb = 0; tb < B.size(); ++tb) {
+            const int64_t n_t = B.end[tb] - B.begin[tb];
+            const int ncz = int(L.cz.count(tb));
+            for (int64_t q0 = 0; q0 < n_t; q0 += items_of)
+                for (int j = 0; j < ncz; ++j) {
+                    segs.clear();
+                    for (int64_t q = q0; q < std::min(n_t, q0 + items_of); ++q)
+                        segs.push_back(L.cev_seg[std::size_t(L.cev_begin[tb] + j * n_t + q)]);
+                    std::sort(segs.begin(), segs.end());
+                    for (std::size_t i = 0; i < segs.size();) {
+                        std::size_t e = i;
+                        while (e < segs.size() && segs[e] == segs[i]) ++e;
+                        ++groups;
+                        tiles += int64_t((e - i + 7) / 8);
+                        evals += int64_t(e - i);
+                        i = e;
+                    }
+                }
+        }
+        out3[0] = evals;
+        out3[1] = groups;
+        out3[2] = tiles;
+    });
+}
+
 int64_t ifgf_plan_npairs(const ifgf_plan* p) { return p ? int64_t(p->pairs.size()) : -1; }
 int64_t ifgf_plan_nfar(const ifgf_plan* p) { return p ? int64_t(p->pairs.far_nodes.size()) : -1; }
 
