@@ -33,6 +33,11 @@ struct LevelDev {
     const std::uint16_t* pev_perm = nullptr;  // evaluations grouped by child segment
     const std::int32_t *pgrp_begin = nullptr, *pgrp_seg = nullptr;
     const std::uint16_t *pgrp_start = nullptr, *pgrp_count = nullptr;
+    // the same groups packed for the tensor-core parent kernel (one 16-byte load per group):
+    // {child segment, child box, start | count << 16 | child octant << 24, cell of the child
+    // segment (seg_code layout when seg_code is set, else gamma)}; the evaluations of
+    // pev_perm carry bit 15 when the parent's geometry template applies (host-checked)
+    const int4* pgrp_rec = nullptr;
     const std::int32_t *ch_ptr = nullptr, *ch_idx = nullptr;  // children (level d+1) of this level's boxes
     const double *s_nodes = nullptr, *th_nodes = nullptr, *ph_nodes = nullptr;
     // sin/cos of the angular node tables (interpolation-node directions)
@@ -41,11 +46,10 @@ struct LevelDev {
     // wider than pi/4 (nc < 4), where local_coords uses acos/atan2
     const double *thc_cos = nullptr, *thc_sin = nullptr, *phc_cos = nullptr, *phc_sin = nullptr;
     // parent-fill geometry templates for this level's children (host/coneplan.hpp
-    // parent_templates): slot per cone cell (-1: none), 8 doubles per (slot, octant, node)
-    // entry and the template child cell; null when the level does not use them
+    // parent_templates): slot per cone cell (-1: none) and 8 doubles per (slot, octant, node)
+    // entry; which evaluations may use them is marked in the child level's pev_perm
     const std::int32_t* tmpl_slot = nullptr;
     const double* tmpl = nullptr;
-    const std::int32_t* tmpl_gc = nullptr;
     // multi-GPU source ownership: box has sources in this rank's Morton range (null = all)
     const std::uint8_t* active = nullptr;
     const std::int32_t *chunk_box = nullptr, *chunk_q0 = nullptr;  // cousin work chunks

@@ -73,8 +73,8 @@ class DevBuf {
 struct LevelBufs {
     DevBuf cx, cy, cz, beg, end, cz_ptr, cz_idx, cev_begin, cev_seg, seg_box, seg_gamma,
         box_seg_begin, pev_begin, pev_seg, pev_perm, pgrp_begin, pgrp_seg, pgrp_start, pgrp_count, ch_ptr, ch_idx, s_nodes, th_nodes, ph_nodes, th_sin, th_cos, ph_sin, ph_cos, thc_cos, thc_sin, phc_cos, phc_sin,
-        chunk_box, chunk_q0, wchunk_box, wchunk_q0, tmpl_slot, tmpl, tmpl_gc, seg_code, litem_seg0,
-        litem_nseg, litem_split, litem_box0, litem_box1;
+        chunk_box, chunk_q0, wchunk_box, wchunk_q0, tmpl_slot, tmpl, seg_code, litem_seg0,
+        litem_nseg, litem_split, litem_box0, litem_box1, pgrp_rec;
 };
 
 Pipes make_pipes(const std::vector<int>& f) {
@@ -659,6 +659,7 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
     // ---- parent-fill geometry templates where a level's cone cells are reused by many
     // parent segments (at least 8 evaluations per template entry); IFGF_PARENT_TEMPLATES=0
     // turns them off, =force builds them on every level (tests)
+    std::vector<std::vector<std::int32_t>> tmpl_slot_h(T.depth + 1), tmpl_gc_h(T.depth + 1);
     {
         const char* env = std::getenv("IFGF_PARENT_TEMPLATES");
         const bool enabled = !(env && std::string(env) == "0");
@@ -681,12 +682,62 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
             LevelBufs& b = e.lb[d - 2];
             b.tmpl_slot.upload(slot);
             b.tmpl.upload(tab);
-            b.tmpl_gc.upload(gc);
             LevelDev& L = e.L[d - 2];
             L.tmpl_slot = b.tmpl_slot.as<std::int32_t>();
             L.tmpl = b.tmpl.as<double>();
-            L.tmpl_gc = b.tmpl_gc.as<std::int32_t>();
+            tmpl_slot_h[d] = std::move(slot);
+            tmpl_gc_h[d] = std::move(gc);
         }
+    }
+
+    // ---- packed parent groups (tensor-core parent kernel): one record per group and the
+    // template bit of every evaluation, so the kernel's per-group and per-chunk loads do not
+    // chain through pev_perm -> ch_idx / seg_gamma -> cell tables / tmpl_gc
+    for (int d = 4; d <= T.depth; ++d) {
+        const ConeLevel& PL = C.level[d - 2];
+        const ConeLevel& CL = C.level[d - 1];
+        if (PL.ps != 3 || PL.pang != 5 || CL.ps != 3 || CL.pang != 5 || CL.pgrp_begin.empty()) continue;
+        const auto& cptr = C.child_ptr[d - 2];
+        const auto& cidx = C.child_idx[d - 2];
+        const std::vector<std::int32_t>& slot = tmpl_slot_h[d];
+        const std::vector<std::int32_t>& gc = tmpl_gc_h[d];
+        const bool packed = e.L[d - 1].seg_code != nullptr;
+        std::vector<int4> rec(CL.pgrp_seg.size());
+        std::vector<std::uint16_t> perm(CL.pev_perm);
+#pragma omp parallel for schedule(dynamic, 1024)
+        for (std::int64_t so = 0; so < std::int64_t(PL.nseg()); ++so) {
+            const int pb = PL.seg_box[so];
+            const std::int64_t ev0 = CL.pev_begin[so];
+            const int tslot = slot.empty() ? -1 : slot[PL.seg_gamma[so]];
+            const Vec3 pc = T.center(d - 1, std::size_t(pb));
+            for (int g = CL.pgrp_begin[so]; g < CL.pgrp_begin[so + 1]; ++g) {
+                const int start = CL.pgrp_start[g], count = CL.pgrp_count[g];
+                if (count > 255) throw InternalError("parent groups: more than 255 evaluations in one group");
+                const int c = (CL.pev_perm[ev0 + start] >> 8) & 7;
+                const int ch = cidx[cptr[pb] + c];
+                const int cso = CL.pgrp_seg[g];
+                const int cgam = CL.seg_gamma[cso];
+                int cell = cgam;
+                if (packed) {
+                    const int g1 = cgam % CL.ns, rest = cgam / CL.ns;
+                    cell = int(std::uint32_t(g1) | (std::uint32_t(rest % CL.nc) << 8) | (std::uint32_t(rest / CL.nc) << 19));
+                }
+                const Vec3 cc = T.center(d, std::size_t(ch));
+                const int oct = (cc.x > pc.x ? 1 : 0) | (cc.y > pc.y ? 2 : 0) | (cc.z > pc.z ? 4 : 0);
+                rec[g] = make_int4(cso, ch, start | (count << 16) | (oct << 24), cell);
+                if (tslot < 0) continue;
+                const std::size_t tbase = (std::size_t(tslot) * 8 + oct) * 75;
+                for (int i = start; i < start + count; ++i) {
+                    std::uint16_t& ent = perm[ev0 + i];
+                    if (gc[tbase + (ent & 0xff)] == cgam) ent = std::uint16_t(ent | 0x8000u);
+                }
+            }
+        }
+        LevelBufs& b = e.lb[d - 1];
+        b.pgrp_rec.upload(rec);
+        b.pev_perm.upload(perm);
+        e.L[d - 1].pgrp_rec = b.pgrp_rec.as<int4>();
+        e.L[d - 1].pev_perm = b.pev_perm.as<std::uint16_t>();
     }
 
     // ---- near field

@@ -81,6 +81,23 @@ __device__ __forceinline__ CellFrame cell_frame(int gamma, const LevelDev& L) {
     return f;
 }
 
+// the same frame from a packed cell code (LevelDev::seg_code layout)
+__device__ __forceinline__ CellFrame cell_frame_code(unsigned code, const LevelDev& L) {
+    CellFrame f;
+    f.g1 = int(code & 0xffu);
+    f.g2 = int((code >> 8) & 0x7ffu);
+    f.g3 = int(code >> 19);
+    if (L.thc_cos) {
+        f.ctc = L.thc_cos[f.g2];
+        f.stc = L.thc_sin[f.g2];
+        f.cpc = L.phc_cos[f.g3];
+        f.spc = L.phc_sin[f.g3];
+    } else {
+        f.ctc = f.stc = f.cpc = f.spc = 0.0;
+    }
+    return f;
+}
+
 // local coordinates inside a decoded cell (see local_coords below)
 __device__ __forceinline__ LocalCoords local_coords_in(double vx, double vy, double vz, double inv_r, double h,
                                                        const CellFrame& f, const LevelDev& L) {

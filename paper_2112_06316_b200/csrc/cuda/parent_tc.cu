@@ -31,6 +31,9 @@ using namespace ifgfdev;
 using namespace tc;
 
 constexpr int kWarps = 4;
+#ifndef IFGF_PARENT_MINB
+#define IFGF_PARENT_MINB 4
+#endif
 constexpr int kRow = kRowLen + 4;     // A slots, T(phi), ratio.re, ratio.im, extra factor, node (odd)
 constexpr int kGeoSz = 32 * kRow;      // one chunk of 32 evaluation rows per warp (even: the
                                        // accumulators behind it stay 16-byte aligned)
@@ -79,7 +82,7 @@ struct Combo<5> {  // (W2,W3) <- (W2,W3)
 };
 
 template <int COMBO>
-__global__ void __launch_bounds__(32 * kWarps, 5)
+__global__ void __launch_bounds__(32 * kWarps, IFGF_PARENT_MINB)
 parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, double k,
                  const double* __restrict__ Ms, const double* __restrict__ Ma,
                  double2* __restrict__ pstore) {
@@ -106,18 +109,27 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
     const int r = lane >> 2, tig = lane & 3;
     using LY = Layout<NPC>;
     const int gb = Lc.pgrp_begin[so], ge = Lc.pgrp_begin[so + 1];
+    // group records (host-packed: child segment, child box, start | count << 16 | child
+    // octant << 24, cell) run two groups ahead and the first pev_perm entries one group ahead,
+    // so a group's template loads issue at its start without a dependent-load chain
+    const int4* __restrict__ grec = Lc.pgrp_rec;
+    const std::uint16_t* __restrict__ perm = Lc.pev_perm + ev0;
+    const int4 zero4 = make_int4(0, 0, 0, 0);
+    int4 rec1 = gb < ge ? grec[gb] : zero4;
+    int4 rec2 = gb + 1 < ge ? grec[gb + 1] : zero4;
+    unsigned ent1 = (gb < ge && lane < ((rec1.z >> 16) & 0xff)) ? perm[(rec1.z & 0xffff) + lane] : 0u;
     for (int g = gb; g < ge; ++g) {
-        const int cso = Lc.pgrp_seg[g];
-        const int start = Lc.pgrp_start[g], count = Lc.pgrp_count[g];
-        // 1. geometry of the group's evaluations (one child box and one child cell per group)
-        const int c_grp = Lc.pev_perm[ev0 + start] >> 8;
-        const int ch = Lp.ch_idx[c0 + c_grp];
+        const int4 rec = rec1;
+        const unsigned ent_first = ent1;
+        rec1 = rec2;
+        if (g + 2 < ge) rec2 = grec[g + 2];
+        ent1 = (g + 1 < ge && lane < ((rec1.z >> 16) & 0xff)) ? perm[(rec1.z & 0xffff) + lane] : 0u;
+        const int cso = rec.x, ch = rec.y;
+        const int start = rec.z & 0xffff, count = (rec.z >> 16) & 0xff, oct = (rec.z >> 24) & 7;
         if (Lc.active && !Lc.active[ch]) continue;  // child holds no sources of this rank
         const double ccx = Lc.cx[ch], ccy = Lc.cy[ch], ccz = Lc.cz[ch];
-        const int cgam = Lc.seg_gamma[cso];
-        const CellFrame cf = cell_frame(cgam, Lc);
+        const CellFrame cf = Lc.seg_code ? cell_frame_code(unsigned(rec.w), Lc) : cell_frame(rec.w, Lc);
         // geometry template of (parent cell, child octant), host/coneplan.hpp parent_templates
-        const int oct = (ccx > pcx ? 1 : 0) | (ccy > pcy ? 2 : 0) | (ccz > pcz ? 4 : 0);
         const std::size_t tbase = (std::size_t(tslot) * 8 + oct) * kNP;
         // B fragments of the group's block, reused by all its tiles (tc_common.cuh)
         double bq[LY::NB];
@@ -125,9 +137,11 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
         for (int e0 = 0; e0 < count; e0 += 32) {  // chunks of 32 evaluations, one per lane
             const int cn = min(32, count - e0);
             if (lane < cn) {
-                const int node = Lc.pev_perm[ev0 + start + e0 + lane] & 0xff;  // entries are node | c << 8
+                // entries are node | c << 8, bit 15: the template applies (engine.cu)
+                const unsigned ent = e0 == 0 ? ent_first : perm[start + e0 + lane];
+                const int node = int(ent & 0xffu);
                 double ls, lt, lp, r1x, r1y, xf;
-                if (tslot >= 0 && Lp.tmpl_gc[tbase + node] == cgam) {
+                if (ent & 0x8000u) {
                     const double2* te = reinterpret_cast<const double2*>(Lp.tmpl + (tbase + node) * 8);
                     const double2 t0 = __ldg(te), t1 = __ldg(te + 1), t2 = __ldg(te + 2), t3 = __ldg(te + 3);
                     ls = t0.x;
@@ -272,7 +286,7 @@ bool launch_parent_fill_tc(const LevelDev& Lp, const LevelDev& Lc, const double2
                            const Pipes& parent_pipes, const Pipes& child_pipes, const double* Ms,
                            const double* Ma, double2* parent_store, cudaStream_t st) {
     const int combo = combo_of(parent_pipes, child_pipes);
-    if (combo < 0 || Lp.ps != kPS || Lp.pang != kPA || Lc.ps != kPS || Lc.pang != kPA || !Lc.pgrp_begin ||
+    if (combo < 0 || Lp.ps != kPS || Lp.pang != kPA || Lc.ps != kPS || Lc.pang != kPA || !Lc.pgrp_rec ||
         !Lp.th_sin)
         return false;
     if (Lp.nseg == 0) return true;

@@ -25,7 +25,7 @@ constexpr int kKS = kPA - 1;  // DMMA k-steps over the 15 (s, theta) pairs (4 x 
 static_assert(kPS == 3 && kPA == 5, "the k-slot map assumes 3 x 5 (s, theta) pairs");
 
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(d0), "+d"(d1)
                  : "d"(a), "d"(b));
 }
