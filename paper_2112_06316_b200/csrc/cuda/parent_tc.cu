@@ -183,12 +183,15 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
                 row[kRowLen + 3] = double(node);
             }
             __syncwarp();
-            // 2. 8-evaluation tensor-core tiles against the child block
-            for (int t0 = 0; t0 < cn; t0 += 8) {
+            // 2. 8-evaluation tensor-core tiles against the child block (issuing the next
+            // tile's DMMAs before this tile's epilogue measured slower)
+            auto mma = [&](int t0, double (&d)[LY::NQ][2]) {
+                const bool valid = t0 + r < cn;
+                tile_mma_row<NPC>(geo + (valid ? t0 + r : 0) * kRow, valid, tig, bq, d);
+            };
+            auto epilogue = [&](int t0, const double (&d)[LY::NQ][2]) {
                 const bool valid = t0 + r < cn;
                 const double* gp = geo + (valid ? t0 + r : 0) * kRow;
-                double d[LY::NQ][2];
-                tile_mma_row<NPC>(gp, valid, tig, bq, d);
                 const double2 val = tile_gather_row<NPC>(gp, lane, d);
                 // lanes tig < NPC now hold (re, im) of child pipe tig for evaluation row r
                 const double2 r1 = make_double2(gp[kRowLen], gp[kRowLen + 1]);
@@ -226,6 +229,11 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
                     double2& a = acc[int(gp[kRowLen + 3]) * NPP + dst];
                     a = cadd(a, ctb);
                 }
+            };
+            for (int t0 = 0; t0 < cn; t0 += 8) {
+                double d[LY::NQ][2];
+                mma(t0, d);
+                epilogue(t0, d);
             }
             __syncwarp();
         }
