@@ -114,6 +114,8 @@ struct Engine::Impl {
     std::size_t store_elems = 0;
     // near field
     DevBuf nb_ptr, nb_idx, leaf_of_m, tpb, pair_patch, far_begin, far_end, far_pos, near_chunk_box, near_chunk_q0;
+    DevBuf near_off, near_src;  // near lists (ensure_near_lists)
+    bool near_lists_done = false;
     NearDev near;
     // rp
     DevBuf patch_nu, patch_nv, patch_start, mat_off, mats, beta_off, beta_s, beta_d, coeffs;
@@ -210,6 +212,7 @@ struct Engine::Impl {
     // correction do not depend on the far field: they run on the side stream st2 into
     // (Sn, Dn) while the IFGF fills (Sp, Dp) on st; a combine kernel joins both.
     int run_apply(const double2* phi, double2* out, double2* S, double2* D) {
+        ensure_near_lists();
         int launches = 0;
         const std::size_t vb = n * sizeof(double2);
         IFGF_CUDA(cudaMemsetAsync(Sp.as<void>(), 0, vb, st));
@@ -268,6 +271,44 @@ struct Engine::Impl {
         if (!beta_ready) throw InternalError("beta tables not computed");
     }
 
+    // Near lists: the screening of every target's neighbourhood (self and singular-patch
+    // exclusions) runs once, on the device, and its compacted sources are kept in HBM (4 bytes
+    // per near pair) so the per-apply near kernel only evaluates pairs. Built at the first
+    // eager apply after construction or a partition change (never under graph capture);
+    // skipped when the lists would take more than a quarter of the free HBM, or with
+    // IFGF_NEAR_LISTS=0.
+    void ensure_near_lists() {
+        if (near_lists_done) return;
+        cudaStreamCaptureStatus cs;
+        IFGF_CUDA(cudaStreamIsCapturing(st, &cs));
+        if (cs != cudaStreamCaptureStatusNone) throw InternalError("near lists requested under graph capture");
+        near_lists_done = true;
+        near.list_off = nullptr;
+        near.list_src = nullptr;
+        near_off.alloc(0);
+        near_src.alloc(0);
+        const char* env = std::getenv("IFGF_NEAR_LISTS");
+        if ((env && env[0] == '0') || !near.leaf_of_m || near.n == 0) return;
+        DevBuf cnt;
+        cnt.alloc(std::size_t(near.n) * sizeof(std::int32_t));
+        launch_near_list_count(near, P, cnt.as<std::int32_t>(), st);
+        std::vector<std::int32_t> c(near.n);
+        IFGF_CUDA(cudaMemcpyAsync(c.data(), cnt.as<void>(), c.size() * sizeof(std::int32_t), cudaMemcpyDeviceToHost, st));
+        IFGF_CUDA(cudaStreamSynchronize(st));
+        std::vector<std::int64_t> off(std::size_t(near.n) + 1, 0);
+        for (int t = 0; t < near.n; ++t) off[t + 1] = off[t] + c[t];
+        const std::size_t bytes = std::size_t(off.back()) * sizeof(std::int32_t) + off.size() * sizeof(std::int64_t);
+        std::size_t free_b = 0, total_b = 0;
+        IFGF_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        if (bytes > free_b / 4) return;
+        near_off.upload(off);
+        near_src.alloc(std::max<std::size_t>(std::size_t(off.back()), 1) * sizeof(std::int32_t));
+        near.list_off = near_off.as<std::int64_t>();
+        near.list_src = near_src.as<std::int32_t>();
+        launch_near_list_fill(near, P, st);
+        IFGF_CUDA(cudaStreamSynchronize(st));
+    }
+
     // ---- multi-GPU: source ownership by Morton ranges of leaf boxes
     std::uint32_t own_lo = 0, own_hi = 0;
     bool partitioned = false;
@@ -289,6 +330,7 @@ struct Engine::Impl {
         own_lo = lo;
         own_hi = hi;
         partitioned = !(lo == 0 && hi == n);
+        near_lists_done = false;  // rebuilt for the owned targets at the next eager apply
         const bool all = lo == 0 && hi == n;
         active.resize(depth);
         for (int d = 3; d <= depth; ++d) {
@@ -1326,6 +1368,7 @@ PhaseTimes Engine::time_phases() {
         rec();
     }
     const int n0 = ie - 1;
+    e.ensure_near_lists();
     launch_near_field(e.near, e.P, e.a_p.as<double2>(), e.k, e.Sp.as<double2>(), e.Dp.as<double2>(), e.st);
     rec();
     const int r0 = ie - 1;
@@ -1408,6 +1451,7 @@ void Engine::finish_owned(const cplx* phi, const cplx* far_S, const cplx* far_D,
                    e.Dp.as<double2>(), e.st);
     launch_weights(int(e.n), e.perm.as<std::uint32_t>(), e.d_phi.as<double2>(), e.jw_p.as<double>(),
                    e.a_p.as<double2>(), e.st);
+    e.ensure_near_lists();
     launch_near_field(e.near, e.P, e.a_p.as<double2>(), e.k, e.Sp.as<double2>(), e.Dp.as<double2>(), e.st);
     launch_density_coeffs(e.rp, e.d_phi.as<double2>(), e.coeffs.as<double2>(), e.st);
     IFGF_CUDA(cudaMemsetAsync(e.scratch.as<void>(), 0, bytes, e.st));

@@ -56,6 +56,10 @@ struct NearDev {
     int nchunk = 0;
     const std::uint8_t* leaf_active = nullptr;  // owned target leaves (null = all)
     const std::int32_t* leaf_of_m = nullptr;    // leaf box of each Morton point (warp kernel)
+    // near lists (null: screen the neighbourhood every apply): the compacted sources of each
+    // Morton target, [list_off[t], list_off[t + 1]) of list_src (Morton indices)
+    const std::int64_t* list_off = nullptr;
+    std::int32_t* list_src = nullptr;
 };
 void launch_weights(int n, const std::uint32_t* perm, const double2* phi, const double* jw_p,
                     double2* a_p, cudaStream_t st);
@@ -64,6 +68,9 @@ void launch_unpermute(int n, const std::uint32_t* perm, const double2* Sp, const
                       double2* S, double2* D, cudaStream_t st);
 void launch_near_field(const NearDev& N, const PointsDev& P, const double2* a_p, double k,
                        double2* Sp, double2* Dp, cudaStream_t st);
+// near lists: per-target source counts (N.n entries), then the lists at N.list_off
+void launch_near_list_count(const NearDev& N, const PointsDev& P, std::int32_t* counts, cudaStream_t st);
+void launch_near_list_fill(const NearDev& N, const PointsDev& P, cudaStream_t st);
 
 struct RpDev {
     int n = 0, npatch = 0;

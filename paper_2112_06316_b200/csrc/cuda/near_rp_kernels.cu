@@ -125,16 +125,22 @@ near_kernel(NearDev N, PointsDev P, const double2* __restrict__ a_p, double k,
 // valid sources to a per-warp queue (ballot) and evaluates full 32-lane batches of pairs, so
 // excluded pairs cost no lane time; the far-node corrections (solver.cpp:131-139) run
 // lane-parallel, and a fixed shuffle tree sums the lanes (deterministic).
+// MODE 1 / 2 run the same screening once at setup and count / write the compacted sources
+// per target (the near lists below), in exactly the order the batches would take them.
 constexpr int kNearWarps = 4;
+template <int MODE>
 __global__ void __launch_bounds__(32 * kNearWarps, 8)
 near_warp_kernel(NearDev N, PointsDev P, const double2* __restrict__ a_p, double k, double2* __restrict__ Sp,
-                 double2* __restrict__ Dp) {
+                 double2* __restrict__ Dp, std::int32_t* __restrict__ out) {
     __shared__ int queue[kNearWarps][64];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int t = blockIdx.x * kNearWarps + w;  // Morton target
     if (t >= N.n) return;
     const int tb = N.leaf_of_m[t];
-    if (N.leaf_active && !N.leaf_active[tb]) return;  // target owned by another rank
+    if (N.leaf_active && !N.leaf_active[tb]) {  // target owned by another rank
+        if (MODE == 1 && lane == 0) out[t] = 0;
+        return;
+    }
     const std::uint32_t l = N.perm[t];
     const double x = P.x[t], y = P.y[t], z = P.z[t];
     const int p0 = int(N.tpb[l]), p1 = int(N.tpb[l + 1]);
@@ -144,6 +150,7 @@ near_warp_kernel(NearDev N, PointsDev P, const double2* __restrict__ a_p, double
     for (int i = 0; i < kMaxSing; ++i) sing[i] = (i < nsing) ? N.pair_patch[p0 + i] : -1;
     int* q = queue[w];
     int qn = 0;
+    std::int64_t written = MODE == 2 ? N.list_off[t] : 0;
     double2 accS = make_double2(0.0, 0.0), accD = make_double2(0.0, 0.0);
     for (int j = N.nb_ptr[tb]; j < N.nb_ptr[tb + 1]; ++j) {
         const int nb = N.nb_idx[j];
@@ -164,7 +171,10 @@ near_warp_kernel(NearDev N, PointsDev P, const double2* __restrict__ a_p, double
             __syncwarp();
             if (qn >= 32) {
                 const int v = q[lane];
-                pair_kernels(x, y, z, P.x[v], P.y[v], P.z[v], P.nx[v], P.ny[v], P.nz[v], a_p[v], k, 1.0, accS, accD);
+                if constexpr (MODE == 0)
+                    pair_kernels(x, y, z, P.x[v], P.y[v], P.z[v], P.nx[v], P.ny[v], P.nz[v], a_p[v], k, 1.0, accS, accD);
+                if constexpr (MODE == 2) N.list_src[written + lane] = v;
+                written += 32;
                 __syncwarp();
                 if (lane < qn - 32) q[lane] = q[lane + 32];
                 qn -= 32;
@@ -172,10 +182,56 @@ near_warp_kernel(NearDev N, PointsDev P, const double2* __restrict__ a_p, double
             }
         }
     }
+    if constexpr (MODE == 1) {
+        if (lane == 0) out[t] = int(written) + qn;
+        return;
+    }
     if (lane < qn) {
         const int v = q[lane];
+        if constexpr (MODE == 0)
+            pair_kernels(x, y, z, P.x[v], P.y[v], P.z[v], P.nx[v], P.ny[v], P.nz[v], a_p[v], k, 1.0, accS, accD);
+        if constexpr (MODE == 2) N.list_src[written + lane] = v;
+    }
+    if constexpr (MODE == 0) {
+        for (int p = p0; p < p1; ++p)
+            for (std::uint32_t f = N.far_begin[p] + lane; f < N.far_end[p]; f += 32) {
+                const int u = int(N.far_pos[f]);
+                pair_kernels(x, y, z, P.x[u], P.y[u], P.z[u], P.nx[u], P.ny[u], P.nz[u], a_p[u], k, -1.0, accS, accD);
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            accS.x += __shfl_xor_sync(0xffffffffu, accS.x, o);
+            accS.y += __shfl_xor_sync(0xffffffffu, accS.y, o);
+            accD.x += __shfl_xor_sync(0xffffffffu, accD.x, o);
+            accD.y += __shfl_xor_sync(0xffffffffu, accD.y, o);
+        }
+        if (lane == 0) {
+            Sp[t] = cadd(Sp[t], accS);
+            Dp[t] = cadd(Dp[t], accD);
+        }
+    }
+}
+
+// Warp per target over its precomputed near list (the compacted sources of near_warp_kernel,
+// built once at setup): lane i takes list entries i, i + 32, ..., the same sources in the same
+// order as the screening kernel, so the sums are bitwise equal to it without the per-apply
+// screening (ballots, patch tests, queue traffic).
+__global__ void __launch_bounds__(32 * kNearWarps, 8)
+near_list_kernel(NearDev N, PointsDev P, const double2* __restrict__ a_p, double k, double2* __restrict__ Sp,
+                 double2* __restrict__ Dp) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int t = blockIdx.x * kNearWarps + w;  // Morton target
+    if (t >= N.n) return;
+    if (N.leaf_active && !N.leaf_active[N.leaf_of_m[t]]) return;
+    const std::uint32_t l = N.perm[t];
+    const double x = P.x[t], y = P.y[t], z = P.z[t];
+    double2 accS = make_double2(0.0, 0.0), accD = make_double2(0.0, 0.0);
+    const std::int64_t e = N.list_off[t + 1];
+    for (std::int64_t i = N.list_off[t] + lane; i < e; i += 32) {
+        const int v = N.list_src[i];
         pair_kernels(x, y, z, P.x[v], P.y[v], P.z[v], P.nx[v], P.ny[v], P.nz[v], a_p[v], k, 1.0, accS, accD);
     }
+    const int p0 = int(N.tpb[l]), p1 = int(N.tpb[l + 1]);
     for (int p = p0; p < p1; ++p)
         for (std::uint32_t f = N.far_begin[p] + lane; f < N.far_end[p]; f += 32) {
             const int u = int(N.far_pos[f]);
@@ -404,10 +460,27 @@ void launch_near_field(const NearDev& N, const PointsDev& P, const double2* a_p,
         const char* e = std::getenv("IFGF_NEAR");
         return e && std::string(e) == "thread";
     }();
+    const int grid = (N.n + kNearWarps - 1) / kNearWarps;
     if (per_thread || !N.leaf_of_m)
         near_kernel<<<N.nchunk, kNearThreads, 0, st>>>(N, P, a_p, k, Sp, Dp);
+    else if (N.list_off)
+        near_list_kernel<<<grid, 32 * kNearWarps, 0, st>>>(N, P, a_p, k, Sp, Dp);
     else
-        near_warp_kernel<<<(N.n + kNearWarps - 1) / kNearWarps, 32 * kNearWarps, 0, st>>>(N, P, a_p, k, Sp, Dp);
+        near_warp_kernel<0><<<grid, 32 * kNearWarps, 0, st>>>(N, P, a_p, k, Sp, Dp, nullptr);
+    IFGF_CUDA(cudaGetLastError());
+}
+
+void launch_near_list_count(const NearDev& N, const PointsDev& P, std::int32_t* counts, cudaStream_t st) {
+    if (N.n == 0 || !N.leaf_of_m) return;
+    near_warp_kernel<1><<<(N.n + kNearWarps - 1) / kNearWarps, 32 * kNearWarps, 0, st>>>(N, P, nullptr, 0.0, nullptr,
+                                                                                         nullptr, counts);
+    IFGF_CUDA(cudaGetLastError());
+}
+
+void launch_near_list_fill(const NearDev& N, const PointsDev& P, cudaStream_t st) {
+    if (N.n == 0 || !N.leaf_of_m || !N.list_off) return;
+    near_warp_kernel<2><<<(N.n + kNearWarps - 1) / kNearWarps, 32 * kNearWarps, 0, st>>>(N, P, nullptr, 0.0, nullptr,
+                                                                                         nullptr, nullptr);
     IFGF_CUDA(cudaGetLastError());
 }
 

@@ -42,6 +42,20 @@ def test_kernel_variants(ref, monkeypatch, env, value, splits, nu, k):
     assert rel_l2(op.apply(phi), ro.apply(phi)) <= TOL
 
 
+@pytest.mark.parametrize("splits,nu,k", [(2, 6, 4 * np.pi), (3, 8, 8 * np.pi)])
+def test_near_lists_bitwise(monkeypatch, splits, nu, k):
+    # the precomputed near lists hold the screened sources in the screening kernel's batch
+    # order: the near field (and so the whole apply) is bitwise the same with and without them
+    pm = P.SurfaceMesh.sphere(1.0, splits, nu, nu)
+    phi = P.random_density(pm.size(), 4)
+    monkeypatch.setenv("IFGF_NEAR_LISTS", "0")
+    screened = P.CombinedOperator(pm, P.SolveConfig(k=k)).layer_potentials(phi)
+    monkeypatch.delenv("IFGF_NEAR_LISTS")
+    listed = P.CombinedOperator(pm, P.SolveConfig(k=k)).layer_potentials(phi)
+    for a, b in zip(screened, listed):
+        assert np.array_equal(a, b)
+
+
 @pytest.mark.parametrize("axes,k", [((4.0, 1.0, 1.0), 2 * np.pi), ((2.5, 0.6, 1.2), 3 * np.pi)])
 def test_spheroid_parity(ref, axes, k):
     pm = P.SurfaceMesh.spheroid(2, 8, 8, *axes)
