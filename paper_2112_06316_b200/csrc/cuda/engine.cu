@@ -105,6 +105,7 @@ struct Engine::Impl {
 
     // points (Morton order)
     DevBuf px, py, pz, pnx, pny, pnz, jw_p, ones_p, perm, pos, patch_p, identity;
+    DevBuf pgeo;  // (x, y), (z, nx), (ny, nz) per Morton point: one 48-byte row per near-pair source
     // original order copies for the direct sum and beta
     DevBuf ox, oy, oz, onx, ony, onz, ojw, opatch;
     std::vector<LevelBufs> lb;   // [d-1]
@@ -455,6 +456,18 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
             pos[l] = std::uint32_t(t);
             pp[t] = S.patch_of[l];
             ident[t] = std::uint32_t(t);
+        }
+        {
+            std::vector<double> g(6 * n);
+            for (std::size_t t = 0; t < n; ++t) {
+                g[6 * t] = x[t];
+                g[6 * t + 1] = y[t];
+                g[6 * t + 2] = z[t];
+                g[6 * t + 3] = nx[t];
+                g[6 * t + 4] = ny[t];
+                g[6 * t + 5] = nz[t];
+            }
+            e.pgeo.upload(g);
         }
         e.px.upload(x);
         e.py.upload(y);
@@ -826,6 +839,7 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         N.nb_idx = e.nb_idx.as<std::int32_t>();
         N.patch_p = e.patch_p.as<std::int32_t>();
         N.leaf_of_m = e.leaf_of_m.as<std::int32_t>();
+        N.geo = e.pgeo.as<double2>();
         N.tpb = e.tpb.as<std::uint32_t>();
         N.pair_patch = e.pair_patch.as<std::int32_t>();
         N.far_begin = e.far_begin.as<std::uint32_t>();

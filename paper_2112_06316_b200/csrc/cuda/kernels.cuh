@@ -59,6 +59,7 @@ struct NearDev {
     // near lists (null: screen the neighbourhood every apply): the compacted sources of each
     // Morton target, [list_off[t], list_off[t + 1]) of list_src (Morton indices)
     const std::int64_t* list_off = nullptr;
+    const double2* geo = nullptr;  // (x, y), (z, nx), (ny, nz) per Morton point
     std::int32_t* list_src = nullptr;
 };
 void launch_weights(int n, const std::uint32_t* perm, const double2* phi, const double* jw_p,

@@ -212,11 +212,26 @@ near_warp_kernel(NearDev N, PointsDev P, const double2* __restrict__ a_p, double
     }
 }
 
+// pair_kernels with the source's geometry from its packed 48-byte row
+__device__ __forceinline__ void near_pair(const double2* __restrict__ geo, int v, double x, double y, double z,
+                                          const double2* __restrict__ a_p, double k, double sg, double2& accS,
+                                          double2& accD) {
+    const double2 g0 = __ldg(geo + 3 * v), g1 = __ldg(geo + 3 * v + 1), g2 = __ldg(geo + 3 * v + 2);
+    pair_kernels(x, y, z, g0.x, g0.y, g1.x, g1.y, g2.x, g2.y, a_p[v], k, sg, accS, accD);
+}
+
 // Warp per target over its precomputed near list (the compacted sources of near_warp_kernel,
 // built once at setup): lane i takes list entries i, i + 32, ..., the same sources in the same
 // order as the screening kernel, so the sums are bitwise equal to it without the per-apply
 // screening (ballots, patch tests, queue traffic).
-__global__ void __launch_bounds__(32 * kNearWarps, 8)
+#ifndef IFGF_NEAR_UNROLL
+#define IFGF_NEAR_UNROLL 2
+#endif
+#ifndef IFGF_NEAR_MINB
+#define IFGF_NEAR_MINB 8
+#endif
+constexpr int kNearUnroll = IFGF_NEAR_UNROLL;
+__global__ void __launch_bounds__(32 * kNearWarps, IFGF_NEAR_MINB)
 near_list_kernel(NearDev N, PointsDev P, const double2* __restrict__ a_p, double k, double2* __restrict__ Sp,
                  double2* __restrict__ Dp) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -227,15 +242,16 @@ near_list_kernel(NearDev N, PointsDev P, const double2* __restrict__ a_p, double
     const double x = P.x[t], y = P.y[t], z = P.z[t];
     double2 accS = make_double2(0.0, 0.0), accD = make_double2(0.0, 0.0);
     const std::int64_t e = N.list_off[t + 1];
+#pragma unroll kNearUnroll
     for (std::int64_t i = N.list_off[t] + lane; i < e; i += 32) {
         const int v = N.list_src[i];
-        pair_kernels(x, y, z, P.x[v], P.y[v], P.z[v], P.nx[v], P.ny[v], P.nz[v], a_p[v], k, 1.0, accS, accD);
+        near_pair(N.geo, v, x, y, z, a_p, k, 1.0, accS, accD);
     }
     const int p0 = int(N.tpb[l]), p1 = int(N.tpb[l + 1]);
     for (int p = p0; p < p1; ++p)
         for (std::uint32_t f = N.far_begin[p] + lane; f < N.far_end[p]; f += 32) {
             const int u = int(N.far_pos[f]);
-            pair_kernels(x, y, z, P.x[u], P.y[u], P.z[u], P.nx[u], P.ny[u], P.nz[u], a_p[u], k, -1.0, accS, accD);
+            near_pair(N.geo, u, x, y, z, a_p, k, -1.0, accS, accD);
         }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
