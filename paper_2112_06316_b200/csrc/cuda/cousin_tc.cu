@@ -8,8 +8,9 @@
 //   2. forms groups of lanes that evaluate the same segment (ballot on the ordinal), lists
 //      each group's lanes, loads the segment's B fragments once and runs 8-row DMMA tiles
 //      over the group (tc_common.cuh: 16 DMMAs per tile for 3 pipes, 12 for 2);
-//   3. applies the pipe factors (W1 -> S; W2 (1/r), W3 (-ik), W4 -> D), adds the D pipes of
-//      each evaluation (one shuffle) and accumulates into the target's shared accumulators.
+//   3. applies the pipe factors (W1 -> S; W2 (1/r), W3 (-ik), W4 -> D; formed per row in
+//      step 1), adds the D pipes of each evaluation (one shuffle) and accumulates into the
+//      target's shared accumulators.
 // Every target gets its cousins' contributions in cousin-list order: deterministic.
 #include "ifgf_device.cuh"
 #include "kernels.cuh"
@@ -23,7 +24,7 @@ using namespace ifgfdev;
 using namespace tc;
 
 constexpr int kThreads = 128, kWarps = kThreads / 32;
-constexpr int kCG = kRowLen + 4;  // A slots, T(phi), e1.re, e1.im, 1/r, pad (odd stride)
+constexpr int kCG = kRowLen + 6;  // A slots, T(phi), the pipe factors (3 complex) (odd stride)
 
 template <int NPC>
 __global__ void __launch_bounds__(kThreads, 4)
@@ -46,7 +47,6 @@ cousin_tc_kernel(LevelDev L, PointsDev P, const double2* __restrict__ store, dou
     const double x = P.x[t], y = P.y[t], z = P.z[t];
     const double h = L.h;
     sacc[warp][lane][0] = sacc[warp][lane][1] = make_double2(0.0, 0.0);
-    const int fpipe = tig < NPC ? pp.f[tig] : 0;  // factor code of the pipe this lane gathers
     // S comes from the W1 lane alone; D from the first D-pipe lane plus, for (W2, W3), its
     // right neighbour (pipe lists keep W2, W3 adjacent)
     int s_lane = -1, d_lane = -1, n_d = 0;
@@ -69,10 +69,17 @@ cousin_tc_kernel(LevelDev L, PointsDev P, const double2* __restrict__ store, dou
             double sn, cs;
             sincos_bounded(k * (r2 * inv_r), &sn, &cs);
             const double f1 = kInv4PiD * inv_r;
+            const double2 e1 = make_double2(cs * f1, sn * f1);  // e^{ikr}/(4 pi r)
             fill_row(lc.ls, lc.lt, lc.lp, mygeo);
-            mygeo[kRowLen] = cs * f1;  // e^{ikr}/(4 pi r)
-            mygeo[kRowLen + 1] = sn * f1;
-            mygeo[kRowLen + 2] = inv_r;
+            // per pipe: W1 -> S and W4 -> D take e1, W2 -> D e1/r, W3 -> D -ik e1
+#pragma unroll
+            for (int p = 0; p < NPC; ++p) {
+                double2 f = e1;
+                if (pp.f[p] == 2) f = cscale(e1, inv_r);
+                if (pp.f[p] == 3) f = make_double2(k * e1.y, -k * e1.x);
+                mygeo[kRowLen + 2 * p] = f.x;
+                mygeo[kRowLen + 2 * p + 1] = f.y;
+            }
         }
         __syncwarp();
         unsigned pending = __ballot_sync(0xffffffffu, act);
@@ -92,22 +99,15 @@ cousin_tc_kernel(LevelDev L, PointsDev P, const double2* __restrict__ store, dou
                 double d[LY::NQ][2];
                 tile_mma_row<NPC>(gp, valid, tig, bq, d);
                 const double2 val = tile_gather_row<NPC>(gp, lane, d);
-                const double2 w = cmul(make_double2(gp[kRowLen], gp[kRowLen + 1]), val);
-                double2 cS = make_double2(0.0, 0.0), cD = make_double2(0.0, 0.0);
-                switch (fpipe) {
-                    case 1: cS = w; break;
-                    case 2: cD = cscale(w, gp[kRowLen + 2]); break;
-                    case 3: cD = make_double2(k * w.y, -k * w.x); break;  // -ik e^{ikr}/(4 pi r) val
-                    case 4: cD = w; break;
-                    default: break;
+                const int fp = tig < NPC ? tig : 0;
+                double2 w = cmul(make_double2(gp[kRowLen + 2 * fp], gp[kRowLen + 2 * fp + 1]), val);
+                if (n_d == 2) {  // (W2, W3): the second D pipe joins the first
+                    const double ox = __shfl_down_sync(0xffffffffu, w.x, 1);
+                    const double oy = __shfl_down_sync(0xffffffffu, w.y, 1);
+                    if (tig == d_lane) w = make_double2(w.x + ox, w.y + oy);
                 }
-                if (n_d == 2) {
-                    const double ox = __shfl_down_sync(0xffffffffu, cD.x, 1);
-                    const double oy = __shfl_down_sync(0xffffffffu, cD.y, 1);
-                    cD = make_double2(cD.x + ox, cD.y + oy);
-                }
-                if (valid && tig == s_lane) sacc[warp][src][0] = cadd(sacc[warp][src][0], cS);
-                if (valid && tig == d_lane) sacc[warp][src][1] = cadd(sacc[warp][src][1], cD);
+                if (valid && tig == s_lane) sacc[warp][src][0] = cadd(sacc[warp][src][0], w);
+                if (valid && tig == d_lane) sacc[warp][src][1] = cadd(sacc[warp][src][1], w);
             }
             __syncwarp();
         }
