@@ -34,7 +34,8 @@ constexpr int kWarps = 4;
 #ifndef IFGF_PARENT_MINB
 #define IFGF_PARENT_MINB 4
 #endif
-constexpr int kRow = kRowLen + 4;     // A slots, T(phi), ratio.re, ratio.im, extra factor, node (odd)
+constexpr int kRow = kRowLen + 8;     // A slots, T(phi), per child pipe its factor (3 complex), node, pad (odd)
+constexpr int kNode = kRowLen + 6;
 constexpr int kGeoSz = 32 * kRow;      // one chunk of 32 evaluation rows per warp (even: the
                                        // accumulators behind it stay 16-byte aligned)
 
@@ -177,10 +178,21 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
                 }
                 double* row = geo + lane * kRow;
                 fill_row(ls, lt, lp, row);
-                row[kRowLen] = r1x;
-                row[kRowLen + 1] = r1y;
-                row[kRowLen + 2] = xf;
-                row[kRowLen + 3] = double(node);
+                // per child pipe: ratio1 times 1 (R1), -ik (MK) or the extra factor (RI, RQ)
+#pragma unroll
+                for (int pc = 0; pc < NPC; ++pc) {
+                    double fx = r1x, fy = r1y;
+                    if (CB::fac(pc) == MK) {
+                        fx = k * r1y;
+                        fy = -k * r1x;
+                    } else if (CB::fac(pc) != R1) {
+                        fx = r1x * xf;
+                        fy = r1y * xf;
+                    }
+                    row[kRowLen + 2 * pc] = fx;
+                    row[kRowLen + 2 * pc + 1] = fy;
+                }
+                row[kNode] = double(node);
             }
             __syncwarp();
             // 2. 8-evaluation tensor-core tiles against the child block (issuing the next
@@ -194,21 +206,8 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
                 const double* gp = geo + (valid ? t0 + r : 0) * kRow;
                 const double2 val = tile_gather_row<NPC>(gp, lane, d);
                 // lanes tig < NPC now hold (re, im) of child pipe tig for evaluation row r
-                const double2 r1 = make_double2(gp[kRowLen], gp[kRowLen + 1]);
-                const double xf = gp[kRowLen + 2];
-                int fac = R1;
-#pragma unroll
-                for (int pc = 0; pc < NPC; ++pc)
-                    if (tig == pc) fac = CB::fac(pc);
-                double2 ctb;
-                if (fac == R1) {
-                    ctb = cmul(r1, val);
-                } else if (fac == MK) {
-                    const double2 w = cmul(r1, val);
-                    ctb = make_double2(k * w.y, -k * w.x);
-                } else {  // RI or RQ: ratio1 times the stored extra factor
-                    ctb = cmul(cscale(r1, xf), val);
-                }
+                const int fp = tig < NPC ? tig : 0;
+                double2 ctb = cmul(make_double2(gp[kRowLen + 2 * fp], gp[kRowLen + 2 * fp + 1]), val);
                 if constexpr (COMBO == 0) {  // child W2, W3 -> parent W4: sum across the quad
                     const double ox = __shfl_down_sync(0xffffffffu, ctb.x, 1);
                     const double oy = __shfl_down_sync(0xffffffffu, ctb.y, 1);
@@ -226,7 +225,7 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
 #pragma unroll
                     for (int pc = 0; pc < NPC; ++pc)
                         if (tig == pc) dst = CB::dst(pc);
-                    double2& a = acc[int(gp[kRowLen + 3]) * NPP + dst];
+                    double2& a = acc[int(gp[kNode]) * NPP + dst];
                     a = cadd(a, ctb);
                 }
             };
