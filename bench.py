@@ -214,8 +214,8 @@ def roofline_for(phases, work, pk):
     return out
 
 
-KERNEL_FAMILY = {"leaf": "leaf_ray_kernel", "cousin": "cousin_kernel", "parent": "parent_tc_kernel",
-                 "near": "near_kernel", "rp": "rp_combine_kernel"}
+KERNEL_FAMILY = {"leaf": "leaf_ray_kernel", "cousin": "cousin_tc_kernel", "parent": "parent_tc_kernel",
+                 "near": "near_list_kernel", "rp": "rp_accum_kernel"}
 
 
 def ncu_traffic(cfg_name, phase):
