@@ -11,6 +11,8 @@ struct PointsDev {
     const double *nx, *ny, *nz;
 };
 
+constexpr int kParentMergeMax = 2;  // parent segments per warp item (IFGF_PARENT_MERGE <= this; 3 measured slower)
+
 struct LevelDev {
     int d = 0;
     int nb = 0;      // boxes at this level
@@ -33,11 +35,17 @@ struct LevelDev {
     const std::uint16_t* pev_perm = nullptr;  // evaluations grouped by child segment
     const std::int32_t *pgrp_begin = nullptr, *pgrp_seg = nullptr;
     const std::uint16_t *pgrp_start = nullptr, *pgrp_count = nullptr;
-    // the same groups packed for the tensor-core parent kernel (one 16-byte load per group):
-    // {child segment, child box, start | count << 16 | child octant << 24, cell of the child
-    // segment (seg_code layout when seg_code is set, else gamma)}; the evaluations of
-    // pev_perm carry bit 15 when the parent's geometry template applies (host-checked)
+    // tensor-core parent kernel work (engine.cu "parent work items"): per item up to
+    // kParentMergeMax parent segments of one box (-1: none), its merged groups
+    // [pitem_grp[i], pitem_grp[i + 1]) of pgrp_rec = {child segment, child box, start |
+    // count << 16 | child octant << 24, cell of the child segment (seg_code layout when
+    // seg_code is set, else gamma)} and its evaluations from pev_perm + pitem_ev[i] (node |
+    // child slot << 8 | item-local segment << 11 | template bit << 15)
     const int4* pgrp_rec = nullptr;
+    const std::int32_t *pitem_seg = nullptr, *pitem_grp = nullptr;
+    const std::int64_t* pitem_ev = nullptr;
+    int n_pitem = 0;
+    int pitem_merge = 1;  // segments per item (accumulator blocks per warp)
     const std::int32_t *ch_ptr = nullptr, *ch_idx = nullptr;  // children (level d+1) of this level's boxes
     const double *s_nodes = nullptr, *th_nodes = nullptr, *ph_nodes = nullptr;
     // sin/cos of the angular node tables (interpolation-node directions)

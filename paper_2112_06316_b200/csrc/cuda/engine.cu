@@ -10,6 +10,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
+#include <atomic>
 #include <type_traits>
 #include <cstdlib>
 #include <string>
@@ -74,7 +76,7 @@ struct LevelBufs {
     DevBuf cx, cy, cz, beg, end, cz_ptr, cz_idx, cev_begin, cev_seg, seg_box, seg_gamma,
         box_seg_begin, pev_begin, pev_seg, pev_perm, pgrp_begin, pgrp_seg, pgrp_start, pgrp_count, ch_ptr, ch_idx, s_nodes, th_nodes, ph_nodes, th_sin, th_cos, ph_sin, ph_cos, thc_cos, thc_sin, phc_cos, phc_sin,
         chunk_box, chunk_q0, wchunk_box, wchunk_q0, tmpl_slot, tmpl, seg_code, litem_seg0,
-        litem_nseg, litem_split, litem_box0, litem_box1, pgrp_rec;
+        litem_nseg, litem_split, litem_box0, litem_box1, pgrp_rec, pitem_seg, pitem_grp, pitem_ev;
 };
 
 Pipes make_pipes(const std::vector<int>& f) {
@@ -745,54 +747,128 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         }
     }
 
-    // ---- packed parent groups (tensor-core parent kernel): one record per group and the
-    // template bit of every evaluation, so the kernel's per-group and per-chunk loads do not
-    // chain through pev_perm -> ch_idx / seg_gamma -> cell tables / tmpl_gc
-    for (int d = 4; d <= T.depth; ++d) {
-        const ConeLevel& PL = C.level[d - 2];
-        const ConeLevel& CL = C.level[d - 1];
-        if (PL.ps != 3 || PL.pang != 5 || CL.ps != 3 || CL.pang != 5 || CL.pgrp_begin.empty()) continue;
-        const auto& cptr = C.child_ptr[d - 2];
-        const auto& cidx = C.child_idx[d - 2];
-        const std::vector<std::int32_t>& slot = tmpl_slot_h[d];
-        const std::vector<std::int32_t>& gc = tmpl_gc_h[d];
-        const bool packed = e.L[d - 1].seg_code != nullptr;
-        std::vector<int4> rec(CL.pgrp_seg.size());
-        std::vector<std::uint16_t> perm(CL.pev_perm);
-#pragma omp parallel for schedule(dynamic, 1024)
-        for (std::int64_t so = 0; so < std::int64_t(PL.nseg()); ++so) {
-            const int pb = PL.seg_box[so];
-            const std::int64_t ev0 = CL.pev_begin[so];
-            const int tslot = slot.empty() ? -1 : slot[PL.seg_gamma[so]];
-            const Vec3 pc = T.center(d - 1, std::size_t(pb));
-            for (int g = CL.pgrp_begin[so]; g < CL.pgrp_begin[so + 1]; ++g) {
-                const int start = CL.pgrp_start[g], count = CL.pgrp_count[g];
-                if (count > 255) throw InternalError("parent groups: more than 255 evaluations in one group");
-                const int c = (CL.pev_perm[ev0 + start] >> 8) & 7;
-                const int ch = cidx[cptr[pb] + c];
-                const int cso = CL.pgrp_seg[g];
-                const int cgam = CL.seg_gamma[cso];
-                int cell = cgam;
-                if (packed) {
-                    const int g1 = cgam % CL.ns, rest = cgam / CL.ns;
-                    cell = int(std::uint32_t(g1) | (std::uint32_t(rest % CL.nc) << 8) | (std::uint32_t(rest / CL.nc) << 19));
+    // ---- parent work items (tensor-core parent kernel): up to `merge` relevant segments of one
+    // parent box per warp (IFGF_PARENT_MERGE, default 2), with their child-segment groups merged
+    // so that evaluations of the item's segments that land in the same child segment share
+    // DMMA tiles. One 16-byte record per merged group {child segment, child box, start |
+    // count << 16 | child octant << 24, packed cell} and per evaluation its node | child slot
+    // << 8 | item-local segment << 11 | template bit << 15, so the kernel's loads do not chain
+    // through pev_perm -> ch_idx / seg_gamma -> cell tables -> template cells. Within a merged
+    // group the evaluations keep their segments' group order, so every node accumulator sees
+    // the same additions in the same order as with one segment per warp.
+    {
+        const char* menv = std::getenv("IFGF_PARENT_MERGE");
+        const int merge = std::clamp(menv ? std::atoi(menv) : 2, 1, kParentMergeMax);
+        for (int d = 4; d <= T.depth; ++d) {
+            const ConeLevel& PL = C.level[d - 2];
+            const ConeLevel& CL = C.level[d - 1];
+            if (PL.ps != 3 || PL.pang != 5 || CL.ps != 3 || CL.pang != 5 || CL.pgrp_begin.empty()) continue;
+            const auto& cptr = C.child_ptr[d - 2];
+            const auto& cidx = C.child_idx[d - 2];
+            const std::vector<std::int32_t>& slot = tmpl_slot_h[d];
+            const std::vector<std::int32_t>& gc = tmpl_gc_h[d];
+            const bool packed = e.L[d - 1].seg_code != nullptr;
+            auto cell_of = [&](int gam, const ConeLevel& L) {
+                if (!packed) return gam;
+                const int g1 = gam % L.ns, rest = gam / L.ns;
+                return int(std::uint32_t(g1) | (std::uint32_t(rest % L.nc) << 8) | (std::uint32_t(rest / L.nc) << 19));
+            };
+            // items: consecutive relevant segments of one parent box
+            std::vector<std::int32_t> item_seg;
+            for (std::size_t pb = 0; pb + 1 < PL.box_seg_begin.size(); ++pb)
+                for (int s0 = PL.box_seg_begin[pb]; s0 < PL.box_seg_begin[pb + 1]; s0 += merge)
+                    for (int w = 0; w < kParentMergeMax; ++w)
+                        item_seg.push_back(w < merge && s0 + w < PL.box_seg_begin[pb + 1] ? s0 + w : -1);
+            const std::int64_t n_item = std::int64_t(item_seg.size()) / kParentMergeMax;
+            // an item's groups: (child segment, item-local segment, group), ordered by child
+            // segment, then segment (stable)
+            auto item_groups = [&](std::int64_t it, std::vector<std::array<int, 3>>& v) {
+                v.clear();
+                for (int w = 0; w < kParentMergeMax; ++w) {
+                    const int so = item_seg[it * kParentMergeMax + w];
+                    if (so < 0) continue;
+                    for (int g = CL.pgrp_begin[so]; g < CL.pgrp_begin[so + 1]; ++g) v.push_back({CL.pgrp_seg[g], w, g});
                 }
-                const Vec3 cc = T.center(d, std::size_t(ch));
-                const int oct = (cc.x > pc.x ? 1 : 0) | (cc.y > pc.y ? 2 : 0) | (cc.z > pc.z ? 4 : 0);
-                rec[g] = make_int4(cso, ch, start | (count << 16) | (oct << 24), cell);
-                if (tslot < 0) continue;
-                const std::size_t tbase = (std::size_t(tslot) * 8 + oct) * 75;
-                for (int i = start; i < start + count; ++i) {
-                    std::uint16_t& ent = perm[ev0 + i];
-                    if (gc[tbase + (ent & 0xff)] == cgam) ent = std::uint16_t(ent | 0x8000u);
+                std::stable_sort(v.begin(), v.end(), [](const auto& a, const auto& b) { return a[0] < b[0]; });
+            };
+            std::vector<std::int64_t> ig(n_item + 1, 0), ie(n_item + 1, 0);
+#pragma omp parallel
+            {
+                std::vector<std::array<int, 3>> v;
+#pragma omp for schedule(dynamic, 256)
+                for (std::int64_t it = 0; it < n_item; ++it) {
+                    item_groups(it, v);
+                    std::int64_t ng = 0, nev = 0;
+                    for (std::size_t x = 0; x < v.size(); ++x) {
+                        if (x == 0 || v[x][0] != v[x - 1][0]) ++ng;
+                        nev += CL.pgrp_count[v[x][2]];
+                    }
+                    ig[it + 1] = ng;
+                    ie[it + 1] = nev;
                 }
             }
+            for (std::int64_t it = 0; it < n_item; ++it) {
+                ig[it + 1] += ig[it];
+                ie[it + 1] += ie[it];
+            }
+            std::vector<int4> rec(static_cast<std::size_t>(ig[n_item]));
+            std::vector<std::uint16_t> perm(static_cast<std::size_t>(ie[n_item]));
+            std::atomic<bool> too_big{false};
+#pragma omp parallel
+            {
+                std::vector<std::array<int, 3>> v;
+#pragma omp for schedule(dynamic, 256)
+                for (std::int64_t it = 0; it < n_item; ++it) {
+                    item_groups(it, v);
+                    const int pb = PL.seg_box[item_seg[it * kParentMergeMax]];
+                    const Vec3 pc = T.center(d - 1, std::size_t(pb));
+                    std::int64_t gi = ig[it];
+                    int at = 0;  // item-local evaluation index
+                    for (std::size_t x = 0; x < v.size();) {
+                        const int cso = v[x][0];
+                        const int start = at;
+                        const int c = (CL.pev_perm[CL.pev_begin[item_seg[it * kParentMergeMax + v[x][1]]] +
+                                                   CL.pgrp_start[v[x][2]]] >> 8) & 7;
+                        const int ch = cidx[cptr[pb] + c];
+                        const int cgam = CL.seg_gamma[cso];
+                        const Vec3 cc = T.center(d, std::size_t(ch));
+                        const int oct = (cc.x > pc.x ? 1 : 0) | (cc.y > pc.y ? 2 : 0) | (cc.z > pc.z ? 4 : 0);
+                        for (; x < v.size() && v[x][0] == cso; ++x) {
+                            const int w = v[x][1], g = v[x][2];
+                            const int so = item_seg[it * kParentMergeMax + w];
+                            const std::int64_t ev0 = CL.pev_begin[so];
+                            const int tslot = slot.empty() ? -1 : slot[PL.seg_gamma[so]];
+                            const std::size_t tbase = (std::size_t(std::max(tslot, 0)) * 8 + oct) * 75;
+                            for (int i = CL.pgrp_start[g]; i < CL.pgrp_start[g] + CL.pgrp_count[g]; ++i) {
+                                std::uint16_t ent = std::uint16_t((CL.pev_perm[ev0 + i] & 0x7ffu) | (w << 11));  // w < 2
+                                if (tslot >= 0 && gc[tbase + (ent & 0xff)] == cgam) ent = std::uint16_t(ent | 0x8000u);
+                                perm[std::size_t(ie[it] + at++)] = ent;
+                            }
+                        }
+                        const int count = at - start;
+                        if (count > 255 || at > 65535) too_big = true;
+                        rec[std::size_t(gi++)] = make_int4(cso, ch, start | (count << 16) | (oct << 24), cell_of(cgam, CL));
+                    }
+                }
+            }
+            if (too_big) throw InternalError("parent items: more than 255 evaluations in one merged group");
+            std::vector<std::int32_t> igr(ig.begin(), ig.end());
+            LevelBufs& b = e.lb[d - 1];
+            b.pgrp_rec.upload(rec);
+            b.pev_perm.upload(perm);
+            b.pitem_seg.upload(item_seg);
+            b.pitem_grp.upload(igr);
+            b.pitem_ev.upload(ie);
+            LevelDev& L = e.L[d - 1];
+            L.pgrp_rec = b.pgrp_rec.as<int4>();
+            L.pev_perm = b.pev_perm.as<std::uint16_t>();
+            L.pitem_seg = b.pitem_seg.as<std::int32_t>();
+            L.pitem_grp = b.pitem_grp.as<std::int32_t>();
+            L.pitem_ev = b.pitem_ev.as<std::int64_t>();
+            L.n_pitem = int(n_item);
+            L.pitem_merge = merge;
+            if (ig[n_item] > std::int64_t(INT32_MAX)) throw InternalError("parent items: too many groups");
         }
-        LevelBufs& b = e.lb[d - 1];
-        b.pgrp_rec.upload(rec);
-        b.pev_perm.upload(perm);
-        e.L[d - 1].pgrp_rec = b.pgrp_rec.as<int4>();
-        e.L[d - 1].pev_perm = b.pev_perm.as<std::uint16_t>();
     }
 
     // ---- near field

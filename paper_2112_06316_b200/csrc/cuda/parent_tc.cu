@@ -91,30 +91,34 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
     constexpr int NPP = CB::npp, NPC = CB::npc;
     extern __shared__ double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int so = blockIdx.x * kWarps + warp;  // one warp per parent segment
-    if (so >= Lp.nseg) return;
-    double* geo = smem + warp * (kGeoSz + 2 * kNP * NPP);                       // per warp
-    double2* acc = reinterpret_cast<double2*>(geo + kGeoSz);                   // 75 x NPP
-    for (int e = lane; e < kNP * NPP; e += 32) acc[e] = make_double2(0.0, 0.0);
-
-    const int pb = Lp.seg_box[so];
+    const int merge = Lc.pitem_merge;
+    double* geo = smem + warp * (kGeoSz + 2 * kNP * NPP * merge);  // per warp
+    double2* acc = reinterpret_cast<double2*>(geo + kGeoSz);  // per item segment: 75 x NPP
+    const int item = blockIdx.x * kWarps + warp;  // one warp per work item
+    if (item >= Lc.n_pitem) return;
+    const int* __restrict__ iseg = Lc.pitem_seg + item * kParentMergeMax;
+    int segs[kParentMergeMax], tsl[kParentMergeMax], pcode[kParentMergeMax];
+    const int pb = Lp.seg_box[iseg[0]];
     if (Lp.active && !Lp.active[pb]) return;  // no sources of this rank below
-    const int gam = Lp.seg_gamma[so];
-    const int g1 = gam % Lp.ns, g2 = (gam / Lp.ns) % Lp.nc, g3 = gam / Lp.ns / Lp.nc;
-    const int c0 = Lp.ch_ptr[pb];
-    const int tslot = Lp.tmpl_slot ? Lp.tmpl_slot[gam] : -1;
-    const std::int64_t ev0 = Lc.pev_begin[so];
+#pragma unroll
+    for (int w = 0; w < kParentMergeMax; ++w) {
+        segs[w] = iseg[w];
+        const int gam = segs[w] >= 0 ? Lp.seg_gamma[segs[w]] : 0;
+        tsl[w] = Lp.tmpl_slot && segs[w] >= 0 ? Lp.tmpl_slot[gam] : -1;
+        pcode[w] = (gam % Lp.ns) | (((gam / Lp.ns) % Lp.nc) << 8) | ((gam / Lp.ns / Lp.nc) << 19);
+    }
+    for (int e = lane; e < kNP * NPP * merge; e += 32) acc[e] = make_double2(0.0, 0.0);
     const double hp = Lp.h, hc = Lc.h;
     const double pcx = Lp.cx[pb], pcy = Lp.cy[pb], pcz = Lp.cz[pb];
 
     const int r = lane >> 2, tig = lane & 3;
     using LY = Layout<NPC>;
-    const int gb = Lc.pgrp_begin[so], ge = Lc.pgrp_begin[so + 1];
+    const int gb = Lc.pitem_grp[item], ge = Lc.pitem_grp[item + 1];
     // group records (host-packed: child segment, child box, start | count << 16 | child
-    // octant << 24, cell) run two groups ahead and the first pev_perm entries one group ahead,
-    // so a group's template loads issue at its start without a dependent-load chain
+    // octant << 24, cell) run two groups ahead and the first evaluation entries one group
+    // ahead, so a group's template loads issue at its start without a dependent-load chain
     const int4* __restrict__ grec = Lc.pgrp_rec;
-    const std::uint16_t* __restrict__ perm = Lc.pev_perm + ev0;
+    const std::uint16_t* __restrict__ perm = Lc.pev_perm + Lc.pitem_ev[item];
     const int4 zero4 = make_int4(0, 0, 0, 0);
     int4 rec1 = gb < ge ? grec[gb] : zero4;
     int4 rec2 = gb + 1 < ge ? grec[gb + 1] : zero4;
@@ -130,20 +134,24 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
         if (Lc.active && !Lc.active[ch]) continue;  // child holds no sources of this rank
         const double ccx = Lc.cx[ch], ccy = Lc.cy[ch], ccz = Lc.cz[ch];
         const CellFrame cf = Lc.seg_code ? cell_frame_code(unsigned(rec.w), Lc) : cell_frame(rec.w, Lc);
-        // geometry template of (parent cell, child octant), host/coneplan.hpp parent_templates
-        const std::size_t tbase = (std::size_t(tslot) * 8 + oct) * kNP;
         // B fragments of the group's block, reused by all its tiles (tc_common.cuh)
         double bq[LY::NB];
         load_b<NPC>(cstore + std::size_t(cso) * NPC * kNP, lane, bq);
         for (int e0 = 0; e0 < count; e0 += 32) {  // chunks of 32 evaluations, one per lane
             const int cn = min(32, count - e0);
             if (lane < cn) {
-                // entries are node | c << 8, bit 15: the template applies (engine.cu)
+                // entries are node | c << 8 | item segment << 11, bit 15: the template applies
                 const unsigned ent = e0 == 0 ? ent_first : perm[start + e0 + lane];
-                const int node = int(ent & 0xffu);
+                const int node = int(ent & 0xffu), ws = int((ent >> 11) & 1u);
+                int tslot = tsl[0], code = pcode[0];
+#pragma unroll
+                for (int w = 1; w < kParentMergeMax; ++w)
+                    if (ws == w) tslot = tsl[w], code = pcode[w];
                 double ls, lt, lp, r1x, r1y, xf;
                 if (ent & 0x8000u) {
-                    const double2* te = reinterpret_cast<const double2*>(Lp.tmpl + (tbase + node) * 8);
+                    // geometry template of (parent cell, child octant, node), host/coneplan.hpp
+                    const std::size_t tent = (std::size_t(tslot) * 8 + oct) * kNP + node;
+                    const double2* te = reinterpret_cast<const double2*>(Lp.tmpl + tent * 8);
                     const double2 t0 = __ldg(te), t1 = __ldg(te + 1), t2 = __ldg(te + 2), t3 = __ldg(te + 3);
                     ls = t0.x;
                     lt = t0.y;
@@ -153,6 +161,7 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
                     xf = CB::extra == RI ? t2.y : t3.x;
                 } else {
                     const int is = node % kPS, it = (node / kPS) % kPA, ip = node / (kPS * kPA);
+                    const int g1 = code & 0xff, g2 = (code >> 8) & 0x7ff, g3 = code >> 19;
                     const double s = Lp.s_nodes[g1 * kPS + is];
                     const double rp = hp / s;
                     const double sth = Lp.th_sin[g2 * kPA + it], cth = Lp.th_cos[g2 * kPA + it];
@@ -192,7 +201,7 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
                     row[kRowLen + 2 * pc] = fx;
                     row[kRowLen + 2 * pc + 1] = fy;
                 }
-                row[kNode] = double(node);
+                row[kNode] = double(node + kNP * ws);  // accumulator row of (segment, node)
             }
             __syncwarp();
             // 2. 8-evaluation tensor-core tiles against the child block (issuing the next
@@ -237,36 +246,40 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
             __syncwarp();
         }
     }
-    // values -> coefficients (transform3, ifgf.cpp:560-562), warp-local
-    double2* v0 = acc;
-    double2* v1 = reinterpret_cast<double2*>(geo);
-    double2* dst = pstore + std::size_t(so) * NPP * kNP;
-    // acc is node-major (node * NPP + i); transpose into pipe-major blocks while applying
-    // the s-direction transform, then theta, then phi
-    for (int e = lane; e < NPP * kNP; e += 32) {
-        const int blk = e / kNP, node = e % kNP;
-        const int is = node % kPS, line = node / kPS;
-        double2 a = make_double2(0.0, 0.0);
-        for (int q = 0; q < kPS; ++q) cfma_r(a, v0[(line * kPS + q) * NPP + blk], Ms[is * kPS + q]);
-        v1[e] = a;
-    }
-    __syncwarp();
-    for (int e = lane; e < NPP * kNP; e += 32) {
-        const int blk = e / kNP, node = e % kNP;
-        const int is = node % kPS, it = (node / kPS) % kPA, ip = node / (kPS * kPA);
-        const double2* src = v1 + blk * kNP + is + kPS * kPA * ip;
-        double2 a = make_double2(0.0, 0.0);
-        for (int q = 0; q < kPA; ++q) cfma_r(a, src[kPS * q], Ma[it * kPA + q]);
-        v0[e] = a;
-    }
-    __syncwarp();
-    for (int e = lane; e < NPP * kNP; e += 32) {
-        const int blk = e / kNP, node = e % kNP;
-        const int is = node % kPS, it = (node / kPS) % kPA, ip = node / (kPS * kPA);
-        const double2* src = v0 + blk * kNP + is + kPS * it;
-        double2 a = make_double2(0.0, 0.0);
-        for (int q = 0; q < kPA; ++q) cfma_r(a, src[kPS * kPA * q], Ma[ip * kPA + q]);
-        dst[e] = a;
+    // values -> coefficients (transform3, ifgf.cpp:560-562), warp-local, per item segment
+    for (int w = 0; w < kParentMergeMax; ++w) {
+        if (segs[w] < 0) break;
+        __syncwarp();
+        double2* v0 = acc + w * kNP * NPP;
+        double2* v1 = reinterpret_cast<double2*>(geo);
+        double2* dst = pstore + std::size_t(segs[w]) * NPP * kNP;
+        // acc is node-major (node * NPP + i); transpose into pipe-major blocks while applying
+        // the s-direction transform, then theta, then phi
+        for (int e = lane; e < NPP * kNP; e += 32) {
+            const int blk = e / kNP, node = e % kNP;
+            const int is = node % kPS, line = node / kPS;
+            double2 a = make_double2(0.0, 0.0);
+            for (int q = 0; q < kPS; ++q) cfma_r(a, v0[(line * kPS + q) * NPP + blk], Ms[is * kPS + q]);
+            v1[e] = a;
+        }
+        __syncwarp();
+        for (int e = lane; e < NPP * kNP; e += 32) {
+            const int blk = e / kNP, node = e % kNP;
+            const int is = node % kPS, it = (node / kPS) % kPA, ip = node / (kPS * kPA);
+            const double2* src = v1 + blk * kNP + is + kPS * kPA * ip;
+            double2 a = make_double2(0.0, 0.0);
+            for (int q = 0; q < kPA; ++q) cfma_r(a, src[kPS * q], Ma[it * kPA + q]);
+            v0[e] = a;
+        }
+        __syncwarp();
+        for (int e = lane; e < NPP * kNP; e += 32) {
+            const int blk = e / kNP, node = e % kNP;
+            const int is = node % kPS, it = (node / kPS) % kPA, ip = node / (kPS * kPA);
+            const double2* src = v0 + blk * kNP + is + kPS * it;
+            double2 a = make_double2(0.0, 0.0);
+            for (int q = 0; q < kPA; ++q) cfma_r(a, src[kPS * kPA * q], Ma[ip * kPA + q]);
+            dst[e] = a;
+        }
     }
 }
 
@@ -293,14 +306,15 @@ bool launch_parent_fill_tc(const LevelDev& Lp, const LevelDev& Lc, const double2
                            const Pipes& parent_pipes, const Pipes& child_pipes, const double* Ms,
                            const double* Ma, double2* parent_store, cudaStream_t st) {
     const int combo = combo_of(parent_pipes, child_pipes);
-    if (combo < 0 || Lp.ps != kPS || Lp.pang != kPA || Lc.ps != kPS || Lc.pang != kPA || !Lc.pgrp_rec ||
+    if (combo < 0 || Lp.ps != kPS || Lp.pang != kPA || Lc.ps != kPS || Lc.pang != kPA || !Lc.pitem_grp ||
         !Lp.th_sin)
         return false;
-    if (Lp.nseg == 0) return true;
-    const std::size_t smem = std::size_t(kWarps) * (kGeoSz + 2 * kNP * parent_pipes.n) * sizeof(double);
+    if (Lc.n_pitem == 0) return true;
+    const std::size_t smem =
+        std::size_t(kWarps) * (kGeoSz + 2 * kNP * parent_pipes.n * Lc.pitem_merge) * sizeof(double);
     auto go = [&](auto kern) {
         IFGF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        kern<<<(Lp.nseg + kWarps - 1) / kWarps, 32 * kWarps, smem, st>>>(Lp, Lc, child_store, k, Ms, Ma, parent_store);
+        kern<<<(Lc.n_pitem + kWarps - 1) / kWarps, 32 * kWarps, smem, st>>>(Lp, Lc, child_store, k, Ms, Ma, parent_store);
     };
     switch (combo) {
         case 0: go(parent_tc_kernel<0>); break;

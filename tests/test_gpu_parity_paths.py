@@ -56,6 +56,20 @@ def test_near_lists_bitwise(monkeypatch, splits, nu, k):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("splits,nu,k", [(2, 6, 4 * np.pi), (3, 8, 8 * np.pi)])
+def test_parent_merge_bitwise(monkeypatch, splits, nu, k):
+    # merged parent work items (IFGF_PARENT_MERGE segments per warp) share DMMA tiles between
+    # segments but add into every node accumulator in the same order: bitwise equal output
+    pm = P.SurfaceMesh.sphere(1.0, splits, nu, nu)
+    phi = P.random_density(pm.size(), 5)
+    out = []
+    for m in ("1", "2"):
+        monkeypatch.setenv("IFGF_PARENT_MERGE", m)
+        out.append(P.CombinedOperator(pm, P.SolveConfig(k=k)).layer_potentials(phi))
+    for o in out[1:]:
+        assert np.array_equal(o[0], out[0][0]) and np.array_equal(o[1], out[0][1])
+
+
 @pytest.mark.parametrize("axes,k", [((4.0, 1.0, 1.0), 2 * np.pi), ((2.5, 0.6, 1.2), 3 * np.pi)])
 def test_spheroid_parity(ref, axes, k):
     pm = P.SurfaceMesh.spheroid(2, 8, 8, *axes)
