@@ -10,6 +10,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <array>
 #include <atomic>
 #include <type_traits>
@@ -713,7 +714,7 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
     e.Ms.upload(cheb::transform(e.ps));
     e.Ma.upload(cheb::transform(e.pang));
 
-    // ---- parent-fill geometry templates on every level whose table is at most 4 GiB and has
+    // ---- parent-fill geometry templates on every level whose table is at most 8 GiB and has
     // no more entries than the level has evaluations (measured: templates on every level beat
     // building them only where each entry serves >= 8 evaluations, cfg2 8.97 -> 8.69 ms,
     // cfg3 271 -> 260 ms of parent fill); IFGF_PARENT_TEMPLATES=0 turns them off, =force
@@ -734,7 +735,10 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
                     gammas.push_back(g);
                 }
             const std::size_t entries = gammas.size() * 8 * std::size_t(PL.nodes_per_seg());
-            if (!force && (entries > CL.pev_perm.size() || entries * 64 > (std::size_t(4) << 30))) continue;
+            if (std::getenv("IFGF_TMPL_DEBUG"))
+                std::fprintf(stderr, "templates level %d: entries %zu evaluations %zu (%.2f GB)\n", d, entries,
+                             CL.pev_perm.size(), entries * 64 / 1e9);
+            if (!force && (entries > CL.pev_perm.size() || entries * 64 > (std::size_t(8) << 30))) continue;
             std::vector<double> tab;
             std::vector<std::int32_t> gc;
             parent_templates(T, C, d, gammas, 0, tab, gc);
