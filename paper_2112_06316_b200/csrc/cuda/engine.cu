@@ -304,6 +304,8 @@ struct Engine::Impl {
         const std::size_t bytes = std::size_t(off.back()) * sizeof(std::int32_t) + off.size() * sizeof(std::int64_t);
         std::size_t free_b = 0, total_b = 0;
         IFGF_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        if (std::getenv("IFGF_SETUP_DEBUG"))
+            std::fprintf(stderr, "near lists: %.2f GB, free %.2f GB\n", bytes / 1e9, free_b / 1e9);
         if (bytes > free_b / 4) return;
         near_off.upload(off);
         near_src.alloc(std::max<std::size_t>(std::size_t(off.back()), 1) * sizeof(std::int32_t));
@@ -735,7 +737,7 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
                     gammas.push_back(g);
                 }
             const std::size_t entries = gammas.size() * 8 * std::size_t(PL.nodes_per_seg());
-            if (std::getenv("IFGF_TMPL_DEBUG"))
+            if (std::getenv("IFGF_SETUP_DEBUG"))
                 std::fprintf(stderr, "templates level %d: entries %zu evaluations %zu (%.2f GB)\n", d, entries,
                              CL.pev_perm.size(), entries * 64 / 1e9);
             if (!force && (entries > CL.pev_perm.size() || entries * 64 > (std::size_t(8) << 30))) continue;
