@@ -135,3 +135,25 @@ def test_per_rank_plans_partition_the_full_plan():
     assert bounds[0][0] == 0 and bounds[0][-1] == n
     with pytest.raises(P.InvalidArgument):
         plan_partition(parts[0], world + 1)
+
+
+@pytest.mark.parametrize("splits,nu,k", [(1, 6, 4 * np.pi), (1, 8, 8 * np.pi), (2, 4, 8 * np.pi)])
+def test_pair_accounting_each_pair_at_one_level(splits, nu, k):
+    # every (target, source) pair is covered exactly once: by the leaf neighbour scope (near
+    # field, self pairs included) or by one cousin list at one level (the reference's
+    # "pair accounting: each far pair at exactly one level", test_ifgf.cpp:197-233)
+    mesh = P.SurfaceMesh.sphere(1.0, splits, nu, nu)
+    hp = P.HostPlan(mesh, P.SolveConfig(k=k))
+    assert hp.depth >= 4
+    n = mesh.size()
+    count = np.zeros((n, n), dtype=np.int32)  # Morton x Morton
+    for d in range(3, hp.depth + 1):
+        bx = hp.boxes(d)
+        kinds = [1] if d < hp.depth else [0, 1]  # neighbours only at the leaf level
+        for which in kinds:
+            ptr, idx = hp.relation(d, which)
+            for b in range(len(ptr) - 1):
+                b0, b1 = bx["begin"][b], bx["end"][b]
+                for j in idx[ptr[b]:ptr[b + 1]]:
+                    count[b0:b1, bx["begin"][j]:bx["end"][j]] += 1
+    assert count.min() == 1 and count.max() == 1
