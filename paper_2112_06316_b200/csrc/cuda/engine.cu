@@ -860,6 +860,15 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
                 }
             }
             if (too_big) throw InternalError("parent items: more than 255 evaluations in one merged group");
+            // bounds the kernel relies on (no device-side checks)
+            for (std::int64_t it = 0; it < n_item; ++it)
+                for (std::int64_t g = ig[it]; g < ig[it + 1]; ++g) {
+                    const int4 r4 = rec[std::size_t(g)];
+                    const int st0 = r4.z & 0xffff, cnt = (r4.z >> 16) & 0xff;
+                    if (r4.x < 0 || std::size_t(r4.x) >= CL.nseg() || r4.y < 0 ||
+                        std::size_t(r4.y) >= T.level[d - 1].size() || cnt < 1 || ie[it] + st0 + cnt > ie[it + 1])
+                        throw InternalError("parent items: inconsistent group record");
+                }
             std::vector<std::int32_t> igr(ig.begin(), ig.end());
             LevelBufs& b = e.lb[d - 1];
             b.pgrp_rec.upload(rec);
