@@ -48,7 +48,7 @@ leaf_ray_kernel(LevelDev L, PointsDev P, const double2* __restrict__ a_p, double
     const int NPTS = kPS * NRAY;
     const int G = max(1, int(blockDim.x) / NRAY);
     const double h = L.h, inv_h = 1.0 / L.h;
-    // staged sources of b0 at smem[0, 10 kTile), of b1 at smem[10 kTile, 20 kTile)
+    // staged sources (10 doubles each) of b0 at smem[0, 10 kTile), of b1 at smem[10 kTile, 20 kTile)
     double2* v0 = reinterpret_cast<double2*>(smem + 20 * kTile);
     double2* v1 = v0 + G * NP * NPTS;
 
@@ -59,17 +59,19 @@ leaf_ray_kernel(LevelDev L, PointsDev P, const double2* __restrict__ a_p, double
             const int t = pb + t0 + q;
             const double dx = P.x[t] - cx, dy = P.y[t] - cy, dz = P.z[t] - cz;
             const double nx = P.nx[t], ny = P.ny[t], nz = P.nz[t];
-            R[q] = dx;
-            R[kTile + q] = dy;
-            R[2 * kTile + q] = dz;
-            R[3 * kTile + q] = fma(dx, dx, fma(dy, dy, dz * dz));
-            R[4 * kTile + q] = nx;
-            R[5 * kTile + q] = ny;
-            R[6 * kTile + q] = nz;
-            R[7 * kTile + q] = fma(dx, nx, fma(dy, ny, dz * nz));
+            // one 80-byte row per source (5 x 16-byte loads in the loop)
+            double* row = R + 10 * q;
+            row[0] = dx;
+            row[1] = dy;
+            row[2] = dz;
+            row[3] = fma(dx, dx, fma(dy, dy, dz * dz));
+            row[4] = nx;
+            row[5] = ny;
+            row[6] = nz;
+            row[7] = fma(dx, nx, fma(dy, ny, dz * nz));
             const double2 a = a_p[t];
-            R[8 * kTile + q] = a.x;
-            R[9 * kTile + q] = a.y;
+            row[8] = a.x;
+            row[9] = a.y;
         }
     };
     const int n0 = int(L.end[b0]) - int(L.beg[b0]);
@@ -122,14 +124,14 @@ leaf_ray_kernel(LevelDev L, PointsDev P, const double2* __restrict__ a_p, double
             __syncthreads();
         }
         if (!act) continue;
-        const double *sdx = R, *sdy = R + kTile, *sdz = R + 2 * kTile, *sd2 = R + 3 * kTile;
-        const double *snx = R + 4 * kTile, *sny = R + 5 * kTile, *snz = R + 6 * kTile, *sdn = R + 7 * kTile;
-        const double *sar = R + 8 * kTile, *sai = R + 9 * kTile;
+        const double2* rows = reinterpret_cast<const double2*>(R);
         for (int q = 0; q < tn; ++q) {
-            const double xd = fma(xh, sdx[q], fma(yh, sdy[q], zh * sdz[q]));
-            const double xn = fma(xh, snx[q], fma(yh, sny[q], zh * snz[q]));
-            const double d2 = sd2[q], dn0 = sdn[q];
-            const double ar = sar[q], ai = sai[q];
+            const double2 s0 = rows[5 * q], s1 = rows[5 * q + 1], s2 = rows[5 * q + 2], s3 = rows[5 * q + 3],
+                          s4 = rows[5 * q + 4];  // (dx, dy) (dz, |d|^2) (nx, ny) (nz, d.n) (a)
+            const double xd = fma(xh, s0.x, fma(yh, s0.y, zh * s1.x));
+            const double xn = fma(xh, s2.x, fma(yh, s2.y, zh * s3.x));
+            const double d2 = s1.y, dn0 = s3.y;
+            const double ar = s4.x, ai = s4.y;
 #pragma unroll
             for (int is = 0; is < kPS; ++is) {
                 const double sg = sig[is];
