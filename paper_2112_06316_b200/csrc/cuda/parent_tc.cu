@@ -132,8 +132,6 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
         const int cso = rec.x, ch = rec.y;
         const int start = rec.z & 0xffff, count = (rec.z >> 16) & 0xff, oct = (rec.z >> 24) & 7;
         if (Lc.active && !Lc.active[ch]) continue;  // child holds no sources of this rank
-        const double ccx = Lc.cx[ch], ccy = Lc.cy[ch], ccz = Lc.cz[ch];
-        const CellFrame cf = Lc.seg_code ? cell_frame_code(unsigned(rec.w), Lc) : cell_frame(rec.w, Lc);
         // B fragments of the group's block, reused by all its tiles (tc_common.cuh)
         double bq[LY::NB];
         load_b<NPC>(cstore + std::size_t(cso) * NPC * kNP, lane, bq);
@@ -160,6 +158,10 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
                     r1y = t2.x;
                     xf = CB::extra == RI ? t2.y : t3.x;
                 } else {
+                    // child frame, loaded only on this (rare, non-template) path
+                    const double ccx = Lc.cx[ch], ccy = Lc.cy[ch], ccz = Lc.cz[ch];
+                    const CellFrame cf =
+                        Lc.seg_code ? cell_frame_code(unsigned(rec.w), Lc) : cell_frame(rec.w, Lc);
                     const int is = node % kPS, it = (node / kPS) % kPA, ip = node / (kPS * kPA);
                     const int g1 = code & 0xff, g2 = (code >> 8) & 0x7ff, g3 = code >> 19;
                     const double s = Lp.s_nodes[g1 * kPS + is];
