@@ -331,6 +331,43 @@ __device__ inline void block_transform(double2* v0, double2* v1, int nblk, int p
     }
 }
 
+// the same transform with compile-time orders (index arithmetic by constants, loops unrolled);
+// identical arithmetic, so identical results
+template <int PS, int PA>
+__device__ inline void block_transform_c(double2* v0, double2* v1, int nblk, const double* __restrict__ Ms,
+                                         const double* __restrict__ Ma, double2* __restrict__ dst) {
+    constexpr int P = PS * PA * PA;
+    const int total = nblk * P;
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {  // along s
+        const int blk = e / P, node = e % P;
+        const int is = node % PS, line = node / PS;
+        const double2* src = v0 + blk * P + line * PS;
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int q = 0; q < PS; ++q) cfma_r(acc, src[q], Ms[is * PS + q]);
+        v1[e] = acc;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {  // along theta
+        const int blk = e / P, node = e % P;
+        const int is = node % PS, it = (node / PS) % PA, ip = node / (PS * PA);
+        const double2* src = v1 + blk * P + is + PS * PA * ip;
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int q = 0; q < PA; ++q) cfma_r(acc, src[PS * q], Ma[it * PA + q]);
+        v0[e] = acc;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {  // along phi
+        const int blk = e / P, node = e % P;
+        const int is = node % PS, it = (node / PS) % PA, ip = node / (PS * PA);
+        const double2* src = v0 + blk * P + is + PS * it;
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int q = 0; q < PA; ++q) cfma_r(acc, src[PS * PA * q], Ma[ip * PA + q]);
+        dst[e] = acc;
+    }
+}
 
 }  // namespace ifgfdev
 }  // namespace ifgfb200

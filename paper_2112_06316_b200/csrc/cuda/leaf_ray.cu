@@ -172,7 +172,10 @@ leaf_ray_kernel(LevelDev L, PointsDev P, const double2* __restrict__ a_p, double
             for (int i = 0; i < NP; ++i) v0[(seg_l * NP + i) * NPTS + is + kPS * ray] = acc[is][i];
     }
     __syncthreads();
-    block_transform(v0, v1, ns * NP, kPS, pa, Ms, Ma, store + std::size_t(s0) * NP * NPTS);
+    if (pa == 5)
+        block_transform_c<kPS, 5>(v0, v1, ns * NP, Ms, Ma, store + std::size_t(s0) * NP * NPTS);
+    else
+        block_transform(v0, v1, ns * NP, kPS, pa, Ms, Ma, store + std::size_t(s0) * NP * NPTS);
 }
 
 }  // namespace
