@@ -94,6 +94,10 @@ struct Engine::Impl {
     cudaStream_t st = nullptr;
     cudaStream_t st2 = nullptr;            // side stream: near field + RP, concurrent with the IFGF
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // cousin stream: cousin(d) beside parent(d); ev_store[d] = level d's store ready (on st),
+    // ev_cousin[d] = cousin(d) done reading it (on st3)
+    cudaStream_t st3 = nullptr;
+    std::vector<cudaEvent_t> ev_store, ev_cousin;
     std::mutex mu;
     std::size_t n = 0;
     int depth = 0;
@@ -197,9 +201,22 @@ struct Engine::Impl {
         ++launches;
         if constexpr (!std::is_same_v<F, void (*)()>) after_leaf();
         if (ev) IFGF_CUDA(cudaEventRecord(ev[0], st));
+        // cousin(d) on st3 beside parent(d) on st (both only read level d's store); parent(d)
+        // overwrites level d+1's store, so it waits for cousin(d+1); the cousins stay in level
+        // order on one stream, so every target's sums are added in the same order as serially
+        const char* cenv = std::getenv("IFGF_COUSIN_STREAM");
+        const bool two = !ev && !(cenv && cenv[0] == '0') && st3;
         for (int d = depth; d >= 3; --d) {
             const Pipes pc = make_pipes(pipes_at(d, single, dbl, s));
-            launch_cousin_eval(L[d - 1], P, cur, k, pc, Sp.as<double2>(), Dp.as<double2>(), st);
+            if (two) {
+                IFGF_CUDA(cudaEventRecord(ev_store[d], st));
+                IFGF_CUDA(cudaStreamWaitEvent(st3, ev_store[d], 0));
+                launch_cousin_eval(L[d - 1], P, cur, k, pc, Sp.as<double2>(), Dp.as<double2>(), st3);
+                IFGF_CUDA(cudaEventRecord(ev_cousin[d], st3));
+                if (d < depth) IFGF_CUDA(cudaStreamWaitEvent(st, ev_cousin[d + 1], 0));
+            } else {
+                launch_cousin_eval(L[d - 1], P, cur, k, pc, Sp.as<double2>(), Dp.as<double2>(), st);
+            }
             ++launches;
             if (d > 3) {
                 const Pipes pp = make_pipes(pipes_at(d - 1, single, dbl, s));
@@ -209,6 +226,7 @@ struct Engine::Impl {
                 std::swap(cur, nxt);
             }
         }
+        if (two) IFGF_CUDA(cudaStreamWaitEvent(st, ev_cousin[3], 0));  // join before Sp/Dp are read
         return launches;
     }
 
@@ -425,6 +443,13 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
     IFGF_CUDA(cudaStreamCreateWithFlags(&e.st2, cudaStreamNonBlocking));
     IFGF_CUDA(cudaEventCreateWithFlags(&e.ev_fork, cudaEventDisableTiming));
     IFGF_CUDA(cudaEventCreateWithFlags(&e.ev_join, cudaEventDisableTiming));
+    IFGF_CUDA(cudaStreamCreateWithFlags(&e.st3, cudaStreamNonBlocking));
+    e.ev_store.assign(64, nullptr);
+    e.ev_cousin.assign(64, nullptr);
+    for (int d = 0; d < 64; ++d) {
+        IFGF_CUDA(cudaEventCreateWithFlags(&e.ev_store[d], cudaEventDisableTiming));
+        IFGF_CUDA(cudaEventCreateWithFlags(&e.ev_cousin[d], cudaEventDisableTiming));
+    }
     const Surface& S = *s.surf;
     const BoxTree& T = *s.tree;
     const BoxRelations& R = *s.rel;
@@ -1041,6 +1066,11 @@ Engine::~Engine() {
         if (d_->comm) ncclCommDestroy(d_->comm);
         if (d_->ev_fork) cudaEventDestroy(d_->ev_fork);
         if (d_->ev_join) cudaEventDestroy(d_->ev_join);
+        for (auto x : d_->ev_store)
+            if (x) cudaEventDestroy(x);
+        for (auto x : d_->ev_cousin)
+            if (x) cudaEventDestroy(x);
+        if (d_->st3) cudaStreamDestroy(d_->st3);
         if (d_->st2) cudaStreamDestroy(d_->st2);
         if (d_->st) cudaStreamDestroy(d_->st);
     }
