@@ -26,11 +26,17 @@ using namespace tc;
 constexpr int kThreads = 128, kWarps = kThreads / 32;
 constexpr int kCG = kRowLen + 6;  // A slots, T(phi), the pipe factors (3 complex) (odd stride)
 
-template <int NPC>
+// CODE = f0 f1 f2 as decimal digits (factor codes of the pipes) for the common pipe sets, so the
+// pipe logic folds at compile time; 0 = read them from pp
+template <int NPC, int CODE>
 __global__ void __launch_bounds__(kThreads, 4)
 cousin_tc_kernel(LevelDev L, PointsDev P, const double2* __restrict__ store, double k, Pipes pp,
                  double2* __restrict__ Sp, double2* __restrict__ Dp) {
     using LY = Layout<NPC>;
+    auto fcode = [&](int i) -> int {
+        if constexpr (CODE != 0) return i == 0 ? CODE / 100 : (i == 1 ? (CODE / 10) % 10 : CODE % 10);
+        else return pp.f[i];
+    };
     __shared__ double sgeo[kWarps][32 * kCG];
     __shared__ double2 sacc[kWarps][32][2];
     __shared__ int slist[kWarps][32];
@@ -50,8 +56,9 @@ cousin_tc_kernel(LevelDev L, PointsDev P, const double2* __restrict__ store, dou
     // S comes from the W1 lane alone; D from the first D-pipe lane plus, for (W2, W3), its
     // right neighbour (pipe lists keep W2, W3 adjacent)
     int s_lane = -1, d_lane = -1, n_d = 0;
+#pragma unroll
     for (int i = 0; i < NPC; ++i) {
-        if (pp.f[i] == 1) s_lane = i;
+        if (fcode(i) == 1) s_lane = i;
         else if (n_d++ == 0) d_lane = i;
     }
     const int j0 = L.cz_ptr[tb], j1 = L.cz_ptr[tb + 1];
@@ -75,8 +82,8 @@ cousin_tc_kernel(LevelDev L, PointsDev P, const double2* __restrict__ store, dou
 #pragma unroll
             for (int p = 0; p < NPC; ++p) {
                 double2 f = e1;
-                if (pp.f[p] == 2) f = cscale(e1, inv_r);
-                if (pp.f[p] == 3) f = make_double2(k * e1.y, -k * e1.x);
+                if (fcode(p) == 2) f = cscale(e1, inv_r);
+                if (fcode(p) == 3) f = make_double2(k * e1.y, -k * e1.x);
                 mygeo[kRowLen + 2 * p] = f.x;
                 mygeo[kRowLen + 2 * p + 1] = f.y;
             }
@@ -126,10 +133,17 @@ bool launch_cousin_eval_tc(const LevelDev& L, const PointsDev& P, const double2*
     if (pipes.n == 3 && pipes.f[1] == 1) return false;  // D pipes must be adjacent (epilogue shuffle)
     if (L.nwchunk == 0) return true;
     const int grid = (L.nwchunk + kWarps - 1) / kWarps;
-    switch (pipes.n) {
-        case 1: cousin_tc_kernel<1><<<grid, kThreads, 0, st>>>(L, P, store, k, pipes, Sp, Dp); break;
-        case 2: cousin_tc_kernel<2><<<grid, kThreads, 0, st>>>(L, P, store, k, pipes, Sp, Dp); break;
-        default: cousin_tc_kernel<3><<<grid, kThreads, 0, st>>>(L, P, store, k, pipes, Sp, Dp); break;
+    const int code = pipes.f[0] * 100 + (pipes.n > 1 ? pipes.f[1] * 10 : 0) + (pipes.n > 2 ? pipes.f[2] : 0);
+    switch (code) {
+        case 123: cousin_tc_kernel<3, 123><<<grid, kThreads, 0, st>>>(L, P, store, k, pipes, Sp, Dp); break;
+        case 140: cousin_tc_kernel<2, 140><<<grid, kThreads, 0, st>>>(L, P, store, k, pipes, Sp, Dp); break;
+        case 100: cousin_tc_kernel<1, 100><<<grid, kThreads, 0, st>>>(L, P, store, k, pipes, Sp, Dp); break;
+        default:
+            switch (pipes.n) {
+                case 1: cousin_tc_kernel<1, 0><<<grid, kThreads, 0, st>>>(L, P, store, k, pipes, Sp, Dp); break;
+                case 2: cousin_tc_kernel<2, 0><<<grid, kThreads, 0, st>>>(L, P, store, k, pipes, Sp, Dp); break;
+                default: cousin_tc_kernel<3, 0><<<grid, kThreads, 0, st>>>(L, P, store, k, pipes, Sp, Dp); break;
+            }
     }
     IFGF_CUDA(cudaGetLastError());
     return true;
