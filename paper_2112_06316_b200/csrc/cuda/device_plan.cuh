@@ -45,7 +45,7 @@ struct LevelDev {
     const std::int32_t *pitem_seg = nullptr, *pitem_grp = nullptr;
     const std::int64_t* pitem_ev = nullptr;
     int n_pitem = 0;
-    int pitem_merge = 1;  // segments per item (accumulator blocks per warp)
+    int pitem_merge = 1;  // segments per item (the kernel always reserves kParentMergeMax blocks)
     const std::int32_t *ch_ptr = nullptr, *ch_idx = nullptr;  // children (level d+1) of this level's boxes
     const double *s_nodes = nullptr, *th_nodes = nullptr, *ph_nodes = nullptr;
     // sin/cos of the angular node tables (interpolation-node directions)

@@ -91,7 +91,7 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
     constexpr int NPP = CB::npp, NPC = CB::npc;
     extern __shared__ double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int merge = Lc.pitem_merge;
+    constexpr int merge = kParentMergeMax;  // accumulator blocks per warp (items may use fewer)
     double* geo = smem + warp * (kGeoSz + 2 * kNP * NPP * merge);  // per warp
     double2* acc = reinterpret_cast<double2*>(geo + kGeoSz);  // per item segment: 75 x NPP
     const int item = blockIdx.x * kWarps + warp;  // one warp per work item
@@ -313,7 +313,7 @@ bool launch_parent_fill_tc(const LevelDev& Lp, const LevelDev& Lc, const double2
         return false;
     if (Lc.n_pitem == 0) return true;
     const std::size_t smem =
-        std::size_t(kWarps) * (kGeoSz + 2 * kNP * parent_pipes.n * Lc.pitem_merge) * sizeof(double);
+        std::size_t(kWarps) * (kGeoSz + 2 * kNP * parent_pipes.n * kParentMergeMax) * sizeof(double);
     auto go = [&](auto kern) {
         IFGF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         kern<<<(Lc.n_pitem + kWarps - 1) / kWarps, 32 * kWarps, smem, st>>>(Lp, Lc, child_store, k, Ms, Ma, parent_store);
