@@ -352,10 +352,19 @@ __global__ void rp_accum_kernel(RpDev R, const double2* __restrict__ coeffs, dou
         const double2* a = coeffs + R.patch_start[q];
         const double2* bs = R.beta_s + R.beta_off[p];
         const double2* bd = R.beta_d + R.beta_off[p];
-        for (int i = lane; i < nn; i += 32) {
-            const double2 ai = a[i];
-            cfma(as, ai, __ldcs(bs + i));
-            cfma(ad, ai, __ldcs(bd + i));
+        if (nn == 256) {  // 16 x 16 patches (every bench config): a fixed, unrolled stream
+#pragma unroll
+            for (int i = lane; i < 256; i += 32) {
+                const double2 ai = a[i];
+                cfma(as, ai, __ldcs(bs + i));
+                cfma(ad, ai, __ldcs(bd + i));
+            }
+        } else {
+            for (int i = lane; i < nn; i += 32) {
+                const double2 ai = a[i];
+                cfma(as, ai, __ldcs(bs + i));
+                cfma(ad, ai, __ldcs(bd + i));
+            }
         }
     }
 #pragma unroll
