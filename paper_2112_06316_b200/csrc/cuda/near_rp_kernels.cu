@@ -291,6 +291,27 @@ __global__ void density_coeffs_kernel(RpDev R, const double2* __restrict__ phi,
     }
 }
 
+// one singular pair's beta rows against its patch's coefficients, lanes strided; 16 x 16
+// patches (every bench config) take a fixed, unrolled stream (more loads in flight)
+__device__ __forceinline__ void rp_pair_stream(const double2* __restrict__ a, const double2* __restrict__ bs,
+                                               const double2* __restrict__ bd, int nn, int lane, double2& as,
+                                               double2& ad) {
+    if (nn == 256) {
+#pragma unroll
+        for (int i = lane; i < 256; i += 32) {
+            const double2 ai = a[i];
+            cfma(as, ai, __ldcs(bs + i));
+            cfma(ad, ai, __ldcs(bd + i));
+        }
+    } else {
+        for (int i = lane; i < nn; i += 32) {
+            const double2 ai = a[i];
+            cfma(as, ai, __ldcs(bs + i));
+            cfma(ad, ai, __ldcs(bd + i));
+        }
+    }
+}
+
 __global__ void rp_combine_kernel(RpDev R, const double2* __restrict__ coeffs,
                                   const double2* __restrict__ phi, const double2* __restrict__ Sp,
                                   const double2* __restrict__ Dp, double gamma,
@@ -309,11 +330,7 @@ __global__ void rp_combine_kernel(RpDev R, const double2* __restrict__ coeffs,
         const double2* a = coeffs + R.patch_start[q];
         const double2* bs = R.beta_s + R.beta_off[p];
         const double2* bd = R.beta_d + R.beta_off[p];
-        for (int i = lane; i < nn; i += 32) {
-            const double2 ai = a[i];
-            cfma(as, ai, __ldcs(bs + i));
-            cfma(ad, ai, __ldcs(bd + i));
-        }
+        rp_pair_stream(a, bs, bd, nn, lane, as, ad);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -352,20 +369,7 @@ __global__ void rp_accum_kernel(RpDev R, const double2* __restrict__ coeffs, dou
         const double2* a = coeffs + R.patch_start[q];
         const double2* bs = R.beta_s + R.beta_off[p];
         const double2* bd = R.beta_d + R.beta_off[p];
-        if (nn == 256) {  // 16 x 16 patches (every bench config): a fixed, unrolled stream
-#pragma unroll
-            for (int i = lane; i < 256; i += 32) {
-                const double2 ai = a[i];
-                cfma(as, ai, __ldcs(bs + i));
-                cfma(ad, ai, __ldcs(bd + i));
-            }
-        } else {
-            for (int i = lane; i < nn; i += 32) {
-                const double2 ai = a[i];
-                cfma(as, ai, __ldcs(bs + i));
-                cfma(ad, ai, __ldcs(bd + i));
-            }
-        }
+        rp_pair_stream(a, bs, bd, nn, lane, as, ad);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
