@@ -2,19 +2,28 @@
 """CF-operator apply benchmark (BASELINE.json metric: applies/s and points/s).
 
 One step = one combined-field operator apply out = 1/2 phi + D[phi] - i gamma S[phi]
-(CombinedOperator::apply, solver.cpp:149-157) over the cfg2 sphere (16 wavelengths,
-N = 393,216; SURVEY.md Appendix A maps BASELINE's 6 x 256^2 layout to the reference-
-constructible 1,536 x 16^2 patches with the same N).
+(CombinedOperator::apply, solver.cpp:149-157). Default workload: cfg3, the 64-wavelength
+sphere (N = 6,291,456), the BASELINE config quoted at 1/2/4/8 GPUs that fits one B200
+(SURVEY.md Appendix A maps BASELINE's 6 x 1024^2 layout to the reference-constructible
+24,576 x 16^2 patches with the same N). --config cfg1/cfg2 select the smaller spheres.
 
   value : points/s with phi resident in HBM (CUDA-graph replays timed with CUDA events on
           the engine stream), whole job (sum over ranks, max time over ranks)
   e2e   : the same through the public API with host buffers — pinned phi copied in and the
           result read back every step (CombinedOperator.apply)
   roofline / rooflines : per-phase device time (CUDA events) against the algorithmic work
-  cpu_baseline : the reference's own CombinedOperator::apply (oracle/_ref, built from the
-          untouched /root/reference sources) on the host's cores, one full apply
+  cpu_baseline : the reference (oracle/_ref, built from the untouched /root/reference
+          sources) on the host's cores: cfg1/cfg2 one full CombinedOperator::apply; cfg3 a
+          bounded sample (ifgf_apply + the near-field loop, run at cfg2)
+  parity : cfg1/cfg2 the reference's full apply with its OWN beta tables; cfg3 the committed
+          reference fixture tests/golden/cfg3_large.npz (64 random projections of S and D
+          over all N, 65,536 sampled targets, the RP term of 16,384 targets from the
+          reference's own beta tables) — see tests/golden/large_check.py
 
---impl reference runs the reference CPU implementation alone (rank 0), same metric/config.
+--impl reference runs the reference CPU implementation alone (rank 0), same metric/config;
+at cfg3 one step = the reference's ifgf_apply + near-field loop (its beta tables would need
+101 GB and hours), one timed step after an untimed setup.
+--gpus N without a torchrun environment re-launches itself under torch.distributed.run.
 Multi-GPU (torchrun): one operator per GPU over a cost-balanced Morton partition of the
 sources/targets, far-field partials reduced and outputs broadcast with NCCL inside the
 engine; the same N-point apply at every N, scaling "strong".
@@ -158,6 +167,26 @@ def reference_apply_time(cfg_name, phi, beta_cache=None, applies=1, warmup=0):
     return times, out, setup, R.lib().ref_op_beta_cache_hit(ro.h) == 1
 
 
+LARGE = {"cfg3"}  # no reference beta tables: ifgf_apply + near loop
+
+
+def reference_ifgf_near_time(cfg_name, phi, steps=1):
+    """The reference's ifgf_apply + near-field loop (layer_potentials without its RP term) on
+    a plan built without beta tables; returns (seconds list, S, D, setup dict)."""
+    from oracle import ref as R
+
+    splits, nu, k, gamma, _ = CONFIGS[cfg_name]
+    rm = make_mesh(cfg_name, R)
+    t0 = time.perf_counter()
+    rp = R.RefPlan(rm, k, gamma=gamma)
+    setup = dict(rp.setup_seconds, total=time.perf_counter() - t0)
+    times, S, D = [], None, None
+    for _ in range(steps):
+        S, D, sec = rp.ifgf_near(phi)
+        times.append(sec["ifgf_apply"] + sec["near"])
+    return times, S, D, setup
+
+
 def run_reference(args, ws, rank):
     cfg_name = args.config
     splits, nu, k, gamma, desc = CONFIGS[cfg_name]
@@ -170,12 +199,34 @@ def run_reference(args, ws, rank):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libifgf_ref.so not built"}))
         return
     phi = R.random_density(n, 1)
+    cores = os.cpu_count()
+    if cfg_name in LARGE:
+        steps, warm = 1, 0
+        times, _, _, setup = reference_ifgf_near_time(cfg_name, phi, steps)
+        total = sum(times)
+        value = n * steps / total
+        sample = (f"1 step = the reference's ifgf_apply (ifgf.cpp:577-608) + the level-D near-field loop "
+                  f"(solver.cpp:100-144) at {cfg_name} (N={n}), i.e. CombinedOperator::layer_potentials minus "
+                  f"its RP term: the reference's beta tables would need 101 GB and hours of CPU (BASELINE.md §3); "
+                  f"setup (octree, plan_cones, classify_targets) {setup['total']:.0f} s untimed; OpenMP {cores} "
+                  f"threads; 1 step, no warm-up, to bound the run")
+        line = {
+            "impl": "reference", "metric": "cf_operator_points_per_s", "value": value, "unit": "points/s",
+            "applies_per_s": steps / total, "n_gpus": args.gpus, "steps": steps, "warmup": warm,
+            "steps_requested": args.steps, "ms_per_step": 1e3 * total / steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "config": {"workload": f"{cfg_name}: {desc}", "N": n, "k": k, "parallelism": "cpu-openmp"},
+            "setup_s": setup,
+            "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "reference", "sample": sample},
+            "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line))
+        return
     steps = max(1, min(args.steps, args.ref_steps))
     warm = min(args.warmup, 1)
     times, _, setup, _ = reference_apply_time(cfg_name, phi, applies=steps, warmup=warm)
     total = sum(times)
     value = n * steps / total
-    cores = os.cpu_count()
     line = {
         "impl": "reference", "metric": "cf_operator_points_per_s", "value": value, "unit": "points/s",
         "applies_per_s": steps / total, "n_gpus": args.gpus, "steps": steps, "warmup": warm,
@@ -232,6 +283,100 @@ def ncu_traffic(cfg_name, phase):
         return (k["dram_bytes_per_apply"] if k else None), os.path.relpath(files[-1], ROOT)
     except Exception:
         return None, None
+
+
+def check_parity(cfg_name, op, phi, out_gpu):
+    """cfg1/cfg2: the reference's full CombinedOperator::apply with its own beta tables,
+    compared over all N. cfg3: the committed reference fixture (large_check.py)."""
+    if cfg_name in LARGE:
+        sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+        import large_check as LC
+
+        path = os.path.join(ROOT, "tests", "golden", f"{cfg_name}_large.npz")
+        fix = np.load(path)
+        if not np.array_equal(phi[:8], fix["phi_head"]):
+            raise RuntimeError("density differs from the fixture's")
+        S, D = op.layer_potentials(phi)
+        rS, rD = op.rp_singular_apply(phi)
+        res = LC.compare(fix, S - rS, D - rD)
+        idx = fix["rp_idx"]
+        rp = LC.compare_rp(fix, rS[idx], rD[idx])
+        # out at the RP-sampled targets from the reference's S, D and RP terms
+        g = float(fix["gamma"])
+        s_ref = fix["S_sample"][np.searchsorted(fix["sample_idx"], idx)] + fix["rpS"]
+        d_ref = fix["D_sample"][np.searchsorted(fix["sample_idx"], idx)] + fix["rpD"]
+        out_ref = 0.5 * phi[idx] + d_ref - 1j * g * s_ref
+        out_rel = float(np.linalg.norm(out_gpu[idx] - out_ref) / np.linalg.norm(out_ref))
+        head = max(res["S"]["rel_l2_est_full"], res["D"]["rel_l2_est_full"], out_rel)
+        return {"rel_l2_vs_reference": head, "parity": {
+            "method": "reference fixture tests/golden/cfg3_large.npz (tests/golden/make_large.py from oracle/_ref): "
+                      "S, D without RP over ALL N via 64 random projections (estimated rel-L2), exact on 65,536 "
+                      "sampled targets; RP from the reference's own beta_precompute + rp_singular_apply on 16,384 "
+                      "targets; out on those targets",
+            "S_D_noRP": res, "rp_sample": rp, "out_rel_l2_rp_sample": out_rel,
+            "fixture_ref_seconds": json.loads(str(fix["ref_seconds"]))}}
+    from oracle import ref as R
+
+    if not R.available():
+        return {"parity": {"error": "oracle/_ref not built"}}
+    times, out_ref, setup = _ref_full(cfg_name, phi)
+    rel = float(np.linalg.norm(out_gpu - out_ref) / np.linalg.norm(out_ref))
+    return {"rel_l2_vs_reference": rel,
+            "parity": {"method": f"reference CombinedOperator::apply at {cfg_name} over all N with its own "
+                                 f"beta_precompute (setup {setup:.1f} s)",
+                       "max_abs": float(np.max(np.abs(out_gpu - out_ref)))}}
+
+
+_REF_FULL = {}
+
+
+def _ref_full(cfg_name, phi):
+    """one reference CombinedOperator (own beta tables) per config: (apply times, out, setup s)"""
+    if cfg_name not in _REF_FULL:
+        times, out, setup, _ = reference_apply_time(cfg_name, phi, applies=1)
+        _REF_FULL[cfg_name] = (times, out, setup)
+    return _REF_FULL[cfg_name]
+
+
+def cpu_baseline(cfg_name, n):
+    """The reference on the host's cores (reported, not the target)."""
+    from oracle import ref as R
+
+    if not R.available():
+        return {"error": "oracle/_ref not built"}
+    cores = os.cpu_count()
+    if cfg_name in LARGE:  # bounded sample: ifgf_apply + near loop at cfg2 (~20 s on 16 cores)
+        sub = "cfg2"
+        m = 6 * 4 ** CONFIGS[sub][0] * CONFIGS[sub][1] ** 2
+        times, _, _, setup = reference_ifgf_near_time(sub, R.random_density(m, 1), 1)
+        return {"value": m / times[0], "unit": "points/s", "cores": cores, "kind": "reference",
+                "seconds": times[0],
+                "sample": f"bounded sample: the reference's ifgf_apply + near-field loop (BASELINE.md §3; no RP: "
+                          f"its cfg3 beta tables would need 101 GB) on the cfg2 sphere of the same family "
+                          f"(N={m}, 1/16 of cfg3's points; the reference's per-point cost grows ~log N, so this "
+                          f"overstates its cfg3 rate); OpenMP {cores} threads; --impl reference times cfg3 itself"}
+    times, _, setup = _ref_full(cfg_name, R.random_density(n, 1))
+    return {"value": n / times[0], "unit": "points/s", "cores": cores, "kind": "reference", "seconds": times[0],
+            "sample": f"one full CombinedOperator::apply at {cfg_name} (N={n}), reference built from /root/reference "
+                      f"sources, OpenMP {cores} threads, its own beta tables (setup {setup:.1f} s)"}
+
+
+def spawn_ranks(args):
+    """--gpus N outside torchrun: re-launch this command under torch.distributed.run"""
+    import socket
+
+    import torch
+
+    if torch.cuda.device_count() < args.gpus:
+        print(json.dumps({"metric": "cf_operator_points_per_s", "n_gpus": args.gpus,
+                          "error": f"--gpus {args.gpus} but {torch.cuda.device_count()} GPU(s) visible"}))
+        sys.exit(1)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
 
 
 def run_b200(args, ws, rank, local):
@@ -334,27 +479,16 @@ def run_b200(args, ws, rank, local):
         "phases_ms": phases, "work": work, "roofline": roof, "rooflines": roofs,
     }
 
-    # --- CPU baseline + parity at the bench config (rank 0, N=1)
+    # --- parity + CPU baseline at the bench config (rank 0, N=1; outside the timed regions)
+    if rank == 0 and ws == 1 and not args.no_check:
+        try:
+            line.update(check_parity(args.config, op, phi, out_gpu))
+        except Exception as e:  # report, never hide
+            line["parity"] = {"error": repr(e)}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
-            from oracle import ref as R
-
-            if R.available():
-                cache = os.path.join(tempfile.gettempdir(), f"ifgf_b200_beta_{args.config}.bin")
-                op.save_beta_cache(cache)
-                times, out_ref, ref_setup, hit = reference_apply_time(args.config, phi, beta_cache=cache,
-                                                                      applies=1)
-                os.unlink(cache)
-                cores = os.cpu_count()
-                line["cpu_baseline"] = {
-                    "value": n / times[0], "unit": "points/s", "cores": cores, "kind": "reference",
-                    "sample": f"one full CombinedOperator::apply at {args.config} (N={n}), reference built from "
-                              f"/root/reference sources, OpenMP {cores} threads; its setup ({ref_setup:.1f} s) "
-                              f"loaded the beta tables from an rpbeta v1 cache (hit={hit})",
-                    "seconds": times[0]}
-                rel = float(np.linalg.norm(out_gpu - out_ref) / np.linalg.norm(out_ref))
-                line["rel_l2_vs_reference"] = rel
-        except Exception as e:  # report, never hide
+            line["cpu_baseline"] = cpu_baseline(args.config, n)
+        except Exception as e:
             line["cpu_baseline"] = {"error": repr(e)}
     if rank == 0:
         print(json.dumps(line))
@@ -368,11 +502,14 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--config", choices=list(CONFIGS), default="cfg2")
+    ap.add_argument("--config", choices=list(CONFIGS), default="cfg3")
     ap.add_argument("--ref-steps", type=int, default=3, help="cap on timed reference applies")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-check", action="store_true", help="skip the parity check against the reference")
     args = ap.parse_args()
     ws, rank, local = dist_setup()
+    if args.impl == "b200" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args)
     if args.impl == "reference":
         run_reference(args, ws, rank)
     else:

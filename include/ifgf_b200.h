@@ -61,6 +61,9 @@ typedef struct {
     int32_t device;           /* CUDA device ordinal */
     int32_t part_rank, part_world;  /* per-rank plan of a multi-GPU run (0, 1: the full plan):
                                        only boxes with sources of rank part_rank's Morton range */
+    const char* beta_cache_path; /* SolveConfig::beta_cache_path: NULL/"" none; else the
+                                    "rpbeta v1" cache is loaded when it matches, otherwise
+                                    the tables are computed and saved there (solver.cpp:64-74) */
 } ifgf_config;
 
 const char* ifgf_last_error(void);
@@ -168,6 +171,9 @@ int ifgf_operator_get_beta(ifgf_operator* op, uint64_t* offset, double* bs, doub
  * load returns 1 when the cache was used, 0 when absent/mismatched */
 int ifgf_operator_save_beta_cache(ifgf_operator* op, const char* path);
 int ifgf_operator_load_beta_cache(ifgf_operator* op, const char* path);
+/* 1 when ifgf_operator_create took the tables from cfg->beta_cache_path
+ * (CombinedOperator::beta_cache_was_reused, solver.hpp:70) */
+int ifgf_operator_beta_cache_hit(const ifgf_operator* op);
 /* benchmark helpers: phi resident in HBM, CUDA-graph replays timed with CUDA events */
 int ifgf_operator_upload_density(ifgf_operator* op, const double* phi);
 int ifgf_operator_time_applies(ifgf_operator* op, int iters, int flush_l2, double* ms_per_apply);

@@ -130,8 +130,9 @@ class GpuCombinedOperator {
         c.cov_d = sc.rp.cov_d;
         c.workers = sc.workers;
         c.device = device;
-        // the beta tables are rebuilt on the GPU in well under a second, so
-        // sc.beta_cache_path is not consulted (ifgf_operator_load/save_beta_cache exist)
+        // the reference ctor's cache policy (solver.cpp:64-74): load when it matches, else
+        // compute on the GPU and save
+        c.beta_cache_path = sc.beta_cache_path.empty() ? nullptr : sc.beta_cache_path.c_str();
         build(surf_, c);
     }
 #endif
@@ -176,6 +177,7 @@ class GpuCombinedOperator {
     }
 
     ifgf_operator* handle() const { return op_; }
+    bool beta_cache_was_reused() const { return ifgf_operator_beta_cache_hit(op_) == 1; }
 
 #ifdef IFGF_B200_WITH_REFERENCE
     // solve(mesh, incident, cfg) (solver.hpp:111-112) on this operator: rhs = -u^i for either
@@ -197,7 +199,9 @@ class GpuCombinedOperator {
         r.residual_history.resize(std::size_t(std::max(it, 0)));
         r.gamma = gamma();
         r.k = sc.k;
-        if (rc == 4) return r;  // not converged: the reference reports it in the result
+        // not converged (or Arnoldi breakdown): the reference's solve() throws
+        // ConvergenceFailure carrying the residual history (solver.cpp:334-338)
+        if (rc == 4) throw ifgf::ConvergenceFailure(std::string("solve: ") + ifgf_last_error(), r.residual_history);
         check(rc, "solve");
         return r;
     }

@@ -90,6 +90,18 @@ def lib():
             "ref_near_field": (C.c_int, [vp, d_p, C.c_double, C.c_double, C.c_double, C.c_double, d_p, C.c_long,
                                          C.c_double, d_p, d_p, C.POINTER(C.c_ubyte)]),
             "ref_mie_far_field": (C.c_int, [C.c_double, C.c_double, d_p, d_p, C.c_long, C.c_int, d_p]),
+            "ref_plan_create": (vp, [vp, C.c_double, C.c_double, C.c_int, d_p]),
+            "ref_plan_free": (None, [vp]),
+            "ref_plan_gamma": (C.c_double, [vp]),
+            "ref_plan_depth": (C.c_int, [vp]),
+            "ref_plan_npairs": (C.c_long, [vp]),
+            "ref_plan_nfar": (C.c_long, [vp]),
+            "ref_plan_nsegs": (C.c_long, [vp, C.c_int]),
+            "ref_plan_segment_hash": (C.c_ulonglong, [vp, C.c_int]),
+            "ref_plan_perm_hash": (C.c_ulonglong, [vp]),
+            "ref_plan_ifgf_near": (C.c_int, [vp, d_p, d_p, d_p, d_p]),
+            "ref_plan_rp_sample": (C.c_int, [vp, d_p, C.POINTER(C.c_long), C.c_long, d_p, d_p,
+                                             C.POINTER(C.c_long), d_p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -347,3 +359,72 @@ class RefOperator:
     def save_beta_cache(self, path):
         if lib().ref_op_save_beta_cache(self.h, path.encode()):
             raise _err("save_beta_cache")
+
+
+class RefPlan:
+    """The reference's setup WITHOUT the beta tables (build_octree, compute_relations,
+    plan_cones, classify_targets; solver.cpp:47-51) for the configs whose tables do not fit
+    here (cfg3: 101 GB). ifgf_near() = layer_potentials without its RP term (ifgf_apply +
+    a restated solver.cpp:100-144 loop over the reference's green/dlayer_kernel);
+    rp_sample() = the reference's beta_precompute + rp_singular_apply on the given targets'
+    pairs only."""
+
+    def __init__(self, mesh: RefMesh, k, gamma=-1.0, workers=0):
+        self.mesh = mesh
+        self.n = mesh.n
+        self.k = k
+        t = np.zeros(3)
+        self.h = lib().ref_plan_create(mesh.h, k, gamma, workers, _p(t))
+        if not self.h:
+            raise _err("reference plan construction failed")
+        self.setup_seconds = {"tree": float(t[0]), "plan_cones": float(t[1]), "classify_targets": float(t[2])}
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.ref_plan_free(self.h)
+            self.h = None
+
+    @property
+    def gamma(self):
+        return lib().ref_plan_gamma(self.h)
+
+    @property
+    def depth(self):
+        return lib().ref_plan_depth(self.h)
+
+    def segment_hashes(self):
+        return {d: int(lib().ref_plan_segment_hash(self.h, d)) for d in range(3, self.depth + 1)}
+
+    def segment_counts(self):
+        return {d: int(lib().ref_plan_nsegs(self.h, d)) for d in range(3, self.depth + 1)}
+
+    def perm_hash(self):
+        return int(lib().ref_plan_perm_hash(self.h))
+
+    def npairs(self):
+        return int(lib().ref_plan_npairs(self.h))
+
+    def ifgf_near(self, phi):
+        """(S, D, seconds{ifgf_apply, near}) without the RP term"""
+        f, keep = _c(phi)
+        S = np.zeros(2 * self.n)
+        D = np.zeros(2 * self.n)
+        t = np.zeros(2)
+        rc = lib().ref_plan_ifgf_near(self.h, _p(f), _p(S), _p(D), _p(t))
+        if rc:
+            raise _err("ifgf_near")
+        return S.view(np.complex128), D.view(np.complex128), {"ifgf_apply": float(t[0]), "near": float(t[1])}
+
+    def rp_sample(self, phi, targets):
+        """RP (S, D) at the ascending original-index targets, npairs, seconds"""
+        f, keep = _c(phi)
+        tg = np.ascontiguousarray(targets, dtype=np.int64)
+        S = np.zeros(2 * len(tg))
+        D = np.zeros(2 * len(tg))
+        npairs = C.c_long(0)
+        sec = np.zeros(1)
+        rc = lib().ref_plan_rp_sample(self.h, _p(f), tg.ctypes.data_as(C.POINTER(C.c_long)), len(tg), _p(S), _p(D),
+                                      C.byref(npairs), _p(sec))
+        if rc:
+            raise _err("rp_sample")
+        return S.view(np.complex128), D.view(np.complex128), int(npairs.value), float(sec[0])

@@ -572,4 +572,207 @@ double ref_graded(int which, double alpha, double tau, int d) {
     }
 }
 
+
+// ---------------------------------------------------------------- plan without beta (cfg3/cfg4)
+// The large configs cannot build the reference's beta tables here (101 GB at cfg3, 178 GB at
+// cfg4, hours of CPU). BASELINE.md §3 / SURVEY.md §8(d) H5: the reference is then run as
+// build_octree -> compute_relations -> plan_cones -> classify_targets (the ctor's own steps,
+// solver.cpp:47-51, minus beta_precompute), ifgf_apply (ifgf.cpp:577-608) and a restatement
+// of the level-D near-field loop (solver.cpp:100-144) that calls the reference's own green()
+// and dlayer_kernel(). The RP term is checked on a sample of targets: the sample's pairs form
+// a sub-ProximityMap whose beta tables the reference's beta_precompute builds and whose
+// rp_singular_apply gives the sampled targets' RP contributions (rp.cpp:309-451).
+struct RefPlan {
+    std::shared_ptr<SurfaceMesh> mesh;
+    SolveConfig cfg;
+    double gamma = 0;
+    DlStrategy strategy = DlStrategy::Hybrid;
+    Octree tree;
+    Relations rel;
+    ConePlan plan;
+    ProximityMap prox;
+    double t_tree = 0, t_plan = 0, t_prox = 0;
+};
+
+static double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+void* ref_plan_create(void* mesh, double k, double gamma, int workers, double* times3) {
+    try {
+        auto* r = new RefPlan;
+        r->mesh = *static_cast<std::shared_ptr<SurfaceMesh>*>(mesh);
+        r->cfg.k = k;
+        r->cfg.gamma = gamma;
+        r->cfg.workers = workers;
+        const SurfaceMesh& m = *r->mesh;
+        const double lambda = 2.0 * std::numbers::pi / k;
+        r->gamma = gamma > 0 ? gamma : coupling_gamma(m.diameter(), lambda);
+        double t0 = now_s();
+        r->tree = build_octree(m.pos, k, r->cfg.finest_box_lambda);
+        r->rel = compute_relations(r->tree);
+        r->t_tree = now_s() - t0;
+        t0 = now_s();
+        r->plan = plan_cones(r->tree, r->rel, m.pos, m.normal, r->cfg.cone, workers);
+        r->t_plan = now_s() - t0;
+        t0 = now_s();
+        r->prox = classify_targets(m, r->tree, r->rel, r->cfg.rp, workers);
+        r->t_prox = now_s() - t0;
+        bool any_sub = false;  // Hybrid resolution as the ctor (solver.cpp:55-62)
+        for (int d = 3; d <= r->tree.depth; ++d)
+            if (r->tree.side(d) / lambda < 0.5 - 1e-12) any_sub = true;
+        r->strategy = any_sub ? DlStrategy::Hybrid : DlStrategy::W4;
+        if (times3) {
+            times3[0] = r->t_tree;
+            times3[1] = r->t_plan;
+            times3[2] = r->t_prox;
+        }
+        return r;
+    } catch (const std::exception& e) {
+        fail(e);
+        return nullptr;
+    }
+}
+
+void ref_plan_free(void* h) { delete static_cast<RefPlan*>(h); }
+static RefPlan& RP(void* h) { return *static_cast<RefPlan*>(h); }
+double ref_plan_gamma(void* h) { return RP(h).gamma; }
+int ref_plan_depth(void* h) { return RP(h).tree.depth; }
+long ref_plan_npairs(void* h) { return long(RP(h).prox.pairs.size()); }
+long ref_plan_nfar(void* h) { return long(RP(h).prox.far_nodes.size()); }
+long ref_plan_nsegs(void* h, int d) { return long(RP(h).plan.level_segs[d - 1].segs.size()); }
+
+// Position-dependent sequence hash sum_i splitmix64(v_i + splitmix64(i)) (mod 2^64), the
+// same as tests/golden/large_check.py:seq_hash (vectorisable on the checking side)
+static std::uint64_t splitmix64(std::uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    std::uint64_t z = x;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// the level's relevant (box, gamma) pairs in plan order: v_i = box << 32 | gamma
+unsigned long long ref_plan_segment_hash(void* h, int d) {
+    std::uint64_t x = 0, i = 0;
+    for (const auto& s : RP(h).plan.level_segs[d - 1].segs)
+        x += splitmix64(((std::uint64_t(std::uint32_t(s.box)) << 32) | std::uint32_t(s.gamma)) + splitmix64(i++));
+    return x;
+}
+
+// the Morton permutation
+unsigned long long ref_plan_perm_hash(void* h) {
+    std::uint64_t x = 0, i = 0;
+    for (std::uint32_t v : RP(h).tree.perm) x += splitmix64(std::uint64_t(v) + splitmix64(i++));
+    return x;
+}
+
+// S, D = IFGF far part + near-field neighbour sum - singular far-node corrections (no RP),
+// i.e. layer_potentials (solver.cpp:78-147) without its final rp_singular_apply. seconds2 gets
+// the wall time of ifgf_apply and of the near loop.
+int ref_plan_ifgf_near(void* h, const double* phi, double* S, double* D, double* seconds2) {
+    try {
+        const RefPlan& r = RP(h);
+        const SurfaceMesh& m = *r.mesh;
+        const std::size_t n = m.size();
+        const auto dens = to_cplx(phi, n);
+        double t0 = now_s();
+        std::vector<cplx> a(n);
+        for (std::size_t i = 0; i < n; ++i) a[i] = dens[i] * (m.jac[i] * m.weight[i]);
+        IfgfRequest req;
+        req.single_layer = true;
+        req.double_layer = true;
+        req.strategy = r.strategy;
+        IfgfOutputs far = ifgf_apply(r.plan, a, req, r.cfg.workers);
+        const double t_ifgf = now_s() - t0;
+        t0 = now_s();
+        const int D_ = r.tree.depth;
+        const auto& leaves = r.tree.levels[D_ - 1];
+        const auto& nbs = r.rel.neighbors[D_ - 1];
+        const auto& lop = r.tree.leaf_of_point();
+        const double k = r.cfg.k;
+        const int w = resolve_workers(r.cfg.workers);
+#pragma omp parallel for schedule(dynamic, 64) num_threads(w)
+        for (std::int64_t t = 0; t < std::int64_t(n); ++t) {
+            const std::uint32_t p0 = r.prox.target_pair_begin[t], p1 = r.prox.target_pair_begin[t + 1];
+            const Vec3 x = m.pos[t];
+            cplx s{}, d{};
+            for (std::int32_t nb : nbs[lop[t]])
+                for (std::uint32_t j = leaves[nb].begin; j < leaves[nb].end; ++j) {
+                    const std::uint32_t src = r.tree.perm[j];
+                    if (src == std::uint32_t(t)) continue;
+                    bool singular = false;  // the target's pairs are patch-ascending
+                    for (std::uint32_t pi = p0; pi < p1 && !singular; ++pi)
+                        singular = r.prox.pairs[pi].patch == m.patch_of[src];
+                    if (singular) continue;
+                    s += green(x, m.pos[src], k) * a[src];
+                    d += dlayer_kernel(x, m.pos[src], m.normal[src], k) * a[src];
+                }
+            for (std::uint32_t pi = p0; pi < p1; ++pi)
+                for (std::uint32_t f = r.prox.pairs[pi].far_begin; f < r.prox.pairs[pi].far_end; ++f) {
+                    const std::uint32_t src = r.prox.far_nodes[f];
+                    s -= green(x, m.pos[src], k) * a[src];
+                    d -= dlayer_kernel(x, m.pos[src], m.normal[src], k) * a[src];
+                }
+            const cplx fs = far.single[t] + s, fd = far.dbl[t] + d;
+            S[2 * t] = fs.real();
+            S[2 * t + 1] = fs.imag();
+            D[2 * t] = fd.real();
+            D[2 * t + 1] = fd.imag();
+        }
+        const double t_near = now_s() - t0;
+        if (seconds2) {
+            seconds2[0] = t_ifgf;
+            seconds2[1] = t_near;
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// RP singular correction of the given targets (ascending, original indices) through a
+// sub-ProximityMap holding only their pairs: beta_precompute + rp_singular_apply of the
+// reference. S/D receive ntarget values each; npairs_out the number of pairs used.
+int ref_plan_rp_sample(void* h, const double* phi, const long* targets, long ntarget, double* S, double* D,
+                       long* npairs_out, double* seconds) {
+    try {
+        const RefPlan& r = RP(h);
+        const SurfaceMesh& m = *r.mesh;
+        const std::size_t n = m.size();
+        ProximityMap sub;
+        sub.cfg = r.prox.cfg;
+        sub.delta = r.prox.delta;
+        sub.target_pair_begin.assign(n + 1, 0);
+        std::vector<char> take(n, 0);
+        for (long i = 0; i < ntarget; ++i) take[std::size_t(targets[i])] = 1;
+        for (std::size_t t = 0; t < n; ++t) {
+            sub.target_pair_begin[t] = std::uint32_t(sub.pairs.size());
+            if (!take[t]) continue;
+            for (std::uint32_t pi = r.prox.target_pair_begin[t]; pi < r.prox.target_pair_begin[t + 1]; ++pi) {
+                SingularPair sp = r.prox.pairs[pi];
+                sp.far_begin = sp.far_end = 0;  // far nodes are not used by the beta tables
+                sub.pairs.push_back(sp);
+            }
+        }
+        sub.target_pair_begin[n] = std::uint32_t(sub.pairs.size());
+        const double t0 = now_s();
+        const SingularPrecompute prec = beta_precompute(m, sub, r.cfg.k, r.cfg.workers);
+        std::vector<cplx> s(n), d(n);
+        rp_singular_apply(m, sub, prec, to_cplx(phi, n), s, d, r.cfg.workers);
+        if (seconds) *seconds = now_s() - t0;
+        for (long i = 0; i < ntarget; ++i) {
+            const std::size_t t = std::size_t(targets[i]);
+            S[2 * i] = s[t].real();
+            S[2 * i + 1] = s[t].imag();
+            D[2 * i] = d[t].real();
+            D[2 * i + 1] = d[t].imag();
+        }
+        if (npairs_out) *npairs_out = long(sub.pairs.size());
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 }  // extern "C"

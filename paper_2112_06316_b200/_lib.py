@@ -38,6 +38,7 @@ class IfgfConfig(C.Structure):
         ("device", C.c_int32),
         ("part_rank", C.c_int32),
         ("part_world", C.c_int32),
+        ("beta_cache_path", C.c_char_p),
     ]
 
 
@@ -100,6 +101,7 @@ _SIGS = {
     "ifgf_operator_get_beta": (C.c_int, [vp, u64_p, d_p, d_p]),
     "ifgf_operator_save_beta_cache": (C.c_int, [vp, C.c_char_p]),
     "ifgf_operator_load_beta_cache": (C.c_int, [vp, C.c_char_p]),
+    "ifgf_operator_beta_cache_hit": (C.c_int, [vp]),
     "ifgf_operator_upload_density": (C.c_int, [vp, d_p]),
     "ifgf_operator_time_applies": (C.c_int, [vp, C.c_int, C.c_int, d_p]),
     "ifgf_operator_time_phases": (C.c_int, [vp, d_p]),

@@ -57,6 +57,7 @@ struct ifgf_plan {
 
 struct ifgf_operator {
     double t_upload = 0, t_beta = 0;  // device setup phases (s)
+    bool beta_cache_hit = false;      // tables loaded from cfg.beta_cache_path
     std::shared_ptr<ifgf_plan> plan;
     std::unique_ptr<Engine> eng;
 };
@@ -224,6 +225,7 @@ void ifgf_config_default(ifgf_config* c) {
     c->device = 0;
     c->part_rank = 0;
     c->part_world = 1;
+    c->beta_cache_path = nullptr;
 }
 
 // ------------------------------------------------------------------ surfaces
@@ -681,12 +683,25 @@ int ifgf_operator_create(const ifgf_surface* s, const ifgf_config* cfg, ifgf_ope
         const auto t0 = std::chrono::steady_clock::now();
         op->eng = make_engine(*op->plan, cfg->device);
         const auto t1 = std::chrono::steady_clock::now();
-        op->eng->compute_beta();
+        // the reference ctor's cache policy (solver.cpp:64-74): a matching cache is used,
+        // otherwise the tables are computed and, with a path, written there
+        const bool cached = cfg->beta_cache_path && *cfg->beta_cache_path &&
+                            ifgf_operator_load_beta_cache(op.get(), cfg->beta_cache_path) == 1;
+        if (!cached) {
+            op->eng->compute_beta();
+            if (cfg->beta_cache_path && *cfg->beta_cache_path) {
+                const int rc = ifgf_operator_save_beta_cache(op.get(), cfg->beta_cache_path);
+                if (rc) throw EngineError(rc, g_error);
+            }
+        }
+        op->beta_cache_hit = cached;
         op->t_upload = std::chrono::duration<double>(t1 - t0).count();
         op->t_beta = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
         *out = op.release();
     });
 }
+
+int ifgf_operator_beta_cache_hit(const ifgf_operator* op) { return op && op->beta_cache_hit ? 1 : 0; }
 
 int ifgf_operator_from_plan(ifgf_plan* p, int device, int compute_beta, ifgf_operator** out) {
     return guarded([&] {

@@ -157,8 +157,12 @@ struct Engine::Impl {
         rp.beta_s = beta_s.as<double2>();
         rp.beta_d = beta_d.as<double2>();
         beta_sharded = owned != nullptr;
+        beta_stale = false;
+        beta_lo = own_lo;
+        beta_hi = own_hi;
         drop_graph();
     }
+    std::uint32_t beta_lo = 0, beta_hi = 0;  // owned range the sharded tables were built for
     // beta inputs
     DevBuf b_target, b_ubar, b_vbar, b_du, b_dv, b_orient, b_series_off, b_series, b_cutoff,
         b_gu, b_gwu, b_gv, b_gwv;
@@ -233,7 +237,9 @@ struct Engine::Impl {
     // full operator on d_phi -> out, S, D (device pointers). The near field and the RP
     // correction do not depend on the far field: they run on the side stream st2 into
     // (Sn, Dn) while the IFGF fills (Sp, Dp) on st; a combine kernel joins both.
-    int run_apply(const double2* phi, double2* out, double2* S, double2* D) {
+    // local_out (sharded GMRES): the owned outputs stay in out_m[own_lo, own_hi) (Morton
+    // order), no gather
+    int run_apply(const double2* phi, double2* out, double2* S, double2* D, bool local_out = false) {
         ensure_near_lists();
         int launches = 0;
         const std::size_t vb = n * sizeof(double2);
@@ -271,25 +277,24 @@ struct Engine::Impl {
         } else {
             launches += run_ifgf(true, true, strategy, nullptr, side_work);
         }
-        if (world > 1) reduce_far_to_owners();  // far-field partials -> target owners
+        if (collective()) launches += reduce_far_to_owners();  // far-field partials -> target owners
         IFGF_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
         RpDev r = rp;
-        if (world > 1) {  // owned targets in Morton order, then exchanged
+        if (collective()) {  // owned targets in Morton order, then exchanged
             r.out_m = out_m.as<double2>();
             S = D = nullptr;
         }
         launch_combine(r, phi, Sp.as<double2>(), Dp.as<double2>(), Sn.as<double2>(), Dn.as<double2>(), gamma, out, S,
                        D, st);
         ++launches;
-        if (world > 1) {
-            gather_out_from_owners();
-            launch_unpermute1(int(n), perm.as<std::uint32_t>(), out_m.as<double2>(), out, st);
-            ++launches;
-        }
+        if (collective() && !local_out) launches += gather_out_from_owners(out);
         return launches;
     }
 
+    bool beta_stale = false;
     void ensure_beta() {
+        if (beta_stale)
+            throw InternalError("beta tables are target-sharded for another Morton range: compute_beta again");
         if (!beta_ready) throw InternalError("beta tables not computed");
     }
 
@@ -351,6 +356,14 @@ struct Engine::Impl {
     // Morton range [lo, hi) of sources (and targets) owned by this engine; leaf-box aligned
     void set_partition(std::uint32_t lo, std::uint32_t hi) {
         if (lo > hi || hi > n) throw InvalidArgument("partition: bad Morton range");
+        // a per-rank plan holds only its own range's boxes: no other range is valid for it
+        if (cones->world > 1 && (lo != cones->bounds[cones->rank] || hi != cones->bounds[cones->rank + 1]))
+            throw InvalidArgument("partition: a per-rank plan only serves its own Morton range");
+        // target-sharded tables hold only the pairs of the range they were built for
+        if (beta_sharded && beta_ready && (lo != beta_lo || hi != beta_hi)) {
+            beta_ready = false;
+            beta_stale = true;
+        }
         own_lo = lo;
         own_hi = hi;
         partitioned = !(lo == 0 && hi == n);
@@ -388,32 +401,55 @@ struct Engine::Impl {
         return partition_sources(*tree, *rel, *cones, parts);
     }
 
-    void reduce_far_to_owners() {
-        IFGF_NCCL(ncclGroupStart());
-        for (int r = 0; r < world; ++r) {
-            const std::size_t off = bounds[r], cnt = 2 * std::size_t(bounds[r + 1] - bounds[r]);
-            if (!cnt) continue;
-            double* s = reinterpret_cast<double*>(Sp.as<double2>() + off);
-            double* d = reinterpret_cast<double*>(Dp.as<double2>() + off);
-            IFGF_NCCL(ncclReduce(s, s, cnt, ncclFloat64, ncclSum, r, comm, st));
-            IFGF_NCCL(ncclReduce(d, d, cnt, ncclFloat64, ncclSum, r, comm, st));
-        }
-        IFGF_NCCL(ncclGroupEnd());
+    // The per-apply exchange: ONE ncclReduceScatter of the far-field
+    // partials (S and D of every rank's range, padded to the longest range C) delivers each
+    // owner the sums over ranks of its targets, then ONE ncclAllGather of the owned outputs.
+    bool collective() const { return comm != nullptr; }
+    std::int64_t chunk = 0;  // C: the longest owned range
+    DevBuf ex_send, ex_recv, ag_send, ag_recv, d_bounds;
+
+    void alloc_exchange() {
+        chunk = 0;
+        for (int r = 0; r < world; ++r) chunk = std::max<std::int64_t>(chunk, bounds[r + 1] - bounds[r]);
+        const std::size_t C = std::size_t(std::max<std::int64_t>(chunk, 1));
+        ex_send.alloc(std::size_t(world) * 2 * C * sizeof(double2));
+        ex_recv.alloc(2 * C * sizeof(double2));
+        ag_send.alloc(C * sizeof(double2));
+        ag_recv.alloc(std::size_t(world) * C * sizeof(double2));
+        d_bounds.upload(bounds);
     }
 
-    void gather_out_from_owners() {
-        IFGF_NCCL(ncclGroupStart());
-        for (int r = 0; r < world; ++r) {
-            const std::size_t off = bounds[r], cnt = 2 * std::size_t(bounds[r + 1] - bounds[r]);
-            if (!cnt) continue;
-            double* o = reinterpret_cast<double*>(out_m.as<double2>() + off);
-            IFGF_NCCL(ncclBroadcast(o, o, cnt, ncclFloat64, r, comm, st));
-        }
-        IFGF_NCCL(ncclGroupEnd());
+    int reduce_far_to_owners() {
+        const std::uint32_t* bd = d_bounds.as<std::uint32_t>();
+        launch_pack_ranges(Sp.as<double2>(), Dp.as<double2>(), bd, world, chunk, ex_send.as<double2>(), st);
+        IFGF_NCCL(ncclReduceScatter(ex_send.as<double>(), ex_recv.as<double>(), std::size_t(4 * chunk), ncclFloat64,
+                                    ncclSum, comm, st));
+        launch_unpack_owned(ex_recv.as<double2>(), own_lo, std::int64_t(own_hi - own_lo), chunk, Sp.as<double2>(),
+                            Dp.as<double2>(), st);
+        return 2;
     }
 
+    // this rank's owned Morton segment `seg` (own_hi - own_lo entries) -> every rank's
+    // original-order full vector `out`
+    int allgather_to_original(const double2* seg, double2* out) {
+        launch_copy_pad(seg, std::int64_t(own_hi - own_lo), chunk, ag_send.as<double2>(), st);
+        IFGF_NCCL(ncclAllGather(ag_send.as<double>(), ag_recv.as<double>(), std::size_t(2 * chunk), ncclFloat64, comm,
+                                st));
+        launch_unpermute_padded(std::int64_t(n), perm.as<std::uint32_t>(), d_bounds.as<std::uint32_t>(), world, chunk,
+                                ag_recv.as<double2>(), out, st);
+        return 2;
+    }
+    int gather_out_from_owners(double2* out) { return allgather_to_original(out_m.as<double2>() + own_lo, out); }
+
+    bool nccl_graph_failed = false;
     void apply_graph() {
-        if (world > 1) {  // collectives in flight: eager launches
+        // under a communicator the NCCL calls are captured with the kernels (one graph launch
+        // per apply on every rank); IFGF_NCCL_GRAPH=0 runs them eagerly
+        static const bool nccl_graph = [] {
+            const char* e = std::getenv("IFGF_NCCL_GRAPH");
+            return !(e && e[0] == '0');
+        }();
+        if (collective() && (!nccl_graph || nccl_graph_failed)) {
             kernels = run_apply(d_phi.as<double2>(), d_out.as<double2>(), d_S.as<double2>(), d_D.as<double2>());
             eager_done = true;
             return;
@@ -425,7 +461,16 @@ struct Engine::Impl {
             eager_done = true;
             cudaGraph_t g;
             IFGF_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-            run_apply(d_phi.as<double2>(), d_out.as<double2>(), d_S.as<double2>(), d_D.as<double2>());
+            try {
+                run_apply(d_phi.as<double2>(), d_out.as<double2>(), d_S.as<double2>(), d_D.as<double2>());
+            } catch (...) {
+                cudaStreamEndCapture(st, &g);
+                if (g) cudaGraphDestroy(g);
+                cudaGetLastError();
+                if (!collective()) throw;
+                nccl_graph_failed = true;  // this NCCL cannot be captured: eager from now on
+                return;
+            }
             IFGF_CUDA(cudaStreamEndCapture(st, &g));
             IFGF_CUDA(cudaGraphInstantiate(&graph, g, 0));
             IFGF_CUDA(cudaGraphDestroy(g));
@@ -1178,7 +1223,7 @@ void Engine::apply(const cplx* phi, cplx* out, cplx* S, cplx* D) {
     Impl& e = *d_;
     std::lock_guard<std::mutex> g(e.mu);
     e.ensure_beta();
-    if (e.world > 1 && (S || D))
+    if (e.collective() && (S || D))
         throw InvalidArgument("layer_potentials: S and D are target-distributed under a communicator");
     IFGF_CUDA(cudaSetDevice(e.dev));
     const std::size_t bytes = e.n * sizeof(double2);
@@ -1204,6 +1249,15 @@ void Engine::apply_device(const void* phi, void* out, void* S, void* D) {
 // Arnoldi step: V_j -> d_phi (device copy), one graph apply -> d_out = w, MGS against
 // V_0..V_j with the coefficients kept on the device, |w|, then ONE copy of the column
 // H[0..j+1] to the host for the rotations and the residual estimate.
+//
+// Under a communicator the solve is SHARDED by the operator's Morton ranges (SURVEY.md
+// §8(e), north_star "GMRES vector segments"): each rank keeps only its owned segment of
+// b, x, r and the Krylov basis (Morton order, (m+1) x n_owned), the apply all-gathers the
+// segment into the full density and returns only the owned outputs, and every inner product
+// and norm is a local partial sum followed by one ncclAllReduce of 2 doubles (modified
+// Gram-Schmidt keeps the reference's orthogonalisation order, so the iteration counts and
+// residual histories are the reference's). The Hessenberg column and the rotations are the
+// same on every rank.
 GmresOutcome Engine::gmres(const cplx* rhs, double tol, int max_iter, int restart) {
     Impl& e = *d_;
     std::lock_guard<std::mutex> g(e.mu);
@@ -1211,37 +1265,62 @@ GmresOutcome Engine::gmres(const cplx* rhs, double tol, int max_iter, int restar
     if (tol <= 0) throw InvalidArgument("gmres_solve: tolerance must be positive");
     if (max_iter < 0) throw InvalidArgument("gmres_solve: max_iter must be >= 0");
     IFGF_CUDA(cudaSetDevice(e.dev));
-    const std::int64_t n = std::int64_t(e.n);
+    const bool shard = e.collective();
+    const std::int64_t lo = shard ? std::int64_t(e.own_lo) : 0;
+    const std::int64_t n = shard ? std::int64_t(e.own_hi - e.own_lo) : std::int64_t(e.n);  // local length
     const std::size_t vb = std::size_t(n) * sizeof(double2);
+    const std::size_t vfull = e.n * sizeof(double2);
     const int m_max = restart > 0 ? std::min(restart, std::max(max_iter, 1)) : std::max(max_iter, 1);
     DevBuf b, x, r, V, H, partial, yv;
-    b.alloc(vb);
-    x.alloc(vb);
-    r.alloc(vb);
-    V.alloc(std::size_t(m_max + 1) * vb);
+    b.alloc(std::max<std::size_t>(vb, 16));
+    x.alloc(std::max<std::size_t>(vb, 16));
+    r.alloc(std::max<std::size_t>(vb, 16));
+    V.alloc(std::max<std::size_t>(std::size_t(m_max + 1) * vb, 16));
     H.alloc(std::size_t(m_max + 2) * sizeof(double2));
     partial.alloc(std::size_t(gmres_reduce_blocks()) * sizeof(double2));
     yv.alloc(std::size_t(m_max + 1) * sizeof(double2));
     cudaStream_t st = e.st;
-    IFGF_CUDA(cudaMemcpyAsync(b.as<void>(), rhs, vb, cudaMemcpyHostToDevice, st));
-    IFGF_CUDA(cudaMemsetAsync(x.as<void>(), 0, vb, st));
+    if (shard) {  // the owned Morton segment of rhs
+        IFGF_CUDA(cudaMemcpyAsync(e.scratch.as<void>(), rhs, vfull, cudaMemcpyHostToDevice, st));
+        launch_gather_local(e.perm.as<std::uint32_t>(), lo, n, e.scratch.as<double2>(), b.as<double2>(), st);
+    } else {
+        IFGF_CUDA(cudaMemcpyAsync(b.as<void>(), rhs, vb, cudaMemcpyHostToDevice, st));
+    }
+    IFGF_CUDA(cudaMemsetAsync(x.as<void>(), 0, std::max<std::size_t>(vb, 16), st));
     auto Vi = [&](int i) { return V.as<double2>() + std::size_t(i) * std::size_t(n); };
     auto read_h = [&](int cnt, std::vector<cplx>& dst) {
         dst.resize(cnt);
         IFGF_CUDA(cudaMemcpyAsync(dst.data(), H.as<void>(), cnt * sizeof(double2), cudaMemcpyDeviceToHost, st));
         IFGF_CUDA(cudaStreamSynchronize(st));
     };
-    auto apply_to = [&](const double2* in) {  // d_out = A in
-        IFGF_CUDA(cudaMemcpyAsync(e.d_phi.as<void>(), in, vb, cudaMemcpyDeviceToDevice, st));
-        e.apply_graph();
+    // the operator output of `in`: d_out (full) or, sharded, the owned segment of out_m
+    double2* w_out = shard ? e.out_m.as<double2>() + lo : e.d_out.as<double2>();
+    auto apply_to = [&](const double2* in) {
+        if (shard) {  // segments -> full density on every rank, owned outputs only
+            e.allgather_to_original(in, e.d_phi.as<double2>());
+            e.run_apply(e.d_phi.as<double2>(), e.d_out.as<double2>(), nullptr, nullptr, true);
+        } else {
+            IFGF_CUDA(cudaMemcpyAsync(e.d_phi.as<void>(), in, vb, cudaMemcpyDeviceToDevice, st));
+            e.apply_graph();
+        }
+    };
+    // dst = <a, b> (as_norm: ||a||) over the whole distributed vector
+    auto dot = [&](const double2* a, const double2* bb, double2* dst, bool as_norm) {
+        if (!shard) {
+            launch_cdot(n, a, bb, partial.as<double2>(), dst, as_norm, st);
+            return;
+        }
+        launch_cdot(n, a, bb, partial.as<double2>(), dst, false, st);
+        IFGF_NCCL(ncclAllReduce(dst, dst, 2, ncclFloat64, ncclSum, e.comm, st));
+        if (as_norm) launch_csqrt_re(dst, st);
     };
     std::vector<cplx> hcol;
-    launch_cdot(n, b.as<double2>(), b.as<double2>(), partial.as<double2>(), H.as<double2>(), true, st);
+    dot(b.as<double2>(), b.as<double2>(), H.as<double2>(), true);
     read_h(1, hcol);
     const double bnorm = hcol[0].real();
     GmresOutcome total;
     if (bnorm == 0.0) {
-        total.x.assign(std::size_t(n), cplx{});
+        total.x.assign(e.n, cplx{});
         total.converged = true;
         return total;
     }
@@ -1250,11 +1329,11 @@ GmresOutcome Engine::gmres(const cplx* rhs, double tol, int max_iter, int restar
     auto cycle = [&](int m, GmresOutcome& res) {
         if (x_nonzero) {
             apply_to(x.as<double2>());
-            launch_csub(n, b.as<double2>(), e.d_out.as<double2>(), r.as<double2>(), st);
-        } else {
+            launch_csub(n, b.as<double2>(), w_out, r.as<double2>(), st);
+        } else if (n > 0) {
             IFGF_CUDA(cudaMemcpyAsync(r.as<void>(), b.as<void>(), vb, cudaMemcpyDeviceToDevice, st));
         }
-        launch_cdot(n, r.as<double2>(), r.as<double2>(), partial.as<double2>(), H.as<double2>(), true, st);
+        dot(r.as<double2>(), r.as<double2>(), H.as<double2>(), true);
         read_h(1, hcol);
         const double beta = hcol[0].real();
         if (beta / bnorm <= tol) return true;
@@ -1264,13 +1343,13 @@ GmresOutcome Engine::gmres(const cplx* rhs, double tol, int max_iter, int restar
         gv[0] = beta;
         for (int j = 0; j < m; ++j) {
             apply_to(Vi(j));
-            double2* w = e.d_out.as<double2>();
+            double2* w = w_out;
             for (int i = 0; i <= j; ++i) {
                 double2* hi = H.as<double2>() + i;
-                launch_cdot(n, Vi(i), w, partial.as<double2>(), hi, false, st);
+                dot(Vi(i), w, hi, false);
                 launch_caxpy_dev(n, hi, w, Vi(i), st);
             }
-            launch_cdot(n, w, w, partial.as<double2>(), H.as<double2>() + j + 1, true, st);
+            dot(w, w, H.as<double2>() + j + 1, true);
             read_h(j + 2, hcol);
             Hh.push_back(hcol);
             std::vector<cplx>& Hj = Hh.back();
@@ -1335,8 +1414,13 @@ GmresOutcome Engine::gmres(const cplx* rhs, double tol, int max_iter, int restar
         h.insert(h.end(), f.history.begin(), f.history.end());
         throw ConvergenceFailure(f.what(), h);
     }
-    total.x.resize(std::size_t(n));
-    IFGF_CUDA(cudaMemcpyAsync(total.x.data(), x.as<void>(), vb, cudaMemcpyDeviceToHost, st));
+    total.x.resize(e.n);
+    if (shard) {  // every rank returns the full solution (original order)
+        e.allgather_to_original(x.as<double2>(), e.scratch.as<double2>());
+        IFGF_CUDA(cudaMemcpyAsync(total.x.data(), e.scratch.as<void>(), vfull, cudaMemcpyDeviceToHost, st));
+    } else {
+        IFGF_CUDA(cudaMemcpyAsync(total.x.data(), x.as<void>(), vb, cudaMemcpyDeviceToHost, st));
+    }
     IFGF_CUDA(cudaStreamSynchronize(st));
     return total;
 }
@@ -1531,7 +1615,7 @@ int Engine::kernels_per_apply() const {
     // weights + leaf + cousin per level + parent per level > 3 + near + coeffs + rp + combine
     // (+ the output un-permute under a communicator)
     const int ifgf = e.depth < 3 ? 0 : 1 + (e.depth - 2) + (e.depth - 3);
-    return 1 + ifgf + 3 + 1 + (e.world > 1 ? 1 : 0);
+    return 1 + ifgf + 3 + 1 + (e.collective() ? 4 : 0);
 }
 
 std::string Engine::describe() const {
@@ -1570,6 +1654,7 @@ void Engine::set_comm(int rank, int world, const void* unique_id) {
     e.world = world;
     e.bounds = e.partition(world);
     e.set_partition(e.bounds[rank], e.bounds[rank + 1]);
+    e.alloc_exchange();
 }
 
 void Engine::finish_owned(const cplx* phi, const cplx* far_S, const cplx* far_D, cplx* out) {

@@ -99,6 +99,20 @@ void launch_rp_accum(const RpDev& R, const double2* coeffs, double2* Sn, double2
 void launch_combine(const RpDev& R, const double2* phi, const double2* Sp, const double2* Dp, const double2* Sn,
                     const double2* Dn, double gamma, double2* out, double2* S, double2* D, cudaStream_t st);
 
+// multi-GPU exchange layouts (exchange_kernels.cu): each rank's Morton range padded to C
+void launch_pack_ranges(const double2* Sp, const double2* Dp, const std::uint32_t* bounds, int world,
+                        std::int64_t C, double2* send, cudaStream_t st);  // send[r][S|D][C]
+void launch_unpack_owned(const double2* recv, std::int64_t lo, std::int64_t cnt, std::int64_t C, double2* Sp,
+                         double2* Dp, cudaStream_t st);
+void launch_copy_pad(const double2* src, std::int64_t cnt, std::int64_t C, double2* dst, cudaStream_t st);
+// out[perm[t]] = recv[r(t) C + t - bounds[r(t)]]
+void launch_unpermute_padded(std::int64_t n, const std::uint32_t* perm, const std::uint32_t* bounds, int world,
+                             std::int64_t C, const double2* recv, double2* out, cudaStream_t st);
+// out[i] = in[perm[lo + i]], i < cnt (original-order vector -> owned Morton segment)
+void launch_gather_local(const std::uint32_t* perm, std::int64_t lo, std::int64_t cnt, const double2* in,
+                         double2* out, cudaStream_t st);
+void launch_csqrt_re(double2* h, cudaStream_t st);  // h = (sqrt(re h), 0)
+
 // device-resident GMRES vector kernels (gmres_kernels.cu); reductions deterministic
 int gmres_reduce_blocks();
 // dst = sum conj(a) b (as_norm: dst = (sqrt(re), 0)); partial holds gmres_reduce_blocks() entries

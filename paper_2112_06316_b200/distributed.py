@@ -4,10 +4,15 @@ NCCL inside the engine for the per-apply exchange.
 Each rank owns the sources and targets of a cost-balanced, leaf-aligned Morton range:
   1. IFGF far field of the owned sources onto ALL targets (leaf fill of owned leaves,
      parent fill and cousin evaluation only for boxes holding owned sources);
-  2. grouped ncclReduce of the far-field partials to the owner of each target range;
+  2. one ncclReduceScatter of the far-field partials (every rank's range padded to the
+     longest) to the owner of each target range;
   3. near field + RP + combine for the owned targets (every rank holds the full phi; the
      beta tables hold only the owned targets' pairs);
-  4. grouped ncclBroadcast of each owner's outputs, so every rank returns the full out.
+  4. one ncclAllGather of the owned outputs, so every rank returns the full out.
+The NCCL calls are captured into the apply's CUDA graph with the kernels. gmres_solve on
+this operator keeps only the owned Morton segment of every Krylov vector (one allreduce of
+2 doubles per inner product). At world 1 the same collective path runs (NCCL over a
+single-rank communicator), which is how it is exercised on one GPU.
 Each rank partitions with the same deterministic, plan-free cost model and then builds
 only its share of the cone plan, so the partition needs no communication; only the
 128-byte ncclUniqueId is broadcast.
@@ -57,8 +62,7 @@ class DistributedCombinedOperator(CombinedOperator):
             cfg = dataclasses.replace(cfg, part_rank=self.rank, part_world=self.world)
         super().__init__(mesh, cfg, compute_beta=False)
         uid = broadcast_unique_id(self.rank)
-        if self.world > 1:
-            self.set_comm(self.rank, self.world, uid)
+        self.set_comm(self.rank, self.world, uid)
         self.compute_beta()
         self.bounds = self.partition(self.world)
 

@@ -62,6 +62,7 @@ class SolveConfig:  # solver.hpp:32-45 (+ device)
     # per-rank plan of a multi-GPU run: only boxes with sources of this rank's Morton range
     part_rank: int = 0
     part_world: int = 1
+    beta_cache_path: str = ""  # solver.hpp:44: load the "rpbeta v1" cache or compute + save
 
     def to_c(self) -> IfgfConfig:
         c = IfgfConfig()
@@ -77,6 +78,7 @@ class SolveConfig:  # solver.hpp:32-45 (+ device)
         c.device = self.device
         c.part_rank = self.part_rank
         c.part_world = self.part_world
+        c.beta_cache_path = self.beta_cache_path.encode() if self.beta_cache_path else None
         return c
 
 
@@ -352,8 +354,21 @@ class CombinedOperator:
         return out
 
     def apply_into(self, phi: np.ndarray, out: np.ndarray) -> None:
-        """apply() into caller-owned (e.g. pinned) buffers, no allocation."""
+        """apply() into caller-owned (e.g. pinned) buffers, no allocation or copy. Both must be
+        C-contiguous complex128 of shape (n,) and out writeable (InvalidArgument otherwise, as
+        the reference's size checks, solver.cpp:82)."""
+        for name, v in (("phi", phi), ("out", out)):
+            if not isinstance(v, np.ndarray) or v.dtype != np.complex128 or v.shape != (self.n,) \
+                    or not v.flags.c_contiguous:
+                raise _lib.InvalidArgument(f"apply_into: {name} must be a C-contiguous complex128 array of shape ({self.n},)")
+        if not out.flags.writeable:
+            raise _lib.InvalidArgument("apply_into: out is not writeable")
         check(lib().ifgf_operator_apply(self._h, _ptr(phi), _ptr(out)), "apply")
+
+    @property
+    def beta_cache_hit(self) -> bool:
+        """the tables came from cfg.beta_cache_path (CombinedOperator::beta_cache_was_reused)"""
+        return lib().ifgf_operator_beta_cache_hit(self._h) == 1
 
     def layer_potentials(self, density):
         phi = _cvec(density, self.n)

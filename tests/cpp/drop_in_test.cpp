@@ -5,6 +5,7 @@
 // Built by oracle/Makefile into oracle/_ref/drop_in_test (links the reference = test infra).
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <numbers>
 #include <random>
 
@@ -90,6 +91,45 @@ int main() {
     check("point-source solve", ps_gpu.iterations == ps_ref.iterations &&
                                     rel_l2(ps_gpu.density, ps_ref.density) <= 1e-8,
           rel_l2(ps_gpu.density, ps_ref.density));
+
+    // non-convergence: the reference's solve() throws ConvergenceFailure with the residual
+    // history (solver.cpp:334-338); so must the GPU face
+    SolveConfig tight = scfg;
+    tight.tol = 1e-12;
+    tight.max_iter = 3;
+    std::vector<double> hist_ref, hist_gpu;
+    try {
+        (void)solve(mesh, inc, tight);
+    } catch (const ConvergenceFailure& f) {
+        hist_ref = f.residual_history;
+    }
+    try {
+        (void)gpu.solve(inc, tight);
+        check("non-convergence throws ConvergenceFailure", false, 0);
+    } catch (const ConvergenceFailure& f) {
+        hist_gpu = f.residual_history;
+        bool same = hist_gpu.size() == hist_ref.size() && hist_ref.size() == 3;
+        for (std::size_t i = 0; same && i < hist_ref.size(); ++i)
+            same = std::abs(hist_gpu[i] - hist_ref[i]) <= 1e-10 * hist_ref[i];
+        check("non-convergence throws ConvergenceFailure with the reference's history", same,
+              double(hist_gpu.size()));
+    }
+
+    // SolveConfig::beta_cache_path (solver.cpp:64-74): the first operator writes the cache, the
+    // second takes its tables from it, and the reference reads the same file
+    {
+        SolveConfig ccfg = cfg;
+        ccfg.beta_cache_path = "/tmp/ifgf_b200_dropin_beta.bin";
+        std::remove(ccfg.beta_cache_path.c_str());
+        ifgfb200::GpuCombinedOperator g1(mesh, ccfg);
+        ifgfb200::GpuCombinedOperator g2(mesh, ccfg);
+        CombinedOperator r2(mesh, ccfg);
+        check("beta cache written then reused", !g1.beta_cache_was_reused() && g2.beta_cache_was_reused() &&
+                                                    r2.beta_cache_was_reused(), 0);
+        check("apply with cached beta", rel_l2(g2.apply(phi), ref.apply(phi)) <= 1e-10,
+              rel_l2(g2.apply(phi), ref.apply(phi)));
+        std::remove(ccfg.beta_cache_path.c_str());
+    }
     std::printf("%d failure(s)\n", failures);
     return failures == 0 ? 0 : 1;
 }
