@@ -46,7 +46,8 @@ def main():
         h1, h2 = np.array(a.residual_history), np.array(b.residual_history)
         res[f"gmres_r{restart}"] = {
             "iters": [a.iterations, b.iterations], "converged": [a.converged, b.converged],
-            "hist_max_rel": float(np.max(np.abs(h1 - h2) / h1)) if len(h1) == len(h2) and len(h1) else None,
+            # the history is the relative residual |r_j| / |b|: differences are absolute in it
+            "hist_max_abs": float(np.max(np.abs(h1 - h2))) if len(h1) == len(h2) and len(h1) else None,
             "x_rel": float(np.linalg.norm(a.solution - b.solution) / np.linalg.norm(a.solution))}
     print("RESULT " + json.dumps(res), flush=True)
     dist.destroy_process_group()

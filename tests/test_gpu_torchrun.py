@@ -5,7 +5,8 @@ distributed apply runs — ncclReduceScatter of the padded far-field partials, t
 combine, ncclAllGather + un-permute, NCCL captured inside the CUDA graph — and so does the
 Morton-sharded GMRES (allreduce per inner product). At world 1 the collectives are identities,
 so the apply must equal the single-GPU apply bit for bit and GMRES must take the same
-iterations (the local Morton-order partial sums round differently: histories to 1e-10).
+iterations (the local Morton-order partial sums round differently: the relative-residual
+histories agree to 1e-12 absolute).
 The N > 1 layout logic is covered on CPU with gloo (tests/test_distributed_cpu.py)."""
 import json
 import os
@@ -42,5 +43,5 @@ def test_torchrun_world1_collective_path():
     for key in ("gmres_r0", "gmres_r5"):
         g = r[key]
         assert g["iters"][0] == g["iters"][1] and g["converged"][0] and g["converged"][1], g
-        assert g["hist_max_rel"] is not None and g["hist_max_rel"] <= 1e-10, g
+        assert g["hist_max_abs"] is not None and g["hist_max_abs"] <= 1e-12, g
         assert g["x_rel"] <= 1e-10, g
