@@ -12,6 +12,8 @@ struct PointsDev {
 };
 
 constexpr int kParentMergeMax = 2;  // parent segments per warp item (IFGF_PARENT_MERGE <= this; 3 measured slower)
+constexpr int kCbSegs = 12;         // parent segments per cell-batched parent item (parent_cb.cu)
+constexpr int kCbMaxGrp = 8;        // child-cell groups per (parent cell, octant) in a batched item
 
 struct LevelDev {
     int d = 0;
@@ -46,6 +48,20 @@ struct LevelDev {
     const std::int64_t* pitem_ev = nullptr;
     int n_pitem = 0;
     int pitem_merge = 1;  // segments per item (the kernel always reserves kParentMergeMax blocks)
+    // cell-batched parent work (parent_cb.cu, engine.cu "cell-batched parent items"): item i
+    // = up to kCbSegs parent segments of ONE parent cone cell (template slot cb_item_slot[i],
+    // segments cb_item_seg[i * kCbSegs + j], -1: none). Per (slot, octant): the 75 nodes in
+    // child-cell group order (cb_nodes), group starts (cb_gstart, kCbMaxGrp + 1 entries) and
+    // count (cb_ngrp). Per (item, j, octant): child box (cb_child) and per group the child
+    // segment (cb_cso, -1: none). Evaluations whose host-decided child segment differs from
+    // the template's group (ties) are exceptions: key j | octant << 8 | node << 16, cso.
+    int n_cbitem = 0;
+    const std::int32_t *cb_item_slot = nullptr, *cb_item_seg = nullptr;
+    const std::uint8_t *cb_nodes = nullptr, *cb_gstart = nullptr, *cb_ngrp = nullptr;
+    const std::int32_t *cb_child = nullptr, *cb_cso = nullptr;
+    const std::int64_t* cb_exc_begin = nullptr;
+    const std::uint32_t* cb_exc_key = nullptr;
+    const std::int32_t* cb_exc_cso = nullptr;
     const std::int32_t *ch_ptr = nullptr, *ch_idx = nullptr;  // children (level d+1) of this level's boxes
     const double *s_nodes = nullptr, *th_nodes = nullptr, *ph_nodes = nullptr;
     // sin/cos of the angular node tables (interpolation-node directions)

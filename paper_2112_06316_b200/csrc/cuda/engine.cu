@@ -78,6 +78,8 @@ struct LevelBufs {
         box_seg_begin, pev_begin, pev_seg, pev_perm, pgrp_begin, pgrp_seg, pgrp_start, pgrp_count, ch_ptr, ch_idx, s_nodes, th_nodes, ph_nodes, th_sin, th_cos, ph_sin, ph_cos, thc_cos, thc_sin, phc_cos, phc_sin,
         chunk_box, chunk_q0, wchunk_box, wchunk_q0, tmpl_slot, tmpl, seg_code, litem_seg0,
         litem_nseg, litem_split, litem_box0, litem_box1, pgrp_rec, pitem_seg, pitem_grp, pitem_ev;
+    DevBuf cb_item_slot, cb_item_seg, cb_nodes, cb_gstart, cb_ngrp, cb_child, cb_cso, cb_exc_begin, cb_exc_key,
+        cb_exc_cso;
 };
 
 Pipes make_pipes(const std::vector<int>& f) {
@@ -825,6 +827,155 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         }
     }
 
+    // ---- cell-batched parent items (parent_cb.cu): on levels with templates whose parent cone
+    // cells are each shared by >= 4 parent segments on average, the segments of one cell are
+    // batched (kCbSegs per CTA) into GEMMs against their children's blocks; the per-segment
+    // kernel below takes the remaining segments. Opt-in (IFGF_PARENT_CB=1; =force batches
+    // every template level): measured 2.2x SLOWER than the per-segment kernel at cfg2 (parent
+    // 18.7 vs 8.4 ms) — its per-item A-matrix build and block staging cost more instructions
+    // than the DMMAs they feed (profiles/r02d_parent_cb_ncu.txt).
+    std::vector<std::vector<std::uint8_t>> cb_seg_h(T.depth + 1);
+    {
+        const char* env = std::getenv("IFGF_PARENT_CB");
+        const bool enabled = env && env[0] != '0';
+        const bool force = env && std::string(env) == "force";
+        const bool dbg = std::getenv("IFGF_SETUP_DEBUG") != nullptr;
+        // tests: also route every n-th evaluation through the exception path (same segment)
+        const char* xenv = std::getenv("IFGF_PARENT_CB_EXC_EVERY");
+        const int exc_every = xenv ? std::max(0, std::atoi(xenv)) : 0;
+        for (int d = 4; enabled && d <= T.depth; ++d) {
+            const std::vector<std::int32_t>& slot = tmpl_slot_h[d];
+            const std::vector<std::int32_t>& gcs = tmpl_gc_h[d];
+            if (slot.empty() || gcs.empty()) continue;
+            const ConeLevel& PL = C.level[d - 2];
+            const ConeLevel& CL = C.level[d - 1];
+            constexpr int P = 75;
+            const int nslot = int(gcs.size() / (8 * P));
+            // per (slot, octant): nodes in child-cell order, group starts and cells
+            std::vector<std::uint8_t> nodes(std::size_t(nslot) * 8 * P), gstart(std::size_t(nslot) * 8 * (kCbMaxGrp + 1), P),
+                ngrp(std::size_t(nslot) * 8, 0), bad(nslot, 0), gpos(std::size_t(nslot) * 8 * P);
+            std::vector<std::int32_t> ggc(std::size_t(nslot) * 8 * kCbMaxGrp, -1);
+#pragma omp parallel for schedule(static)
+            for (int sl = 0; sl < nslot; ++sl)
+                for (int o = 0; o < 8; ++o) {
+                    const std::size_t so8 = std::size_t(sl) * 8 + o;
+                    std::array<std::pair<int, int>, P> v;
+                    for (int nd = 0; nd < P; ++nd) v[nd] = {gcs[so8 * P + nd], nd};
+                    std::stable_sort(v.begin(), v.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+                    int ng = 0;
+                    for (int i = 0; i < P; ++i) {
+                        if (i == 0 || v[i].first != v[i - 1].first) {
+                            if (ng == kCbMaxGrp) {
+                                bad[sl] = 1;
+                                break;
+                            }
+                            gstart[so8 * (kCbMaxGrp + 1) + ng] = std::uint8_t(i);
+                            ggc[so8 * kCbMaxGrp + ng] = v[i].first;
+                            ++ng;
+                        }
+                        nodes[so8 * P + i] = std::uint8_t(v[i].second);
+                        gpos[so8 * P + v[i].second] = std::uint8_t(ng - 1);  // group of node
+                    }
+                    ngrp[so8] = std::uint8_t(ng);
+                    gstart[so8 * (kCbMaxGrp + 1) + ng] = P;
+                }
+            std::vector<std::vector<std::int32_t>> by_slot(nslot);
+            for (std::size_t so = 0; so < PL.nseg(); ++so) {
+                const int sl = slot[PL.seg_gamma[so]];
+                if (sl >= 0 && !bad[sl]) by_slot[sl].push_back(std::int32_t(so));
+            }
+            std::size_t cnt = 0, used = 0;
+            for (const auto& v : by_slot) {
+                cnt += v.size();
+                used += v.empty() ? 0 : 1;
+            }
+            if (!force && cnt < 4 * used) continue;  // cells too rarely shared at this level
+            std::vector<std::int32_t> item_slot, item_seg;
+            for (int sl = 0; sl < nslot; ++sl)
+                for (std::size_t a = 0; a < by_slot[sl].size(); a += kCbSegs) {
+                    item_slot.push_back(sl);
+                    for (int j = 0; j < kCbSegs; ++j)
+                        item_seg.push_back(a + j < by_slot[sl].size() ? by_slot[sl][a + j] : -1);
+                }
+            const std::int64_t n_item = std::int64_t(item_slot.size());
+            const auto& cptr = C.child_ptr[d - 2];
+            const auto& cidx = C.child_idx[d - 2];
+            std::vector<std::int32_t> child(std::size_t(n_item) * kCbSegs * 8, -1),
+                cso(std::size_t(n_item) * kCbSegs * 8 * kCbMaxGrp, -1);
+            std::vector<std::vector<std::pair<std::uint32_t, std::int32_t>>> exc(n_item);
+            auto ordinal = [&](int ch, int gam) {
+                const auto b0 = CL.seg_gamma.begin() + CL.box_seg_begin[ch];
+                const auto b1 = CL.seg_gamma.begin() + CL.box_seg_begin[ch + 1];
+                const auto it = std::lower_bound(b0, b1, gam);
+                return (it == b1 || *it != gam) ? -1 : std::int32_t(it - CL.seg_gamma.begin());
+            };
+#pragma omp parallel for schedule(dynamic, 256)
+            for (std::int64_t it = 0; it < n_item; ++it) {
+                const int sl = item_slot[it];
+                for (int j = 0; j < kCbSegs; ++j) {
+                    const int so = item_seg[it * kCbSegs + j];
+                    if (so < 0) continue;
+                    const int pb = PL.seg_box[so];
+                    const int nch = cptr[pb + 1] - cptr[pb];
+                    const Vec3 pc = T.center(d - 1, std::size_t(pb));
+                    for (int c = 0; c < nch; ++c) {
+                        const int ch = cidx[cptr[pb] + c];
+                        const Vec3 cc = T.center(d, std::size_t(ch));
+                        const int o = (cc.x > pc.x ? 1 : 0) | (cc.y > pc.y ? 2 : 0) | (cc.z > pc.z ? 4 : 0);
+                        const std::size_t so8 = std::size_t(sl) * 8 + o;
+                        child[(std::size_t(it) * kCbSegs + j) * 8 + o] = ch;
+                        std::int32_t* cg = cso.data() + ((std::size_t(it) * kCbSegs + j) * 8 + o) * kCbMaxGrp;
+                        for (int g = 0; g < ngrp[so8]; ++g) cg[g] = ordinal(ch, ggc[so8 * kCbMaxGrp + g]);
+                        for (int nd = 0; nd < P; ++nd) {
+                            const std::int32_t host = CL.pev_seg[CL.pev_begin[so] + std::int64_t(nd) * nch + c];
+                            if (host != cg[gpos[so8 * P + nd]] || (exc_every > 0 && (nd + j + o) % exc_every == 0))
+                                exc[it].push_back({std::uint32_t(j) | (std::uint32_t(o) << 8) | (std::uint32_t(nd) << 16), host});
+                        }
+                    }
+                }
+            }
+            std::vector<std::int64_t> exc_begin(n_item + 1, 0);
+            for (std::int64_t it = 0; it < n_item; ++it) exc_begin[it + 1] = exc_begin[it] + std::int64_t(exc[it].size());
+            std::vector<std::uint32_t> exc_key(static_cast<std::size_t>(exc_begin[n_item]));
+            std::vector<std::int32_t> exc_cso(exc_key.size());
+            for (std::int64_t it = 0; it < n_item; ++it)
+                for (std::size_t x = 0; x < exc[it].size(); ++x) {
+                    exc_key[std::size_t(exc_begin[it]) + x] = exc[it][x].first;
+                    exc_cso[std::size_t(exc_begin[it]) + x] = exc[it][x].second;
+                }
+            std::vector<std::uint8_t>& done = cb_seg_h[d];
+            done.assign(PL.nseg(), 0);
+            for (std::int32_t so : item_seg)
+                if (so >= 0) done[so] = 1;
+            if (dbg)
+                std::fprintf(stderr, "cell-batched parent level %d: %zu of %zu segments in %lld items, %zu cells, %zu exceptions\n",
+                             d - 1, cnt, PL.nseg(), (long long)n_item, used, exc_key.size());
+            LevelBufs& b = e.lb[d - 1];
+            b.cb_item_slot.upload(item_slot);
+            b.cb_item_seg.upload(item_seg);
+            b.cb_nodes.upload(nodes);
+            b.cb_gstart.upload(gstart);
+            b.cb_ngrp.upload(ngrp);
+            b.cb_child.upload(child);
+            b.cb_cso.upload(cso);
+            b.cb_exc_begin.upload(exc_begin);
+            b.cb_exc_key.upload(exc_key);
+            b.cb_exc_cso.upload(exc_cso);
+            LevelDev& L = e.L[d - 1];
+            L.n_cbitem = int(n_item);
+            L.cb_item_slot = b.cb_item_slot.as<std::int32_t>();
+            L.cb_item_seg = b.cb_item_seg.as<std::int32_t>();
+            L.cb_nodes = b.cb_nodes.as<std::uint8_t>();
+            L.cb_gstart = b.cb_gstart.as<std::uint8_t>();
+            L.cb_ngrp = b.cb_ngrp.as<std::uint8_t>();
+            L.cb_child = b.cb_child.as<std::int32_t>();
+            L.cb_cso = b.cb_cso.as<std::int32_t>();
+            L.cb_exc_begin = b.cb_exc_begin.as<std::int64_t>();
+            L.cb_exc_key = b.cb_exc_key.as<std::uint32_t>();
+            L.cb_exc_cso = b.cb_exc_cso.as<std::int32_t>();
+        }
+    }
+
     // ---- parent work items (tensor-core parent kernel): up to `merge` relevant segments of one
     // parent box per warp (IFGF_PARENT_MERGE, default 2), with their child-segment groups merged
     // so that evaluations of the item's segments that land in the same child segment share
@@ -851,12 +1002,17 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
                 const int g1 = gam % L.ns, rest = gam / L.ns;
                 return int(std::uint32_t(g1) | (std::uint32_t(rest % L.nc) << 8) | (std::uint32_t(rest / L.nc) << 19));
             };
-            // items: consecutive relevant segments of one parent box
-            std::vector<std::int32_t> item_seg;
-            for (std::size_t pb = 0; pb + 1 < PL.box_seg_begin.size(); ++pb)
-                for (int s0 = PL.box_seg_begin[pb]; s0 < PL.box_seg_begin[pb + 1]; s0 += merge)
+            // items: consecutive relevant segments of one parent box (those not cell-batched)
+            const std::vector<std::uint8_t>& cbd = cb_seg_h[d];
+            std::vector<std::int32_t> item_seg, rest;
+            for (std::size_t pb = 0; pb + 1 < PL.box_seg_begin.size(); ++pb) {
+                rest.clear();
+                for (int s = PL.box_seg_begin[pb]; s < PL.box_seg_begin[pb + 1]; ++s)
+                    if (cbd.empty() || !cbd[s]) rest.push_back(s);
+                for (std::size_t s0 = 0; s0 < rest.size(); s0 += merge)
                     for (int w = 0; w < kParentMergeMax; ++w)
-                        item_seg.push_back(w < merge && s0 + w < PL.box_seg_begin[pb + 1] ? s0 + w : -1);
+                        item_seg.push_back(w < merge && s0 + w < rest.size() ? rest[s0 + w] : -1);
+            }
             const std::int64_t n_item = std::int64_t(item_seg.size()) / kParentMergeMax;
             // an item's groups: (child segment, item-local segment, group), ordered by child
             // segment, then segment (stable)

@@ -35,6 +35,10 @@ int leaf_item_tile();
 bool launch_leaf_fill_ray(const LevelDev& L, const PointsDev& P, const double2* a_p, double k, const Pipes& pipes,
                           const double* Ms, const double* Ma, double2* store, cudaStream_t st);
 // FP64 tensor-core parent fill (parent_tc.cu) for ps = 3, pang = 5; false if not applicable
+// cell-batched items of the level (Lc.n_cbitem), false when there are none
+bool launch_parent_fill_cb(const LevelDev& Lp, const LevelDev& Lc, const double2* child_store, double k,
+                           const Pipes& parent_pipes, const Pipes& child_pipes, const double* Ms, const double* Ma,
+                           double2* parent_store, cudaStream_t st);
 bool launch_parent_fill_tc(const LevelDev& Lp, const LevelDev& Lc, const double2* child_store, double k,
                            const Pipes& parent_pipes, const Pipes& child_pipes, const double* Ms,
                            const double* Ma, double2* parent_store, cudaStream_t st);

@@ -30,7 +30,8 @@ def test_nondefault_orders(ref, ps, pang):
 
 
 @pytest.mark.parametrize("env,value", [("IFGF_PARENT_TEMPLATES", "force"), ("IFGF_PARENT_TEMPLATES", "0"),
-                                       ("IFGF_COUSIN_TC", "0")])
+                                       ("IFGF_COUSIN_TC", "0"), ("IFGF_PARENT_CB", "1"),
+                                       ("IFGF_PARENT_CB", "force")])
 @pytest.mark.parametrize("splits,nu,k", [(2, 6, 4 * np.pi), (2, 16, 4 * np.pi), (3, 6, 8 * np.pi)])
 def test_kernel_variants(ref, monkeypatch, env, value, splits, nu, k):
     monkeypatch.setenv(env, value)  # read when the operator (and its kernels) are set up
@@ -40,6 +41,35 @@ def test_kernel_variants(ref, monkeypatch, env, value, splits, nu, k):
     ro = ref.RefOperator(rm, k)
     phi = P.random_density(pm.size(), 2)
     assert rel_l2(op.apply(phi), ro.apply(phi)) <= TOL
+
+
+@pytest.mark.parametrize("strategy", ["hybrid", "w4", "w2w3"])
+def test_parent_cell_batched_equals_per_segment(monkeypatch, strategy):
+    # the cell-batched parent fill (parent_cb.cu: segments of one cone cell as GEMMs against
+    # their children's blocks) against the per-segment kernel, on every pipe combination the
+    # strategies produce (S only, D only, both), with extra evaluations routed through its
+    # one-by-one exception path; equal to rounding
+    pm = P.SurfaceMesh.sphere(1.0, 3, 8, 8)
+    k = 8 * np.pi
+    st = {"hybrid": P.DlStrategy.Hybrid, "w4": P.DlStrategy.W4, "w2w3": P.DlStrategy.W2W3}[strategy]
+    nd = pm.nodes()
+    a = P.random_density(pm.size(), 6) * nd["jac"] * nd["weight"]
+    res = {}
+    for mode, extra in (("0", None), ("force", None), ("force", "7")):
+        monkeypatch.setenv("IFGF_PARENT_CB", mode)
+        if extra:
+            monkeypatch.setenv("IFGF_PARENT_CB_EXC_EVERY", extra)
+        else:
+            monkeypatch.delenv("IFGF_PARENT_CB_EXC_EVERY", raising=False)
+        op = P.CombinedOperator(pm, P.SolveConfig(k=k, dl_strategy=st))
+        res[(mode, extra)] = [op.ifgf_apply(a, s, d) for s, d in ((True, True), (True, False), (False, True))]
+    base = res[("0", None)]
+    for key in (("force", None), ("force", "7")):
+        for (S0, D0), (S1, D1), which in zip(base, res[key], ("both", "S", "D")):
+            if which != "D":
+                assert rel_l2(S1, S0) <= 1e-13, (key, which)
+            if which != "S":
+                assert rel_l2(D1, D0) <= 1e-13, (key, which)
 
 
 @pytest.mark.parametrize("splits,nu,k", [(2, 6, 4 * np.pi), (3, 8, 8 * np.pi)])
