@@ -10,6 +10,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <array>
 #include <atomic>
@@ -39,6 +40,83 @@ namespace {
 
 constexpr int kChunk = 128;  // targets per CTA in the cousin / near-field work lists
 
+// Host -> HBM uploads through pinned staging buffers: the host threads copy chunk i into one
+// pinned buffer while the copy engine moves chunk i - 1 from the other (a synchronous
+// pageable cudaMemcpy per array ran at ~4 GB/s: 15 s of cfg3's setup). Inside an
+// UploadBatch the copies are left in flight and the batch waits once at its end; outside
+// one every upload waits for its own copies.
+class Uploader {
+  public:
+    static Uploader& get() {
+        thread_local Uploader u;
+        int dev = 0;
+        IFGF_CUDA(cudaGetDevice(&dev));
+        if (u.dev_ != dev) u.init(dev);
+        return u;
+    }
+    void copy(void* dst, const void* src, std::size_t bytes) {
+        if (bytes < (std::size_t(1) << 20)) {  // small: not worth the staging
+            IFGF_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st_));
+            if (!batch_) IFGF_CUDA(cudaStreamSynchronize(st_));
+            return;
+        }
+        for (std::size_t off = 0; off < bytes; off += kChunk) {
+            const std::size_t len = std::min(kChunk, bytes - off);
+            IFGF_CUDA(cudaEventSynchronize(ev_[cur_]));  // this buffer's previous copy is done
+            char* pin = pin_[cur_];
+            const char* s = static_cast<const char*>(src) + off;
+            const std::int64_t parts = std::int64_t((len + (std::size_t(4) << 20) - 1) >> 22);
+#pragma omp parallel for schedule(static) num_threads(16)
+            for (std::int64_t q = 0; q < parts; ++q) {
+                const std::size_t a = std::size_t(q) << 22, n = std::min(std::size_t(4) << 20, len - a);
+                std::memcpy(pin + a, s + a, n);
+            }
+            IFGF_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, pin, len, cudaMemcpyHostToDevice, st_));
+            IFGF_CUDA(cudaEventRecord(ev_[cur_], st_));
+            cur_ ^= 1;
+        }
+        if (!batch_) IFGF_CUDA(cudaStreamSynchronize(st_));
+    }
+    void begin_batch() { ++batch_; }
+    cudaError_t end_batch() noexcept {  // called from a destructor: reports, never throws
+        return --batch_ == 0 ? cudaStreamSynchronize(st_) : cudaSuccess;
+    }
+    ~Uploader() { release(); }
+
+  private:
+    static constexpr std::size_t kChunk = std::size_t(64) << 20;
+    void release() {
+        for (int i = 0; i < 2; ++i) {
+            if (pin_[i]) cudaFreeHost(pin_[i]);
+            if (ev_[i]) cudaEventDestroy(ev_[i]);
+            pin_[i] = nullptr;
+            ev_[i] = nullptr;
+        }
+        if (st_) cudaStreamDestroy(st_);
+        st_ = nullptr;
+        cur_ = 0;
+    }
+    void init(int dev) {
+        release();
+        dev_ = dev;
+        IFGF_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            IFGF_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&pin_[i]), kChunk, cudaHostAllocDefault));
+            IFGF_CUDA(cudaEventCreateWithFlags(&ev_[i], cudaEventDisableTiming));
+        }
+    }
+    int dev_ = -1, cur_ = 0, batch_ = 0;
+    cudaStream_t st_ = nullptr;
+    char* pin_[2] = {nullptr, nullptr};
+    cudaEvent_t ev_[2] = {nullptr, nullptr};
+};
+
+struct UploadBatch {
+    Uploader& u;
+    UploadBatch() : u(Uploader::get()) { u.begin_batch(); }
+    ~UploadBatch() { (void)u.end_batch(); }  // the engine's final cudaDeviceSynchronize reports errors
+};
+
 class DevBuf {
   public:
     DevBuf() = default;
@@ -60,7 +138,7 @@ class DevBuf {
     template <class T>
     void upload(const std::vector<T>& v) {
         alloc(v.size() * sizeof(T));
-        if (!v.empty()) IFGF_CUDA(cudaMemcpy(p_, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+        if (!v.empty()) Uploader::get().copy(p_, v.data(), v.size() * sizeof(T));
     }
     template <class T>
     T* as() const {
@@ -122,6 +200,30 @@ struct Engine::Impl {
     DevBuf Ms, Ma;
     DevBuf storeA, storeB;
     std::size_t store_elems = 0;
+    std::size_t capA = 0, capB = 0;  // complex entries of the two stores
+    // The IFGF stores alternate: level d lives in storeA when D - d is even (the leaf level,
+    // then every second level), else in storeB. Each is sized for ITS levels' segments x
+    // pipes of the request (cfg3: 11.5 + 8.5 GB instead of 2 x 13 GB for 3 pipes everywhere);
+    // a request with more pipes (another strategy) grows them, dropping the captured graph.
+    void ensure_stores(bool single, bool dbl, DlStrategy s, int leaf_pipes = -1) {
+        std::size_t a = 1, b = 1;
+        for (int d = 3; d <= depth; ++d) {
+            const int np = (d == depth && leaf_pipes > 0) ? leaf_pipes : int(pipes_at(d, single, dbl, s).size());
+            const std::size_t need = std::size_t(L[d - 1].nseg) * std::size_t(L[d - 1].ps * L[d - 1].pang * L[d - 1].pang) * np;
+            ((depth - d) % 2 == 0 ? a : b) = std::max((depth - d) % 2 == 0 ? a : b, need);
+        }
+        if (a > capA) {
+            storeA.alloc(a * sizeof(double2));
+            capA = a;
+            drop_graph();
+        }
+        if (b > capB) {
+            storeB.alloc(b * sizeof(double2));
+            capB = b;
+            drop_graph();
+        }
+        store_elems = std::max(capA, capB);
+    }
     // near field
     DevBuf nb_ptr, nb_idx, leaf_of_m, tpb, pair_patch, far_begin, far_end, far_pos, near_chunk_box, near_chunk_q0;
     DevBuf near_off, near_src;  // near lists (ensure_near_lists)
@@ -304,7 +406,7 @@ struct Engine::Impl {
     // exclusions) runs once, on the device, and its compacted sources are kept in HBM (4 bytes
     // per near pair) so the per-apply near kernel only evaluates pairs. Built at the first
     // eager apply after construction or a partition change (never under graph capture);
-    // skipped when the lists would take more than a quarter of the free HBM, or with
+    // skipped when the lists would not leave the reserve below free in HBM, or with
     // IFGF_NEAR_LISTS=0.
     void ensure_near_lists() {
         if (near_lists_done) return;
@@ -331,7 +433,12 @@ struct Engine::Impl {
         IFGF_CUDA(cudaMemGetInfo(&free_b, &total_b));
         if (std::getenv("IFGF_SETUP_DEBUG"))
             std::fprintf(stderr, "near lists: %.2f GB, free %.2f GB\n", bytes / 1e9, free_b / 1e9);
-        if (bytes > free_b / 4) return;
+        // keep a reserve for the solver's Krylov basis and work vectors (GMRES at restart 50
+        // needs 51 x 16 N bytes): IFGF_NEAR_LISTS_RESERVE_GB, default max(6 GB, 51 x 16 N)
+        const char* renv = std::getenv("IFGF_NEAR_LISTS_RESERVE_GB");
+        const std::size_t reserve = renv ? std::size_t(std::atof(renv) * 1e9)
+                                         : std::max<std::size_t>(std::size_t(6e9), 51 * 16 * n);
+        if (bytes + reserve > free_b) return;
         near_off.upload(off);
         near_src.alloc(std::max<std::size_t>(std::size_t(off.back()), 1) * sizeof(std::int32_t));
         near.list_off = near_off.as<std::int64_t>();
@@ -486,6 +593,19 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
     Impl& e = *d_;
     e.dev = device;
     IFGF_CUDA(cudaSetDevice(device));
+    UploadBatch batch;  // plan uploads stay in flight until the end of the constructor
+    // IFGF_SETUP_DEBUG: host wall time of each setup phase (uploads are asynchronous)
+    const bool phase_dbg = std::getenv("IFGF_SETUP_DEBUG") != nullptr;
+    auto phase_t0 = std::chrono::steady_clock::now();
+    std::string phase_name = "start";
+    auto phase_mark = [&](const char* next) {
+        const auto t = std::chrono::steady_clock::now();
+        if (phase_dbg)
+            std::fprintf(stderr, "engine setup %-20s %.3f s\n", phase_name.c_str(),
+                         std::chrono::duration<double>(t - phase_t0).count());
+        phase_t0 = t;
+        phase_name = next;
+    };
     IFGF_CUDA(cudaStreamCreateWithFlags(&e.st, cudaStreamNonBlocking));
     IFGF_CUDA(cudaStreamCreateWithFlags(&e.st2, cudaStreamNonBlocking));
     IFGF_CUDA(cudaEventCreateWithFlags(&e.ev_fork, cudaEventDisableTiming));
@@ -516,6 +636,7 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
     e.pang = C.params.pang;
     const std::size_t n = e.n;
 
+    phase_mark("points");
     // ---- points in Morton order
     {
         std::vector<double> x(n), y(n), z(n), nx(n), ny(n), nz(n), jw(n), one(n, 1.0);
@@ -579,6 +700,7 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         e.opatch.upload(S.patch_of);
     }
 
+    phase_mark("levels");
     // ---- IFGF levels
     e.lb.resize(T.depth);
     e.L.resize(T.depth);
@@ -782,12 +904,12 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         L.max_pts = max_pts;
         store = std::max(store, CL.nseg() * std::size_t(CL.nodes_per_seg()) * 3);
     }
-    e.store_elems = store;
-    e.storeA.alloc(std::max<std::size_t>(store, 1) * sizeof(double2));
-    e.storeB.alloc(std::max<std::size_t>(store, 1) * sizeof(double2));
+    (void)store;
+    e.ensure_stores(true, true, e.strategy);
     e.Ms.upload(cheb::transform(e.ps));
     e.Ma.upload(cheb::transform(e.pang));
 
+    phase_mark("templates");
     // ---- parent-fill geometry templates on every level whose table is at most 8 GiB and has
     // no more entries than the level has evaluations (measured: templates on every level beat
     // building them only where each entry serves >= 8 evaluations, cfg2 8.97 -> 8.69 ms,
@@ -827,6 +949,7 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         }
     }
 
+    phase_mark("cell-batched items");
     // ---- cell-batched parent items (parent_cb.cu): on levels with templates whose parent cone
     // cells are each shared by >= 4 parent segments on average, the segments of one cell are
     // batched (kCbSegs per CTA) into GEMMs against their children's blocks; the per-segment
@@ -976,6 +1099,7 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         }
     }
 
+    phase_mark("parent items");
     // ---- parent work items (tensor-core parent kernel): up to `merge` relevant segments of one
     // parent box per warp (IFGF_PARENT_MERGE, default 2), with their child-segment groups merged
     // so that evaluations of the item's segments that land in the same child segment share
@@ -1114,6 +1238,7 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         }
     }
 
+    phase_mark("near field");
     // ---- near field
     {
         const int D = T.depth;
@@ -1169,6 +1294,7 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         N.nchunk = int(chunk_box.size());
     }
 
+    phase_mark("rp");
     // ---- RP: patch transforms, pair lists; beta offsets
     {
         const std::size_t nq = S.patches.size();
@@ -1247,6 +1373,7 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         cheb::fejer(PL.cfg.n_beta, e.rule_x, e.rule_w);
     }
 
+    phase_mark("work vectors");
     // ---- direct-sum view and work vectors
     e.direct = {int(n), e.ox.as<double>(), e.oy.as<double>(), e.oz.as<double>(), e.onx.as<double>(),
                 e.ony.as<double>(), e.onz.as<double>(), e.ojw.as<double>(), e.opatch.as<std::int32_t>(),
@@ -1257,7 +1384,9 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
     e.own_lo = 0;
     e.own_hi = std::uint32_t(n);
     e.bounds = {0u, std::uint32_t(n)};
+    phase_mark("device sync");
     IFGF_CUDA(cudaDeviceSynchronize());
+    phase_mark("end");
 }
 
 Engine::~Engine() {
@@ -1591,6 +1720,7 @@ void Engine::ifgf_apply(const cplx* a, bool single, bool dbl, DlStrategy s, cplx
     IFGF_CUDA(cudaMemsetAsync(e.Dp.as<void>(), 0, bytes, e.st));
     launch_weights(int(e.n), e.perm.as<std::uint32_t>(), e.d_phi.as<double2>(), e.ones_p.as<double>(),
                    e.a_p.as<double2>(), e.st);
+    e.ensure_stores(single, dbl, s);
     e.run_ifgf(single, dbl, s);
     launch_unpermute(int(e.n), e.perm.as<std::uint32_t>(), e.Sp.as<double2>(), e.Dp.as<double2>(),
                      e.d_S.as<double2>(), e.d_D.as<double2>(), e.st);
@@ -1608,6 +1738,7 @@ void Engine::level_d_fill(const cplx* a_perm, const std::vector<int>& pipes, std
     if (pipes.empty() || pipes.size() > 3) throw InvalidArgument("level_d_fill: 1..3 pipelines");
     const LevelDev& L = e.L[e.depth - 1];
     const std::size_t total = std::size_t(L.nseg) * (L.ps * L.pang * L.pang) * pipes.size();
+    e.ensure_stores(true, true, e.strategy, int(pipes.size()));
     IFGF_CUDA(cudaMemcpyAsync(e.a_p.as<void>(), a_perm, e.n * sizeof(double2), cudaMemcpyHostToDevice, e.st));
     launch_leaf_fill(L, e.P, e.a_p.as<double2>(), e.k, make_pipes(pipes), e.Ms.as<double>(),
                      e.Ma.as<double>(), e.storeA.as<double2>(), e.st);

@@ -12,7 +12,7 @@ splits, nu, k, gamma, desc = CONFIGS[name]
 t = time.perf_counter()
 mesh = make_mesh(name, P)
 op = P.CombinedOperator(mesh, P.SolveConfig(k=k, gamma=gamma))
-print(f"setup {time.perf_counter() - t:.1f}s N={mesh.size()}", flush=True)
+print(f"setup {time.perf_counter() - t:.1f}s N={mesh.size()} breakdown {op.setup_times()}", flush=True)
 op.upload_density(P.random_density(mesh.size(), 1))
 ms = op.time_applies(applies, flush_l2=False)
 print(f"{name}: {ms:.3f} ms/apply over {applies}; phases {op.time_phases()}", flush=True)
