@@ -8,10 +8,10 @@ TAG=${1:-prof}; CFG=${2:-cfg2}
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
 timeout 900 python bench.py --config $CFG --steps 20 --warmup 3 > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
 echo "bench rc=$?" >> gpurun_out/${TAG}_bench.err
-CMD="python bench.py --config $CFG --steps 2 --warmup 3 --no-cpu-baseline"
+CMD="python bench.py --config $CFG --steps 2 --warmup 3 --no-cpu-baseline --no-check"
 $CMD > gpurun_out/${TAG}_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu_launch.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"parent_tc|cousin_tc|leaf_ray|near_list|rp_accum" \
+ncu --set full --clock-control none --import-source on -k regex:"parent_tc|cousin_tc|leaf_ray|near_list|rp_accum|parent_cb" \
     -c 16 -o gpurun_out/${TAG}_prof $CMD > gpurun_out/${TAG}_ncu_full.log 2>&1
 echo "ncu rc=$?"; tail -3 gpurun_out/${TAG}_bench.err; tail -2 gpurun_out/${TAG}_ncu_full.log
