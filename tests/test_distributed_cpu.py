@@ -116,3 +116,82 @@ def test_per_rank_plans_over_gloo():
         assert union == F, d
     # pairs are classified for the owned targets only: the shares add up to the full list
     assert gathered[0][2] + gathered[1][2] == len(full.proximity()["target"])
+
+
+# ---- the per-apply exchange layout of the NCCL path (engine.cu reduce_far_to_owners /
+# allgather_to_original, exchange_kernels.cu), restated in numpy and run over gloo at world 2
+# with the real plan partition: each rank's Morton range padded to the longest range C;
+# reduce-scatter send [rank][S | D][C]; all-gather of the owned outputs, then
+# out[perm[t]] = recv[r(t) C + t - bounds[r(t)]]. (gloo has no reduce_scatter: all_reduce +
+# the rank's chunk is the same sum.)
+def _pack_ranges(Sp, Dp, bounds, C):
+    world = len(bounds) - 1
+    send = np.zeros((world, 2, C), complex)
+    for r in range(world):
+        lo, hi = bounds[r], bounds[r + 1]
+        send[r, 0, : hi - lo] = Sp[lo:hi]
+        send[r, 1, : hi - lo] = Dp[lo:hi]
+    return send
+
+
+def _exchange_worker(rank, world, port, q):
+    import torch
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2112_06316_b200 as P
+    from paper_2112_06316_b200.distributed import plan_partition
+
+    mesh = P.SurfaceMesh.sphere(1.0, 2, 8, 8)
+    plan = P.HostPlan(mesh, P.SolveConfig(k=4 * np.pi, device=-1))
+    bounds = [int(x) for x in plan_partition(plan, world)]
+    perm = plan.perm().astype(np.int64)
+    n = mesh.size()
+    C = max(bounds[r + 1] - bounds[r] for r in range(world))
+    rng = np.random.default_rng(100 + rank)
+    Sp = rng.standard_normal(n) + 1j * rng.standard_normal(n)  # this rank's far partials (Morton)
+    Dp = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    send = _pack_ranges(Sp, Dp, bounds, C)
+    t = torch.from_numpy(send.view(np.float64).copy())
+    dist.all_reduce(t)
+    mine = t.numpy().view(complex).reshape(world, 2, C)[rank]
+    lo, hi = bounds[rank], bounds[rank + 1]
+    S_owned, D_owned = mine[0, : hi - lo], mine[1, : hi - lo]
+    # owned outputs (here: S + D), padded, all-gathered, un-permuted into original order
+    seg = np.zeros(C, complex)
+    seg[: hi - lo] = S_owned + D_owned
+    out_t = [torch.zeros(2 * C, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(out_t, torch.from_numpy(seg.view(np.float64).copy()))
+    recv = np.concatenate([x.numpy().view(complex) for x in out_t])
+    out = np.zeros(n, complex)
+    for tt in range(n):
+        r = max(i for i in range(world) if bounds[i] <= tt) if tt < bounds[-1] else world - 1
+        out[perm[tt]] = recv[r * C + tt - bounds[r]]
+    q.put((rank, Sp, Dp, S_owned, D_owned, out, bounds, perm))
+    dist.destroy_process_group()
+
+
+def test_exchange_layout_world2():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_exchange_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    bounds, perm = res[0][6], res[0][7]
+    S_sum = sum(x[1] for x in res)
+    D_sum = sum(x[2] for x in res)
+    for r, Sp, Dp, S_owned, D_owned, out, _, _ in res:
+        lo, hi = bounds[r], bounds[r + 1]
+        assert np.allclose(S_owned, S_sum[lo:hi], rtol=0, atol=1e-12)  # every partial reached its owner
+        assert np.allclose(D_owned, D_sum[lo:hi], rtol=0, atol=1e-12)
+    want = np.zeros(len(perm), complex)
+    want[perm] = S_sum + D_sum  # original order
+    for x in res:
+        assert np.allclose(x[5], want, rtol=0, atol=1e-12)  # every rank holds the full output
