@@ -135,8 +135,8 @@ class DevBuf {
         bytes_ = bytes;
         if (bytes) IFGF_CUDA(cudaMalloc(&p_, bytes));
     }
-    template <class T>
-    void upload(const std::vector<T>& v) {
+    template <class T, class A>
+    void upload(const std::vector<T, A>& v) {
         alloc(v.size() * sizeof(T));
         if (!v.empty()) Uploader::get().copy(p_, v.data(), v.size() * sizeof(T));
     }
@@ -227,6 +227,7 @@ struct Engine::Impl {
     // near field
     DevBuf nb_ptr, nb_idx, leaf_of_m, tpb, pair_patch, far_begin, far_end, far_pos, near_chunk_box, near_chunk_q0;
     DevBuf near_off, near_src;  // near lists (ensure_near_lists)
+    DevBuf run_ptr, run_start, run_len, run_patch;  // neighbourhood patch runs (near_run_kernel)
     bool near_lists_done = false;
     NearDev near;
     // rp
@@ -418,8 +419,10 @@ struct Engine::Impl {
         near.list_src = nullptr;
         near_off.alloc(0);
         near_src.alloc(0);
-        const char* env = std::getenv("IFGF_NEAR_LISTS");
-        if ((env && env[0] == '0') || !near.leaf_of_m || near.n == 0) return;
+        // lists unless another near kernel is requested (IFGF_NEAR=runs | screen | thread);
+        // where they do not fit, the patch-run kernel (no per-pair data) takes over
+        const char* env = std::getenv("IFGF_NEAR");
+        if ((env && std::string(env) != "lists") || !near.leaf_of_m || near.n == 0) return;
         DevBuf cnt;
         cnt.alloc(std::size_t(near.n) * sizeof(std::int32_t));
         launch_near_list_count(near, P, cnt.as<std::int32_t>(), st);
@@ -935,7 +938,7 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
                 std::fprintf(stderr, "templates level %d: entries %zu evaluations %zu (%.2f GB)\n", d, entries,
                              CL.pev_perm.size(), entries * 64 / 1e9);
             if (!force && (entries > CL.pev_perm.size() || entries * 64 > (std::size_t(8) << 30))) continue;
-            std::vector<double> tab;
+            uninit_vector<double> tab;
             std::vector<std::int32_t> gc;
             parent_templates(T, C, d, gammas, 0, tab, gc);
             LevelBufs& b = e.lb[d - 2];
@@ -1169,8 +1172,8 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
                 ig[it + 1] += ig[it];
                 ie[it + 1] += ie[it];
             }
-            std::vector<int4> rec(static_cast<std::size_t>(ig[n_item]));
-            std::vector<std::uint16_t> perm(static_cast<std::size_t>(ie[n_item]));
+            uninit_vector<int4> rec(static_cast<std::size_t>(ig[n_item]));  // every entry written below
+            uninit_vector<std::uint16_t> perm(static_cast<std::size_t>(ie[n_item]));
             std::atomic<bool> too_big{false};
 #pragma omp parallel
             {
@@ -1273,6 +1276,36 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         e.far_pos.upload(fpos);
         e.near_chunk_box.upload(chunk_box);
         e.near_chunk_q0.upload(chunk_q0);
+        // patch runs of every leaf's neighbourhood (near_run_kernel: used when the near lists
+        // do not fit, or with IFGF_NEAR=runs; cfg2 2.77 vs 2.45 ms with lists, cfg3 45 vs
+        // 40 ms, 61 ms screening every apply)
+        const char* nenv = std::getenv("IFGF_NEAR");
+        if (!nenv || std::string(nenv) == "runs") {
+            std::vector<std::int32_t> rptr(B.size() + 1, 0), rst, rln, rpa;
+            for (std::size_t b = 0; b < B.size(); ++b) {
+                rptr[b] = std::int32_t(rst.size());
+                for (int j = R.nbr[D - 1].ptr[b]; j < R.nbr[D - 1].ptr[b + 1]; ++j) {
+                    const int nb = R.nbr[D - 1].idx[j];
+                    for (std::uint32_t u = B.begin[nb]; u < B.end[nb];) {
+                        const std::int32_t pq = S.patch_of[T.perm[u]];
+                        std::uint32_t v = u + 1;
+                        while (v < B.end[nb] && S.patch_of[T.perm[v]] == pq) ++v;
+                        rst.push_back(std::int32_t(u));
+                        rln.push_back(std::int32_t(v - u));
+                        rpa.push_back(pq);
+                        u = v;
+                    }
+                }
+            }
+            rptr[B.size()] = std::int32_t(rst.size());
+            e.run_ptr.upload(rptr);
+            e.run_start.upload(rst);
+            e.run_len.upload(rln);
+            e.run_patch.upload(rpa);
+            if (std::getenv("IFGF_SETUP_DEBUG"))
+                std::fprintf(stderr, "near runs: %zu over %zu leaves (%.1f per neighbourhood)\n", rst.size(), B.size(),
+                             double(rst.size()) / double(std::max<std::size_t>(B.size(), 1)));
+        }
         NearDev& N = e.near;
         N.n = int(n);
         N.nleaf = int(B.size());
@@ -1290,6 +1323,10 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         N.far_end = e.far_end.as<std::uint32_t>();
         N.far_pos = e.far_pos.as<std::uint32_t>();
         N.chunk_box = e.near_chunk_box.as<std::int32_t>();
+        N.run_ptr = e.run_ptr.as<std::int32_t>();
+        N.run_start = e.run_start.as<std::int32_t>();
+        N.run_len = e.run_len.as<std::int32_t>();
+        N.run_patch = e.run_patch.as<std::int32_t>();
         N.chunk_q0 = e.near_chunk_q0.as<std::int32_t>();
         N.nchunk = int(chunk_box.size());
     }

@@ -65,6 +65,11 @@ struct NearDev {
     const std::int64_t* list_off = nullptr;
     const double2* geo = nullptr;  // (x, y), (z, nx), (ny, nz) per Morton point
     std::int32_t* list_src = nullptr;
+    // patch runs of each leaf's neighbourhood (near_run_kernel): the neighbour leaves' Morton
+    // spans in neighbour order, split where the patch changes (within a leaf the points are in
+    // original, i.e. patch-major, order), CSR per leaf
+    const std::int32_t* run_ptr = nullptr;
+    const std::int32_t *run_start = nullptr, *run_len = nullptr, *run_patch = nullptr;
 };
 void launch_weights(int n, const std::uint32_t* perm, const double2* phi, const double* jw_p,
                     double2* a_p, cudaStream_t st);

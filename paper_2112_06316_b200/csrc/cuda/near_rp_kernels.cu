@@ -266,6 +266,101 @@ near_list_kernel(NearDev N, PointsDev P, const double2* __restrict__ a_p, double
     }
 }
 
+// Warp per target over its neighbourhood's PATCH RUNS (no per-pair lists): a run whose patch
+// is singular for the target is dropped whole (warp-uniform), the target itself is cut out
+// of its run, and lane i takes entries i, i + 32, ... of the remaining sequence — the same
+// sources in the same order as the near lists / the screening kernel, so the sums are
+// bitwise equal to theirs, without the lists' 4 bytes per pair in HBM (cfg3: 27 GB) and with
+// consecutive (coalesced) source rows. Runs are taken 32 at a time: lanes load a window of
+// runs, a warp scan gives their offsets, and each lane walks its entries with a cursor.
+__global__ void __launch_bounds__(32 * kNearWarps, IFGF_NEAR_MINB)
+near_run_kernel(NearDev N, PointsDev P, const double2* __restrict__ a_p, double k, double2* __restrict__ Sp,
+                double2* __restrict__ Dp) {
+    __shared__ int rs_s[kNearWarps][33], rb_s[kNearWarps][33], re_s[kNearWarps][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int t = blockIdx.x * kNearWarps + w;  // Morton target
+    if (t >= N.n) return;
+    const int tb = N.leaf_of_m[t];
+    if (N.leaf_active && !N.leaf_active[tb]) return;
+    const std::uint32_t l = N.perm[t];
+    const double x = P.x[t], y = P.y[t], z = P.z[t];
+    const int p0 = int(N.tpb[l]), p1 = int(N.tpb[l + 1]);
+    const int nsing = p1 - p0;
+    int sing[kMaxSing];
+#pragma unroll
+    for (int i = 0; i < kMaxSing; ++i) sing[i] = (i < nsing) ? N.pair_patch[p0 + i] : -1;
+    double2 accS = make_double2(0.0, 0.0), accD = make_double2(0.0, 0.0);
+    const int r0 = N.run_ptr[tb], r1 = N.run_ptr[tb + 1];
+    int phase = 0;  // (entries before this window) mod 32
+    for (int wr = r0; wr < r1; wr += 32) {
+        const int r = wr + lane;
+        int st = 0, len = 0;
+        bool self = false;
+        if (r < r1) {
+            st = N.run_start[r];
+            len = N.run_len[r];
+            const int pq = N.run_patch[r];
+            bool ok = true;
+#pragma unroll
+            for (int i = 0; i < kMaxSing; ++i) ok &= (sing[i] != pq);
+            if (nsing > kMaxSing)
+                for (int i = kMaxSing; i < nsing; ++i) ok &= (N.pair_patch[p0 + i] != pq);
+            if (!ok) {
+                len = 0;
+            } else if (t >= st && t < st + len) {
+                self = true;
+                len -= 1;
+            }
+        }
+        int inc = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+        }
+        const int tot = __shfl_sync(0xffffffffu, inc, 31);
+        const unsigned selfm = __ballot_sync(0xffffffffu, self);
+        rs_s[w][lane] = st;
+        rb_s[w][lane] = inc - len;
+        re_s[w][lane] = inc;
+        if (lane == 0) re_s[w][32] = 0x7fffffff;  // cursor sentinel
+        __syncwarp();
+        int cur = 0, cst = rs_s[w][0], cb = rb_s[w][0], ce = re_s[w][0];
+        bool cself = selfm & 1u;
+#pragma unroll 2
+        for (int e = (lane - phase) & 31; e < tot; e += 32) {
+            while (ce <= e) {  // advance to the run holding entry e (skips emptied runs)
+                ++cur;
+                cst = rs_s[w][cur];
+                cb = rb_s[w][cur];
+                ce = re_s[w][cur];
+                cself = (selfm >> cur) & 1u;
+            }
+            int v = cst + (e - cb);
+            if (cself && v >= t) ++v;  // the target itself is not in the sequence
+            near_pair(N.geo, v, x, y, z, a_p, k, 1.0, accS, accD);
+        }
+        phase = (phase + tot) & 31;
+        __syncwarp();
+    }
+    for (int p = p0; p < p1; ++p)
+        for (std::uint32_t f = N.far_begin[p] + lane; f < N.far_end[p]; f += 32) {
+            const int u = int(N.far_pos[f]);
+            near_pair(N.geo, u, x, y, z, a_p, k, -1.0, accS, accD);
+        }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        accS.x += __shfl_xor_sync(0xffffffffu, accS.x, o);
+        accS.y += __shfl_xor_sync(0xffffffffu, accS.y, o);
+        accD.x += __shfl_xor_sync(0xffffffffu, accD.x, o);
+        accD.y += __shfl_xor_sync(0xffffffffu, accD.y, o);
+    }
+    if (lane == 0) {
+        Sp[t] = cadd(Sp[t], accS);
+        Dp[t] = cadd(Dp[t], accD);
+    }
+}
+
 // one CTA per patch: a^q = Mv (Mu phi_q) along u then v (chebyshev.cpp:43-61)
 __global__ void density_coeffs_kernel(RpDev R, const double2* __restrict__ phi,
                                       double2* __restrict__ coeffs) {
@@ -494,6 +589,8 @@ void launch_near_field(const NearDev& N, const PointsDev& P, const double2* a_p,
         near_kernel<<<N.nchunk, kNearThreads, 0, st>>>(N, P, a_p, k, Sp, Dp);
     else if (N.list_off)
         near_list_kernel<<<grid, 32 * kNearWarps, 0, st>>>(N, P, a_p, k, Sp, Dp);
+    else if (N.run_ptr)
+        near_run_kernel<<<grid, 32 * kNearWarps, 0, st>>>(N, P, a_p, k, Sp, Dp);
     else
         near_warp_kernel<0><<<grid, 32 * kNearWarps, 0, st>>>(N, P, a_p, k, Sp, Dp, nullptr);
     IFGF_CUDA(cudaGetLastError());

@@ -465,13 +465,13 @@ ConePlanHost build_cone_plan(const BoxTree& t, const BoxRelations& rel,
 }
 
 void parent_templates(const BoxTree& t, const ConePlanHost& plan, int d, const std::vector<std::int32_t>& gammas,
-                      int workers, std::vector<double>& entries, std::vector<std::int32_t>& gc) {
+                      int workers, uninit_vector<double>& entries, std::vector<std::int32_t>& gc) {
     const ConeLevel& PL = plan.level[d - 2];
     const ConeLevel& CL = plan.level[d - 1];
     const int P = PL.nodes_per_seg();
     const double hp = t.half_diag(d - 1), hc = t.half_diag(d), half = 0.5 * t.side(d);
     const double k = plan.k;
-    entries.assign(gammas.size() * 8 * std::size_t(P) * 8, 0.0);
+    entries.resize(gammas.size() * 8 * std::size_t(P) * 8);  // every entry written below
     gc.assign(gammas.size() * 8 * std::size_t(P), -1);
     const Vec3 origin{0.0, 0.0, 0.0};
     parallel_for(std::int64_t(gammas.size()), worker_count(workers), [&](std::int64_t slot) {
@@ -502,6 +502,7 @@ void parent_templates(const BoxTree& t, const ConePlanHost& plan, int d, const s
                         e[4] = rp / rc * std::sin(k * dr);
                         e[5] = 1.0 / rc;
                         e[6] = rp / rc;
+                        e[7] = 0.0;
                         gc[at] = g;
                     }
         }

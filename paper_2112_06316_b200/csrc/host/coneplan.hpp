@@ -119,7 +119,7 @@ std::vector<std::vector<std::uint8_t>> active_boxes(const BoxTree& t, std::uint3
 // per-box decisions stay the host's (pev ordinals); a device evaluation uses an entry only
 // when gc equals its host-decided child cell. d = child level (parent level d - 1).
 void parent_templates(const BoxTree& t, const ConePlanHost& plan, int d, const std::vector<std::int32_t>& gammas,
-                      int workers, std::vector<double>& entries, std::vector<std::int32_t>& gc);
+                      int workers, uninit_vector<double>& entries, std::vector<std::int32_t>& gc);
 
 // Cost-balanced, leaf-aligned Morton boundaries (parts + 1) of the multi-GPU source/target
 // ownership: per leaf box, near pairs, leaf-fill interactions and cousin

@@ -14,9 +14,32 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <memory>
+#include <utility>
 #include <vector>
 
 namespace ifgfb200 {
+
+// Allocator that leaves elements default-initialised (no zero fill): the multi-GB setup
+// tables (parent templates, parent work items) are then first touched by the parallel loops
+// that fill them instead of by one thread's memset.
+template <class T>
+struct default_init_allocator : std::allocator<T> {
+    template <class U>
+    struct rebind {
+        using other = default_init_allocator<U>;
+    };
+    using std::allocator<T>::allocator;
+    template <class U, class... Args>
+    void construct(U* p, Args&&... args) {
+        if constexpr (sizeof...(Args) == 0)
+            ::new (static_cast<void*>(p)) U;
+        else
+            ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...);
+    }
+};
+template <class T>
+using uninit_vector = std::vector<T, default_init_allocator<T>>;
 
 using cplx = std::complex<double>;
 

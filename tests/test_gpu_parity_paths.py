@@ -72,18 +72,22 @@ def test_parent_cell_batched_equals_per_segment(monkeypatch, strategy):
                 assert rel_l2(D1, D0) <= 1e-13, (key, which)
 
 
-@pytest.mark.parametrize("splits,nu,k", [(2, 6, 4 * np.pi), (3, 8, 8 * np.pi)])
-def test_near_lists_bitwise(monkeypatch, splits, nu, k):
-    # the precomputed near lists hold the screened sources in the screening kernel's batch
-    # order: the near field (and so the whole apply) is bitwise the same with and without them
+@pytest.mark.parametrize("splits,nu,k", [(2, 6, 4 * np.pi), (3, 8, 8 * np.pi), (2, 16, 4 * np.pi)])
+def test_near_variants_bitwise(monkeypatch, splits, nu, k):
+    # the near field's three warp-per-target kernels visit the same sources in the same order
+    # with the same lane assignment: per-apply screening, precomputed near lists, and the
+    # default patch runs (no per-pair lists) give bitwise the same near field / apply
     pm = P.SurfaceMesh.sphere(1.0, splits, nu, nu)
     phi = P.random_density(pm.size(), 4)
-    monkeypatch.setenv("IFGF_NEAR_LISTS", "0")
-    screened = P.CombinedOperator(pm, P.SolveConfig(k=k)).layer_potentials(phi)
-    monkeypatch.delenv("IFGF_NEAR_LISTS")
-    listed = P.CombinedOperator(pm, P.SolveConfig(k=k)).layer_potentials(phi)
-    for a, b in zip(screened, listed):
-        assert np.array_equal(a, b)
+    res = {}
+    for mode in ("screen", "lists", "runs"):
+        monkeypatch.setenv("IFGF_NEAR", mode)
+        res[mode] = P.CombinedOperator(pm, P.SolveConfig(k=k)).layer_potentials(phi)
+    monkeypatch.delenv("IFGF_NEAR")
+    res["default"] = P.CombinedOperator(pm, P.SolveConfig(k=k)).layer_potentials(phi)
+    for mode in ("lists", "runs", "default"):
+        for a, b in zip(res["screen"], res[mode]):
+            assert np.array_equal(a, b), mode
 
 
 @pytest.mark.parametrize("splits,nu,k", [(2, 6, 4 * np.pi), (3, 8, 8 * np.pi)])
