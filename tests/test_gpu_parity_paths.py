@@ -104,10 +104,12 @@ def test_parent_merge_bitwise(monkeypatch, splits, nu, k):
         assert np.array_equal(o[0], out[0][0]) and np.array_equal(o[1], out[0][1])
 
 
-@pytest.mark.parametrize("axes,k", [((4.0, 1.0, 1.0), 2 * np.pi), ((2.5, 0.6, 1.2), 3 * np.pi)])
-def test_spheroid_parity(ref, axes, k):
-    pm = P.SurfaceMesh.spheroid(2, 8, 8, *axes)
-    rm = ref.RefMesh.spheroid(2, 8, 8, *axes)
+@pytest.mark.parametrize("axes,k,nu", [((4.0, 1.0, 1.0), 2 * np.pi, 8), ((2.5, 0.6, 1.2), 3 * np.pi, 8),
+                                       ((40.0, 4.0, 4.0), np.pi / 4, 16)])
+def test_spheroid_parity(ref, axes, k, nu):
+    # the last case is cfg4's (40, 4, 4) spheroid (10:1 patches) at 1/8 of its wavenumber
+    pm = P.SurfaceMesh.spheroid(2, nu, nu, *axes)
+    rm = ref.RefMesh.spheroid(2, nu, nu, *axes)
     op = P.CombinedOperator(pm, P.SolveConfig(k=k))
     ro = ref.RefOperator(rm, k)
     phi = P.random_density(pm.size(), 3)
@@ -133,7 +135,7 @@ def test_gpu_closest_points_bitwise(ref, mesh):
         assert np.array_equal(cpu[key], theirs[key]), key
 
 
-@pytest.mark.parametrize("mesh", ["sphere", "spheroid", "cfg1"])
+@pytest.mark.parametrize("mesh", ["sphere", "spheroid", "cfg1", "cfg4_small"])
 def test_gpu_cone_decisions_bitwise(ref, mesh):
     # segment decisions batched on the GPU (uncertain ones redone on the host with glibc)
     # give the reference's relevant segments, cousin / parent ordinals and groups bit for bit
@@ -141,6 +143,10 @@ def test_gpu_cone_decisions_bitwise(ref, mesh):
         pm, rm, k = P.SurfaceMesh.sphere(1.0, 2, 10, 10), ref.RefMesh.sphere(1.0, 2, 10, 10), 8 * np.pi
     elif mesh == "spheroid":
         pm, rm, k = P.SurfaceMesh.spheroid(2, 8, 8, 4.0, 1.0, 1.0), ref.RefMesh.spheroid(2, 8, 8, 4.0, 1.0, 1.0), 2 * np.pi
+    elif mesh == "cfg4_small":  # cfg4's (40, 4, 4) spheroid, 10:1 patches, at 1/8 the wavenumber
+        pm = P.SurfaceMesh.spheroid(2, 16, 16, 40.0, 4.0, 4.0)
+        rm = ref.RefMesh.spheroid(2, 16, 16, 40.0, 4.0, 4.0)
+        k = np.pi / 4
     else:
         pm, rm, k = P.SurfaceMesh.sphere(1.0, 2, 16, 16), ref.RefMesh.sphere(1.0, 2, 16, 16), 4 * np.pi
     gpu = P.HostPlan(pm, P.SolveConfig(k=k, device=0))
