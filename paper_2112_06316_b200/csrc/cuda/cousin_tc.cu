@@ -71,7 +71,7 @@ cousin_tc_kernel(LevelDev L, PointsDev P, const double2* __restrict__ store, dou
         if (act) {
             const double vx = x - L.cx[sb], vy = y - L.cy[sb], vz = z - L.cz[sb];
             const double r2 = fma(vx, vx, fma(vy, vy, vz * vz));
-            const double inv_r = rsqrt(r2);
+            const double inv_r = rsqrt_normal(r2);
             const LocalCoords lc = local_coords_seg(vx, vy, vz, inv_r, h, so, L);
             double sn, cs;
             sincos_bounded(k * (r2 * inv_r), &sn, &cs);

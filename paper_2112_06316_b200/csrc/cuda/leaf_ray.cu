@@ -137,7 +137,7 @@ leaf_ray_kernel(LevelDev L, PointsDev P, const double2* __restrict__ a_p, double
                 const double sg = sig[is];
                 const double w = fma(sg, d2, -2.0 * xd);   // (|v|^2 - 1) / sigma
                 const double nv2 = fma(sg, w, 1.0);
-                const double inv = rsqrt(nv2);
+                const double inv = rsqrt_normal(nv2);
                 const double arg = khos[is] * fma(nv2, inv, -1.0);  // kh/s (|v| - 1)
                 double sn, cs;
                 sincos_bounded(arg, &sn, &cs);

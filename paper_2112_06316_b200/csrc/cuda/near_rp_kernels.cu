@@ -56,7 +56,7 @@ __device__ __forceinline__ void pair_kernels(double x, double y, double z, doubl
                                              double k, double sg, double2& accS, double2& accD) {
     const double dx = x - yx, dy = y - yy, dz = z - yz;
     const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
-    const double inv = rsqrt(r2);
+    const double inv = rsqrt_normal(r2);
     const double r = r2 * inv;
     double sn, cs;
     sincos_bounded(k * r, &sn, &cs);

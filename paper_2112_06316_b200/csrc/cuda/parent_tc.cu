@@ -130,7 +130,7 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
                     const double x = pcx + rp * sth * cph, y = pcy + rp * sth * sph, z = pcz + rp * cth;
                     const double vx = x - ccx, vy = y - ccy, vz = z - ccz;
                     const double rc2 = fma(vx, vx, fma(vy, vy, vz * vz));
-                    const double inv_rc = rsqrt(rc2);
+                    const double inv_rc = rsqrt_normal(rc2);
                     const double rc = rc2 * inv_rc;
                     const LocalCoords lc = local_coords_in(vx, vy, vz, inv_rc, hc, cf, Lc);
                     // stable r_c - r_p (ifgf.cpp:149-153)
