@@ -103,10 +103,10 @@ __device__ __forceinline__ LocalCoords local_coords_in(double vx, double vy, dou
                                                        const CellFrame& f, const LevelDev& L) {
     const int gamma = f.g1 + L.ns * (f.g2 + L.nc * f.g3);
     if (!L.thc_cos) return local_coords_lib(vx, vy, vz, inv_r, h, gamma, L);
-    const double rho = sqrt(fma(vx, vx, vy * vy));
+    const double rho = sqrt_nonneg(fma(vx, vx, vy * vy));
     const double tn = fma(rho, f.ctc, -vz * f.stc), td = fma(vz, f.ctc, rho * f.stc);
     const double pn = fma(vy, f.cpc, -vx * f.spc), pd = fma(vx, f.cpc, vy * f.spc);
-    const double inv = 1.0 / (td * pd);  // one division for both tangents
+    const double inv = rcp_normal(td * pd);  // one division for both tangents (td, pd > 0 checked below)
     const double tt = tn * pd * inv, tp = pn * td * inv;
     if (!(fabs(tt) <= 0.4225 && fabs(tp) <= 0.4225 && td > 0.0 && pd > 0.0))
         return local_coords_lib(vx, vy, vz, inv_r, h, gamma, L);
@@ -128,12 +128,12 @@ __device__ __forceinline__ LocalCoords local_coords(double vx, double vy, double
     const int rest = gamma / L.ns;
     const int g2 = rest % L.nc;
     const int g3 = rest / L.nc;
-    const double rho = sqrt(fma(vx, vx, vy * vy));
+    const double rho = sqrt_nonneg(fma(vx, vx, vy * vy));
     const double ctc = L.thc_cos[g2], stc = L.thc_sin[g2];
     const double cpc = L.phc_cos[g3], spc = L.phc_sin[g3];
     const double tn = fma(rho, ctc, -vz * stc), td = fma(vz, ctc, rho * stc);
     const double pn = fma(vy, cpc, -vx * spc), pd = fma(vx, cpc, vy * spc);
-    const double inv = 1.0 / (td * pd);  // one division for both tangents
+    const double inv = rcp_normal(td * pd);  // one division for both tangents (td, pd > 0 checked below)
     const double tt = tn * pd * inv, tp = pn * td * inv;
     if (!(fabs(tt) <= 0.4225 && fabs(tp) <= 0.4225 && td > 0.0 && pd > 0.0))
         return local_coords_lib(vx, vy, vz, inv_r, h, gamma, L);
@@ -150,12 +150,12 @@ __device__ __forceinline__ LocalCoords local_coords_seg(double vx, double vy, do
     if (!L.thc_cos || !L.seg_code) return local_coords(vx, vy, vz, inv_r, h, L.seg_gamma[so], L);
     const unsigned code = L.seg_code[so];
     const int g1 = int(code & 0xffu), g2 = int((code >> 8) & 0x7ffu), g3 = int(code >> 19);
-    const double rho = sqrt(fma(vx, vx, vy * vy));
+    const double rho = sqrt_nonneg(fma(vx, vx, vy * vy));
     const double ctc = L.thc_cos[g2], stc = L.thc_sin[g2];
     const double cpc = L.phc_cos[g3], spc = L.phc_sin[g3];
     const double tn = fma(rho, ctc, -vz * stc), td = fma(vz, ctc, rho * stc);
     const double pn = fma(vy, cpc, -vx * spc), pd = fma(vx, cpc, vy * spc);
-    const double inv = 1.0 / (td * pd);  // one division for both tangents
+    const double inv = rcp_normal(td * pd);  // one division for both tangents (td, pd > 0 checked below)
     const double tt = tn * pd * inv, tp = pn * td * inv;
     if (!(fabs(tt) <= 0.4225 && fabs(tp) <= 0.4225 && td > 0.0 && pd > 0.0))
         return local_coords_lib(vx, vy, vz, inv_r, h, L.seg_gamma[so], L);
