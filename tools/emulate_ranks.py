@@ -26,12 +26,12 @@ import paper_2112_06316_b200 as P  # noqa: E402
 from bench import CONFIGS, make_mesh  # noqa: E402
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("cfg")
-    ap.add_argument("world", type=int)
-    ap.add_argument("--steps", type=int, default=5)
-    args = ap.parse_args()
+def emulate(cfg_name, world, steps=5, log=sys.stderr):
+    class A:  # noqa: N801
+        pass
+
+    args = A()
+    args.cfg, args.world, args.steps = cfg_name, world, steps
     splits, nu, k, gamma, desc = CONFIGS[args.cfg]
     mesh = make_mesh(args.cfg, P)
     n = mesh.size()
@@ -71,7 +71,8 @@ def main():
         ranks.append({"rank": r, "owned": hi - lo, "setup_s": setup, "setup_breakdown_s": op.setup_times(),
                       "ms_per_apply": float(np.mean(each)), "ms_best": float(np.min(each)), "phases_ms": phases,
                       "kernels_per_apply": op.kernels_per_apply()})
-        print(json.dumps(ranks[-1]), file=sys.stderr, flush=True)
+        if log:
+            print(json.dumps(ranks[-1]), file=log, flush=True)
         del op
     S = np.zeros(n, complex)
     D = np.zeros(n, complex)
@@ -102,7 +103,16 @@ def main():
         pos = np.searchsorted(fix["sample_idx"], idx)
         want = 0.5 * phi[idx] + (fix["D_sample"][pos] + fix["rpD"]) - 1j * gam * (fix["S_sample"][pos] + fix["rpS"])
         res["parity"]["out_rel_l2_rp_sample"] = float(np.linalg.norm(out[idx] - want) / np.linalg.norm(want))
-    print(json.dumps(res))
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("cfg")
+    ap.add_argument("world", type=int)
+    ap.add_argument("--steps", type=int, default=5)
+    args = ap.parse_args()
+    print(json.dumps(emulate(args.cfg, args.world, args.steps)))
 
 
 if __name__ == "__main__":
