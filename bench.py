@@ -50,6 +50,8 @@ CONFIGS = {
     "cfg2": (4, 16, 16 * np.pi, -1.0, "sphere r=1, 16 wavelengths, 1536 patches x 16^2, k=16pi"),
     "cfg3": (6, 16, 64 * np.pi, -1.0, "sphere r=1, 64 wavelengths, 24576 patches x 16^2, k=64pi"),
     "cfg4": (6, 16, 2 * np.pi, -1.0, "spheroid (40,4,4) lambda=1, 24576 patches x 16^2, k=2pi"),
+    # BASELINE configs[4] (a GMRES solve on 8 B200s; 406 GB of beta tables: >= 3 GPUs)
+    "cfg5": (7, 16, 128 * np.pi, -1.0, "sphere r=1, 128 wavelengths, 98304 patches x 16^2, k=128pi"),
 }
 SPHEROIDS = {"cfg4": (40.0, 4.0, 4.0)}  # cube-sphere coefficients scaled
 
@@ -167,7 +169,8 @@ def reference_apply_time(cfg_name, phi, beta_cache=None, applies=1, warmup=0):
     return times, out, setup, R.lib().ref_op_beta_cache_hit(ro.h) == 1
 
 
-LARGE = {"cfg3"}  # no reference beta tables: ifgf_apply + near loop
+LARGE = {"cfg3", "cfg4", "cfg5"}
+BETA_GB = {"cfg3": 101, "cfg4": 178, "cfg5": 406}  # no reference beta tables: ifgf_apply + near loop
 
 
 def reference_ifgf_near_time(cfg_name, phi, steps=1):
@@ -200,6 +203,10 @@ def run_reference(args, ws, rank):
         return
     phi = R.random_density(n, 1)
     cores = os.cpu_count()
+    if cfg_name == "cfg5":
+        print(json.dumps({"impl": "reference", "unavailable": "cfg5 (N = 25.2 M): the reference's setup alone takes "
+                          "hours on the host cores and its GMRES basis ~20 GB; no CPU baseline (SURVEY.md 8(d))"}))
+        return
     if cfg_name in LARGE:
         steps, warm = 1, 0
         times, _, _, setup = reference_ifgf_near_time(cfg_name, phi, steps)
@@ -207,7 +214,8 @@ def run_reference(args, ws, rank):
         value = n * steps / total
         sample = (f"1 step = the reference's ifgf_apply (ifgf.cpp:577-608) + the level-D near-field loop "
                   f"(solver.cpp:100-144) at {cfg_name} (N={n}), i.e. CombinedOperator::layer_potentials minus "
-                  f"its RP term: the reference's beta tables would need 101 GB and hours of CPU (BASELINE.md §3); "
+                  f"its RP term: the reference's beta tables would need {BETA_GB.get(cfg_name, '100+')} GB and hours of "
+                  f"CPU (BASELINE.md §3); "
                   f"setup (octree, plan_cones, classify_targets) {setup['total']:.0f} s untimed; OpenMP {cores} "
                   f"threads; 1 step, no warm-up, to bound the run")
         line = {
@@ -293,6 +301,8 @@ def check_parity(cfg_name, op, phi, out_gpu):
         import large_check as LC
 
         path = os.path.join(ROOT, "tests", "golden", f"{cfg_name}_large.npz")
+        if not os.path.exists(path):
+            return {"parity": {"error": f"no reference fixture for {cfg_name} (tests/golden/make_large.py)"}}
         fix = np.load(path)
         if not np.array_equal(phi[:8], fix["phi_head"]):
             raise RuntimeError("density differs from the fixture's")
@@ -352,9 +362,10 @@ def cpu_baseline(cfg_name, n):
         return {"value": m / times[0], "unit": "points/s", "cores": cores, "kind": "reference",
                 "seconds": times[0],
                 "sample": f"bounded sample: the reference's ifgf_apply + near-field loop (BASELINE.md §3; no RP: "
-                          f"its cfg3 beta tables would need 101 GB) on the cfg2 sphere of the same family "
-                          f"(N={m}, 1/16 of cfg3's points; the reference's per-point cost grows ~log N, so this "
-                          f"overstates its cfg3 rate); OpenMP {cores} threads; --impl reference times cfg3 itself"}
+                          f"its {cfg_name} beta tables would need 100+ GB) on the cfg2 sphere "
+                          f"(N={m}, 1/16 of {cfg_name}'s points; the reference's per-point cost grows ~log N, so this "
+                          f"overstates its {cfg_name} rate); OpenMP {cores} threads; --impl reference times "
+                          f"{cfg_name} itself"}
     times, _, setup = _ref_full(cfg_name, R.random_density(n, 1))
     return {"value": n / times[0], "unit": "points/s", "cores": cores, "kind": "reference", "seconds": times[0],
             "sample": f"one full CombinedOperator::apply at {cfg_name} (N={n}), reference built from /root/reference "
