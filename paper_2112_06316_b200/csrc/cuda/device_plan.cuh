@@ -12,6 +12,7 @@ struct PointsDev {
 };
 
 constexpr int kParentMergeMax = 2;  // parent segments per warp item (IFGF_PARENT_MERGE <= this; 3 measured slower)
+constexpr int kTmplDoubles = 6;      // parent template entry: ls, lt, lp, ratio1 (re, im), 1/r_c
 constexpr int kCbSegs = 12;         // parent segments per cell-batched parent item (parent_cb.cu)
 constexpr int kCbMaxGrp = 8;        // child-cell groups per (parent cell, octant) in a batched item
 
@@ -70,7 +71,7 @@ struct LevelDev {
     // wider than pi/4 (nc < 4), where local_coords uses acos/atan2
     const double *thc_cos = nullptr, *thc_sin = nullptr, *phc_cos = nullptr, *phc_sin = nullptr;
     // parent-fill geometry templates for this level's children (host/coneplan.hpp
-    // parent_templates): slot per cone cell (-1: none) and 8 doubles per (slot, octant, node)
+    // parent_templates): slot per cone cell (-1: none) and kTmplDoubles per (slot, octant, node)
     // entry; which evaluations may use them is marked in the child level's pev_perm
     const std::int32_t* tmpl_slot = nullptr;
     const double* tmpl = nullptr;

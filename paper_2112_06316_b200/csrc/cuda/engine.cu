@@ -936,8 +936,8 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
             const std::size_t entries = gammas.size() * 8 * std::size_t(PL.nodes_per_seg());
             if (std::getenv("IFGF_SETUP_DEBUG"))
                 std::fprintf(stderr, "templates level %d: entries %zu evaluations %zu (%.2f GB)\n", d, entries,
-                             CL.pev_perm.size(), entries * 64 / 1e9);
-            if (!force && (entries > CL.pev_perm.size() || entries * 64 > (std::size_t(8) << 30))) continue;
+                             CL.pev_perm.size(), entries * 8 * kTmplDoubles / 1e9);
+            if (!force && (entries > CL.pev_perm.size() || entries * 8 * kTmplDoubles > (std::size_t(8) << 30))) continue;
             uninit_vector<double> tab;
             std::vector<std::int32_t> gc;
             parent_templates(T, C, d, gammas, 0, tab, gc);

@@ -185,16 +185,19 @@ parent_cb_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
             if (tid < kNP) {
                 const int node = Lc.cb_nodes[so8 * kNP + tid];
                 nodes_s[tid] = (unsigned char)node;
-                const double* te = Lp.tmpl + (so8 * kNP + node) * 8;
+                const double* te = Lp.tmpl + (so8 * kNP + node) * kTmplDoubles;
                 const double2 t0 = __ldg(reinterpret_cast<const double2*>(te));
                 const double2 t1 = __ldg(reinterpret_cast<const double2*>(te) + 1);
                 const double2 t2 = __ldg(reinterpret_cast<const double2*>(te) + 2);
-                const double2 t3 = __ldg(reinterpret_cast<const double2*>(te) + 3);
                 double* cr = cheb + tid * 13;
                 cheb_row<3>(t0.x, cr);
                 cheb_row<5>(t0.y, cr + 3);
                 cheb_row<5>(t1.x, cr + 8);
-                const double xf = CB::extra == RI ? t2.y : t3.x;
+                double xf = t2.y;  // 1/r_c
+                if (CB::extra == RQ) {  // r_p/r_c = (h_p / s) (1/r_c), s of the cell's radial node
+                    const int gam = Lp.seg_gamma[Lc.cb_item_seg[std::size_t(item) * kMB]];
+                    xf *= Lp.h / Lp.s_nodes[(gam % Lp.ns) * 3 + node % 3];
+                }
 #pragma unroll
                 for (int p = 0; p < NPC; ++p) fac[tid * NPC + p] = child_factor<COMBO>(p, t1.y, t2.x, xf, k);
             }

@@ -108,14 +108,15 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
                 if (ent & 0x8000u) {
                     // geometry template of (parent cell, child octant, node), host/coneplan.hpp
                     const std::size_t tent = (std::size_t(tslot) * 8 + oct) * kNP + node;
-                    const double2* te = reinterpret_cast<const double2*>(Lp.tmpl + tent * 8);
-                    const double2 t0 = __ldg(te), t1 = __ldg(te + 1), t2 = __ldg(te + 2), t3 = __ldg(te + 3);
+                    const double2* te = reinterpret_cast<const double2*>(Lp.tmpl + tent * kTmplDoubles);
+                    const double2 t0 = __ldg(te), t1 = __ldg(te + 1), t2 = __ldg(te + 2);
                     ls = t0.x;
                     lt = t0.y;
                     lp = t1.x;
                     r1x = t1.y;
                     r1y = t2.x;
-                    xf = CB::extra == RI ? t2.y : t3.x;
+                    xf = t2.y;  // 1/r_c
+                    if (CB::extra == RQ) xf *= hp / Lp.s_nodes[(code & 0xff) * kPS + node % kPS];  // r_p/r_c
                 } else {
                     // child frame, loaded only on this (rare, non-template) path
                     const double ccx = Lc.cx[ch], ccy = Lc.cy[ch], ccz = Lc.cz[ch];

@@ -471,7 +471,8 @@ void parent_templates(const BoxTree& t, const ConePlanHost& plan, int d, const s
     const int P = PL.nodes_per_seg();
     const double hp = t.half_diag(d - 1), hc = t.half_diag(d), half = 0.5 * t.side(d);
     const double k = plan.k;
-    entries.resize(gammas.size() * 8 * std::size_t(P) * 8);  // every entry written below
+    constexpr int E = 6;  // doubles per entry (device_plan.cuh kTmplDoubles)
+    entries.resize(gammas.size() * 8 * std::size_t(P) * E);  // every entry written below
     gc.assign(gammas.size() * 8 * std::size_t(P), -1);
     const Vec3 origin{0.0, 0.0, 0.0};
     parallel_for(std::int64_t(gammas.size()), worker_count(workers), [&](std::int64_t slot) {
@@ -494,15 +495,13 @@ void parent_templates(const BoxTree& t, const ConePlanHost& plan, int d, const s
                         const Vec3 sv = off - 2.0 * x;  // stable r_c - r_p (ifgf.cpp:149-153)
                         const double dr = dot3(sv, off) / (rc + rp);
                         const std::size_t at = (std::size_t(slot) * 8 + o) * P + node;
-                        double* e = entries.data() + at * 8;
+                        double* e = entries.data() + at * E;
                         e[0] = 2.0 * cc.s / CL.ds - (2 * c1 + 1.0);
                         e[1] = 2.0 * (cc.th - (c2 + 0.5) * CL.dth) / CL.dth;
                         e[2] = 2.0 * (cc.ph - (c3 + 0.5) * CL.dph) / CL.dph;
                         e[3] = rp / rc * std::cos(k * dr);
                         e[4] = rp / rc * std::sin(k * dr);
                         e[5] = 1.0 / rc;
-                        e[6] = rp / rc;
-                        e[7] = 0.0;
                         gc[at] = g;
                     }
         }

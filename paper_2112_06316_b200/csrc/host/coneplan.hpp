@@ -115,7 +115,8 @@ std::vector<std::vector<std::uint8_t>> active_boxes(const BoxTree& t, std::uint3
 // node and the child's octant (box centres are exact grid points up to one rounding), so
 // per (parent cell gamma_p, octant, node) the child cell the node falls in and its
 // continuous data are tabulated once per level: entry = {ls, lt, lp, re/im of
-// (r_p/r_c) e^{ik(r_c - r_p)}, 1/r_c, r_p/r_c, 0} (8 doubles) and gc = child cell. The
+// (r_p/r_c) e^{ik(r_c - r_p)}, 1/r_c} (6 doubles; r_p/r_c = (h_p/s) (1/r_c) is formed on the
+// device where needed) and gc = child cell. The
 // per-box decisions stay the host's (pev ordinals); a device evaluation uses an entry only
 // when gc equals its host-decided child cell. d = child level (parent level d - 1).
 void parent_templates(const BoxTree& t, const ConePlanHost& plan, int d, const std::vector<std::int32_t>& gammas,
