@@ -13,7 +13,11 @@ struct PointsDev {
 
 constexpr int kParentMergeMax = 2;  // parent segments per warp item (IFGF_PARENT_MERGE <= this; 3 measured slower)
 constexpr int kTmplDoubles = 6;      // parent template entry: ls, lt, lp, ratio1 (re, im), 1/r_c
-constexpr int kCbSegs = 12;         // parent segments per cell-batched parent item (parent_cb.cu)
+constexpr int kCbSegs = 16;         // parent segments per cell-batched parent item (parent_cb.cu: 4 per warp)
+constexpr int kCbRows = 80;         // rows of a cell-batched (slot, octant) table (75 nodes + padding)
+constexpr int kCbTabP = kCbRows * 16;            // table: A2 [80][16], then phi weights [80][8],
+constexpr int kCbTabG = kCbTabP + kCbRows * 8;   // then re-centring data [80][4] (ratio1, 1/r_c)
+constexpr int kCbTab = kCbTabG + kCbRows * 4;    // doubles per (slot, octant)
 constexpr int kCbMaxGrp = 8;        // child-cell groups per (parent cell, octant) in a batched item
 
 struct LevelDev {
@@ -63,6 +67,7 @@ struct LevelDev {
     const std::int64_t* cb_exc_begin = nullptr;
     const std::uint32_t* cb_exc_key = nullptr;
     const std::int32_t* cb_exc_cso = nullptr;
+    const double* cb_tab = nullptr;  // per (slot, octant): kCbTab doubles (parent_cb.cu cb_table_kernel)
     const std::int32_t *ch_ptr = nullptr, *ch_idx = nullptr;  // children (level d+1) of this level's boxes
     const double *s_nodes = nullptr, *th_nodes = nullptr, *ph_nodes = nullptr;
     // sin/cos of the angular node tables (interpolation-node directions)

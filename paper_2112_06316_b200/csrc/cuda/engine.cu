@@ -157,7 +157,7 @@ struct LevelBufs {
         chunk_box, chunk_q0, wchunk_box, wchunk_q0, tmpl_slot, tmpl, seg_code, litem_seg0,
         litem_nseg, litem_split, litem_box0, litem_box1, pgrp_rec, pitem_seg, pitem_grp, pitem_ev;
     DevBuf cb_item_slot, cb_item_seg, cb_nodes, cb_gstart, cb_ngrp, cb_child, cb_cso, cb_exc_begin, cb_exc_key,
-        cb_exc_cso;
+        cb_exc_cso, cb_tab;
 };
 
 Pipes make_pipes(const std::vector<int>& f) {
@@ -954,21 +954,25 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
 
     phase_mark("cell-batched items");
     // ---- cell-batched parent items (parent_cb.cu): on levels with templates whose parent cone
-    // cells are each shared by >= 4 parent segments on average, the segments of one cell are
-    // batched (kCbSegs per CTA) into GEMMs against their children's blocks; the per-segment
-    // kernel below takes the remaining segments. Opt-in (IFGF_PARENT_CB=1; =force batches
-    // every template level): measured 2.2x SLOWER than the per-segment kernel at cfg2 (parent
-    // 18.7 vs 8.4 ms) — its per-item A-matrix build and block staging cost more instructions
-    // than the DMMAs they feed (profiles/r02d_parent_cb_ncu.txt).
+    // cells are each shared by >= min_avg parent segments on average (default 400: cfg3's two
+    // finest parent levels), the segments of one cell are batched (kCbSegs per CTA, sorted by
+    // child-octant pattern) into GEMMs against their children's blocks; the per-segment kernel
+    // below takes the remaining segments. IFGF_PARENT_CB=0 disables, =force batches every
+    // template level, IFGF_PARENT_CB_MINAVG sets the threshold. cfg3: parent 251 -> 231 ms;
+    // on levels with fewer segments per cell the per-segment kernel is faster (cfg2 level 5,
+    // 396 per cell: break-even; level 4, 45 per cell: 30% slower).
     std::vector<std::vector<std::uint8_t>> cb_seg_h(T.depth + 1);
     {
         const char* env = std::getenv("IFGF_PARENT_CB");
-        const bool enabled = env && env[0] != '0';
+        const bool enabled = !(env && env[0] == '0');
         const bool force = env && std::string(env) == "force";
         const bool dbg = std::getenv("IFGF_SETUP_DEBUG") != nullptr;
         // tests: also route every n-th evaluation through the exception path (same segment)
         const char* xenv = std::getenv("IFGF_PARENT_CB_EXC_EVERY");
         const int exc_every = xenv ? std::max(0, std::atoi(xenv)) : 0;
+        // levels batch when their template cells hold >= min_avg segments on average
+        const char* menv = std::getenv("IFGF_PARENT_CB_MINAVG");
+        const std::size_t min_avg = menv ? std::size_t(std::max(1, std::atoi(menv))) : 400;
         for (int d = 4; enabled && d <= T.depth; ++d) {
             const std::vector<std::int32_t>& slot = tmpl_slot_h[d];
             const std::vector<std::int32_t>& gcs = tmpl_gc_h[d];
@@ -1005,17 +1009,37 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
                     ngrp[so8] = std::uint8_t(ng);
                     gstart[so8 * (kCbMaxGrp + 1) + ng] = P;
                 }
+            const auto& cptr = C.child_ptr[d - 2];
+            const auto& cidx = C.child_idx[d - 2];
+            // child-octant pattern of each parent box: an item's warps take 4 segments each, so
+            // segments with the same pattern are kept together (no idle GEMM columns)
+            std::vector<std::uint8_t> omask(PL.box_seg_begin.size() - 1, 0);
+#pragma omp parallel for schedule(static)
+            for (std::int64_t pb = 0; pb < std::int64_t(omask.size()); ++pb) {
+                const Vec3 pc = T.center(d - 1, std::size_t(pb));
+                std::uint8_t m = 0;
+                for (int c = cptr[pb]; c < cptr[pb + 1]; ++c) {
+                    const Vec3 cc = T.center(d, std::size_t(cidx[c]));
+                    m |= std::uint8_t(1u << ((cc.x > pc.x ? 1 : 0) | (cc.y > pc.y ? 2 : 0) | (cc.z > pc.z ? 4 : 0)));
+                }
+                omask[pb] = m;
+            }
             std::vector<std::vector<std::int32_t>> by_slot(nslot);
             for (std::size_t so = 0; so < PL.nseg(); ++so) {
                 const int sl = slot[PL.seg_gamma[so]];
                 if (sl >= 0 && !bad[sl]) by_slot[sl].push_back(std::int32_t(so));
             }
+#pragma omp parallel for schedule(dynamic, 64)
+            for (int sl = 0; sl < nslot; ++sl)
+                std::stable_sort(by_slot[sl].begin(), by_slot[sl].end(), [&](std::int32_t a, std::int32_t b) {
+                    return omask[PL.seg_box[a]] < omask[PL.seg_box[b]];
+                });
             std::size_t cnt = 0, used = 0;
             for (const auto& v : by_slot) {
                 cnt += v.size();
                 used += v.empty() ? 0 : 1;
             }
-            if (!force && cnt < 4 * used) continue;  // cells too rarely shared at this level
+            if (!force && cnt < min_avg * used) continue;  // cells too rarely shared at this level
             std::vector<std::int32_t> item_slot, item_seg;
             for (int sl = 0; sl < nslot; ++sl)
                 for (std::size_t a = 0; a < by_slot[sl].size(); a += kCbSegs) {
@@ -1024,8 +1048,6 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
                         item_seg.push_back(a + j < by_slot[sl].size() ? by_slot[sl][a + j] : -1);
                 }
             const std::int64_t n_item = std::int64_t(item_slot.size());
-            const auto& cptr = C.child_ptr[d - 2];
-            const auto& cidx = C.child_idx[d - 2];
             std::vector<std::int32_t> child(std::size_t(n_item) * kCbSegs * 8, -1),
                 cso(std::size_t(n_item) * kCbSegs * 8 * kCbMaxGrp, -1);
             std::vector<std::vector<std::pair<std::uint32_t, std::int32_t>>> exc(n_item);
@@ -1073,9 +1095,21 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
             done.assign(PL.nseg(), 0);
             for (std::int32_t so : item_seg)
                 if (so >= 0) done[so] = 1;
-            if (dbg)
-                std::fprintf(stderr, "cell-batched parent level %d: %zu of %zu segments in %lld items, %zu cells, %zu exceptions\n",
-                             d - 1, cnt, PL.nseg(), (long long)n_item, used, exc_key.size());
+            if (dbg) {
+                double sg = 0, st = 0, nso = 0;
+                for (int sl = 0; sl < nslot; ++sl)
+                    for (int o = 0; o < 8; ++o) {
+                        const std::size_t so8 = std::size_t(sl) * 8 + o;
+                        if (by_slot[sl].empty()) continue;
+                        nso += 1;
+                        sg += ngrp[so8];
+                        for (int g = 0; g < ngrp[so8]; ++g)
+                            st += (gstart[so8 * (kCbMaxGrp + 1) + g + 1] - gstart[so8 * (kCbMaxGrp + 1) + g] + 7) / 8;
+                    }
+                std::fprintf(stderr, "cell-batched parent level %d: %zu of %zu segments in %lld items, %zu cells, %zu exceptions; "
+                             "per (cell, octant): %.2f child cells, %.2f 8-row tiles\n",
+                             d - 1, cnt, PL.nseg(), (long long)n_item, used, exc_key.size(), sg / std::max(1.0, nso), st / std::max(1.0, nso));
+            }
             LevelBufs& b = e.lb[d - 1];
             b.cb_item_slot.upload(item_slot);
             b.cb_item_seg.upload(item_seg);
@@ -1099,6 +1133,11 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
             L.cb_exc_begin = b.cb_exc_begin.as<std::int64_t>();
             L.cb_exc_key = b.cb_exc_key.as<std::uint32_t>();
             L.cb_exc_cso = b.cb_exc_cso.as<std::int32_t>();
+            // (slot, octant) tables from the level's geometry templates (device-side)
+            b.cb_tab.alloc(std::size_t(nslot) * 8 * kCbTab * sizeof(double));
+            IFGF_CUDA(cudaDeviceSynchronize());  // the template and node uploads are in flight
+            launch_cb_tables(e.L[d - 2].tmpl, L.cb_nodes, nslot, b.cb_tab.as<double>(), 0);
+            L.cb_tab = b.cb_tab.as<double>();
         }
     }
 

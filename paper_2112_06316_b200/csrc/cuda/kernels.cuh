@@ -39,6 +39,8 @@ bool launch_leaf_fill_ray(const LevelDev& L, const PointsDev& P, const double2* 
 bool launch_parent_fill_cb(const LevelDev& Lp, const LevelDev& Lc, const double2* child_store, double k,
                            const Pipes& parent_pipes, const Pipes& child_pipes, const double* Ms, const double* Ma,
                            double2* parent_store, cudaStream_t st);
+// per (slot, octant) tables of the cell-batched parent fill from the geometry templates
+void launch_cb_tables(const double* tmpl, const std::uint8_t* nodes, std::int64_t nslot, double* tab, cudaStream_t st);
 bool launch_parent_fill_tc(const LevelDev& Lp, const LevelDev& Lc, const double2* child_store, double k,
                            const Pipes& parent_pipes, const Pipes& child_pipes, const double* Ms,
                            const double* Ma, double2* parent_store, cudaStream_t st);

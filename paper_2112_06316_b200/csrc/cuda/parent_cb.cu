@@ -1,25 +1,31 @@
-// Cell-batched parent fill (ifgf.cpp:452-568) on the FP64 tensor cores.
+// Cell-batched parent fill (ifgf.cpp:452-568) as GEMMs on the FP64 tensor cores.
 //
 // The position of a parent interpolation node in a child frame depends only on (parent cone
 // cell, child octant, node) (host/coneplan.hpp parent_templates), and so does the child cone
 // cell it falls in. All parent segments of ONE cone cell therefore interpolate their
-// children's coefficient blocks with the SAME real matrix: row = node, column k = the 75
-// products T_is(s) T_it(theta) T_ip(phi) of its local coordinates. A CTA takes up to
-// kCbSegs (12) parent segments of one cell (an "item", built on the host) and, per child
-// octant and per child-cell group of nodes, runs one small GEMM on mma.sync.m8n8k4.f64:
+// children's coefficient blocks with the SAME real matrix. Per (cell, octant) a setup kernel
+// tabulates, with the nodes in child-cell group order (rows [gs, ge) = group g):
+//   A2[row][16]  T_is(s) T_it(theta) in tc_common.cuh's k-slot order (15 pairs + a zero pad),
+//   phw[row][ip] T_ip(phi), geo[row] the re-centring data (ratio1, 1/r_c) of the template.
+// A CTA takes an item of kCbSegs (16) parent segments of one cell (host-sorted by their
+// child-octant pattern); warp w owns segments 4w..4w+3 for all octants and computes, per
+// octant o and group g present among them,
 //
-//   C (group nodes x [segment, child pipe, re/im]) = A (group nodes x 76) * B (76 x ...),
+//   V[node, (segment, child pipe)] += f[node, pipe] * sum_ip phw[row, ip]
+//                                      * A2[row, :] B_ip[:, (segment, pipe)]
 //
-// A built once per octant in shared memory from the template entries, B = the children's
-// coefficient blocks staged by cp.async into shared memory (double-buffered: the next
-// group's blocks load while this group multiplies), 2x2 tiles of 8x8 per warp (4
-// independent accumulator chains, one A and one B fragment load per two DMMAs). The
-// epilogue multiplies each (node, child pipe) by its re-centring factor and adds into
-// per-(segment, node, child pipe) accumulators in shared memory; each entry has one writer
-// per group, and groups run in a fixed order, so results are bitwise reproducible.
-// Evaluations whose host-decided child segment differs from the template's group (ties) are
-// masked out of the GEMM and evaluated one by one (exceptions). Finally the child pipes are
-// summed into the parent pipes and transform3 (ifgf.cpp:560-562) writes the blocks.
+// with B_ip the 15 coefficients of phi index ip of each child block: the phi weight is folded
+// into the A fragment (one multiply), so the 5 x 4 k-steps (mma.sync.m8n8k4.f64) accumulate
+// straight into up to 5 x NPC register tiles whose 8 columns are the 4 segments x {re, im}:
+// a lane's D fragment is one complex (row, segment) value, and there is no gather epilogue.
+// The child blocks stream through a per-warp 3-stage cp.async ring (one chunk = one ip,
+// two chunks ahead, across groups and octants). Warps never wait for each other: the
+// accumulators V[segment][node][parent pipe] are warp-private (one writer, fixed order, so
+// bitwise reproducible). Evaluations whose host-decided child segment differs from the
+// template's group (ties) are masked out and evaluated one by one (exceptions); transform3
+// (ifgf.cpp:560-562) finishes each segment.
+#include <cstdio>
+
 #include "ifgf_device.cuh"
 #include "kernels.cuh"
 #include "parent_common.cuh"
@@ -32,42 +38,37 @@ using namespace dev;
 using namespace ifgfdev;
 using namespace pfill;
 
-constexpr int kW = 8;                  // warps per CTA
-constexpr int kNP = 75, kK = 76;       // coefficients per pipe block; k padded to 19 steps of 4
-constexpr int kKS = kK / 4;
-constexpr int kMB = kCbSegs;
+constexpr int kW = kCbSegs / 4;  // warps per CTA (4 segments each)
+constexpr int kNP = 75;          // nodes / coefficients per pipe block
+constexpr int kRows = kCbRows;   // table rows (75 + zero padding)
+constexpr int kStages = 3;       // cp.async ring depth per warp
+constexpr int kMaxUnits = 8 * (kCbMaxGrp + 1);  // per octant: its groups, one of which may split in 2
 constexpr int kG = kCbMaxGrp;
-constexpr int kCheb = 976;             // 75 rows x 13 basis values (+1: keeps B 16-byte aligned)
-
-// staged block layout in shared memory: pipe stride SP, block stride SB (doubles), chosen
-// so that an 8x4 B fragment load takes the minimum two wavefronts
-template <int NPC>
-struct Stage;
-template <>
-struct Stage<1> {
-    static constexpr int SP = 150, SB = 152;
-};
-template <>
-struct Stage<2> {
-    static constexpr int SP = 150, SB = 312;
-};
-template <>
-struct Stage<3> {
-    static constexpr int SP = 152, SB = 456;
-};
 
 template <int NPC>
-constexpr std::size_t cb_smem_bytes() {
-    return std::size_t(kMB) * kNP * NPC * 16 + std::size_t(kNP) * kK * 8 + std::size_t(kNP) * NPC * 16 +
-           std::size_t(kCheb) * 8 + 2 * std::size_t(kMB) * Stage<NPC>::SB * 8 + 2 * (kMB + 1) * 4 + kMB * kNP;
-}
+struct Ring {
+    static constexpr int SS = NPC * 32 + 8;  // doubles per segment (pipes x 16 complex + pad):
+                                              // 4 segments' fragment loads take 2 wavefronts
+    static constexpr int STAGE = 4 * SS;
+};
+
+// per warp: accumulators [4][75][NPP] complex, ring, unit list, exception bits [8][4][75]
+template <int NPC, int NPP>
+struct WarpSmem {
+    static constexpr int ACC = 4 * kNP * NPP * 2;                 // doubles
+    static constexpr int RING = kStages * Ring<NPC>::STAGE;       // doubles
+    static constexpr int UNITS = kMaxUnits * 5;                   // ints
+    static constexpr int EXC = (8 * 4 * kNP + 31) / 32;           // words
+    static constexpr std::size_t bytes = (std::size_t(ACC + RING) * 8 + std::size_t(UNITS + EXC) * 4 + 15) / 16 * 16;
+};
 
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
     const unsigned s = unsigned(__cvta_generic_to_shared(sdst));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 template <int COMBO>
 __device__ __forceinline__ double2 child_factor(int p, double r1x, double r1y, double xf, double k) {
@@ -78,230 +79,265 @@ __device__ __forceinline__ double2 child_factor(int p, double r1x, double r1y, d
     return make_double2(r1x * xf, r1y * xf);              // RI (1/r_c) or RQ (r_p/r_c)
 }
 
+#ifdef IFGF_CB_STATS
+__device__ unsigned long long g_cb_stats[4];
+#endif
+
 template <int COMBO>
-__global__ void __launch_bounds__(32 * kW, 1)
+__global__ void __launch_bounds__(32 * kW, Combo<COMBO>::npc == 3 ? 2 : 3)
 parent_cb_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, double k,
                  const double* __restrict__ Ms, const double* __restrict__ Ma, double2* __restrict__ pstore) {
     using CB = Combo<COMBO>;
     constexpr int NPP = CB::npp, NPC = CB::npc;
-    constexpr int SP = Stage<NPC>::SP, SB = Stage<NPC>::SB;
-    constexpr int NCOL = 2 * NPC;  // B columns per staged block: (child pipe, re/im)
+    using WS = WarpSmem<NPC, NPP>;
+    constexpr int SS = Ring<NPC>::SS, STAGE = Ring<NPC>::STAGE;
+    constexpr int kMT = NPC == 3 ? 6 : 5;  // 8-row tiles per unit (a larger group takes 2 units)
     extern __shared__ __align__(16) double smem[];
-    double2* acc = reinterpret_cast<double2*>(smem);                    // [j][node][child pipe]
-    double* A = smem + 2 * kMB * kNP * NPC;                              // [row][kK]
-    double2* fac = reinterpret_cast<double2*>(A + kNP * kK);             // [row][child pipe]
-    double* cheb = reinterpret_cast<double*>(fac + kNP * NPC);           // [row][13]
-    double* Bs = cheb + kCheb;                                           // 2 x [kMB][SB]
-    int* blist = reinterpret_cast<int*>(Bs + 2 * kMB * SB);              // 2 x (kMB + 1)
-    unsigned char* mask = reinterpret_cast<unsigned char*>(blist + 2 * (kMB + 1));  // [j][node]
-    __shared__ int segs_s[kMB];
-    __shared__ unsigned char use_s[kMB * 8];
-    __shared__ unsigned char nodes_s[kNP];
-    __shared__ int steps_s[8 * kG];
-    __shared__ int nsteps_s;
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int r = lane >> 2, tig = lane & 3;
+    char* wbase = reinterpret_cast<char*>(smem) + std::size_t(warp) * WS::bytes;
+    double2* acc = reinterpret_cast<double2*>(wbase);                       // [c][node][pp]
+    double* ring = reinterpret_cast<double*>(wbase) + WS::ACC;               // [stage][STAGE]
+    int* units = reinterpret_cast<int*>(ring + WS::RING);                    // [unit][5]
+    unsigned* excb = reinterpret_cast<unsigned*>(units + WS::UNITS);         // [o][c][node] bits
+
     const int item = blockIdx.x;
     const int slot = Lc.cb_item_slot[item];
-    const std::int32_t* __restrict__ iseg = Lc.cb_item_seg + std::size_t(item) * kMB;
+    const std::int32_t* __restrict__ iseg = Lc.cb_item_seg + std::size_t(item) * kCbSegs + 4 * warp;
 
-    if (tid < kMB) {
-        int s = iseg[tid];
-        if (s >= 0 && Lp.active && !Lp.active[Lp.seg_box[s]]) s = -1;  // no sources of this rank below
-        segs_s[tid] = s;
-    }
-    for (int i = tid; i < kMB * kNP * NPC; i += 32 * kW) acc[i] = make_double2(0.0, 0.0);
-    for (int i = tid; i < 2 * kMB * SB; i += 32 * kW) Bs[i] = 0.0;  // padding read as k = 75 stays 0
-    __syncthreads();
-    if (tid < kMB * 8) {
-        const int j = tid >> 3, o = tid & 7;
-        bool u = false;
-        if (segs_s[j] >= 0) {
-            const int ch = Lc.cb_child[(std::size_t(item) * kMB + j) * 8 + o];
-            u = ch >= 0 && !(Lc.active && !Lc.active[ch]);
-        }
-        use_s[tid] = u ? 1 : 0;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        int ns = 0;
-        for (int o = 0; o < 8; ++o) {
-            bool any = false;
-            for (int j = 0; j < kMB; ++j) any = any || use_s[j * 8 + o];
-            if (!any) continue;
-            const int ng = Lc.cb_ngrp[slot * 8 + o];
-            for (int g = 0; g < ng; ++g) steps_s[ns++] = (o << 8) | g;
-        }
-        nsteps_s = ns;
-    }
-    __syncthreads();
-    const int nsteps = nsteps_s;
+    for (int i = lane; i < WS::RING; i += 32) ring[i] = 0.0;  // pad slots (coefficient "75") stay 0
+    for (int i = lane; i < WS::ACC / 2; i += 32) acc[i] = make_double2(0.0, 0.0);
+    for (int i = lane; i < WS::EXC; i += 32) excb[i] = 0u;
 
-    // stage step s's child blocks into buffer buf (every warp derives the same list)
-    auto stage = [&](int s, int buf) {
-        const int o = steps_s[s] >> 8, g = steps_s[s] & 0xff;
-        int cso = -1;
-        if (lane < kMB && use_s[lane * 8 + o]) cso = Lc.cb_cso[((std::size_t(item) * kMB + lane) * 8 + o) * kG + g];
-        const unsigned bal = __ballot_sync(0xffffffffu, cso >= 0);
-        const int m = __popc(bal);
-        if (warp == 0) {
-            if (cso >= 0) blist[buf * (kMB + 1) + __popc(bal & ((1u << lane) - 1u))] = lane;
-            if (lane == 0) blist[buf * (kMB + 1) + kMB] = m;
+    // ---- unit list: lane = c + 4 o holds segment c's child in octant o, then per octant
+    // lane = c + 4 g the child segment of segment c in group g
+    const int c_l = lane & 3, o_l = lane >> 2;
+    int seg_l = iseg[c_l];
+    if (seg_l >= 0 && Lp.active && !Lp.active[Lp.seg_box[seg_l]]) seg_l = -1;
+    int ch_l = -1;
+    if (seg_l >= 0) {
+        ch_l = Lc.cb_child[(std::size_t(item) * kCbSegs + 4 * warp + c_l) * 8 + o_l];
+        if (ch_l >= 0 && Lc.active && !Lc.active[ch_l]) ch_l = -1;
+    }
+    const unsigned has = __ballot_sync(0xffffffffu, ch_l >= 0);
+    // all octants' child segments and group bounds at once (independent loads)
+    int cso_o[8], gb_o[8];
+    int ng_l = lane < 8 ? Lc.cb_ngrp[std::size_t(slot) * 8 + lane] : 0;
+#pragma unroll
+    for (int o = 0; o < 8; ++o) {
+        const int ng = __shfl_sync(0xffffffffu, ng_l, o);
+        const int chc = __shfl_sync(0xffffffffu, ch_l, c_l + 4 * o);
+        const int g = lane >> 2;
+        cso_o[o] = (g < ng && chc >= 0)
+                       ? Lc.cb_cso[((std::size_t(item) * kCbSegs + 4 * warp + c_l) * 8 + o) * kG + g]
+                       : -1;
+        gb_o[o] = lane <= ng ? Lc.cb_gstart[(std::size_t(slot) * 8 + o) * (kG + 1) + lane] : 0;
+    }
+    int nu = 0;
+#pragma unroll
+    for (int o = 0; o < 8; ++o) {
+        if (((has >> (4 * o)) & 0xfu) == 0u) continue;
+        const int ng = __shfl_sync(0xffffffffu, ng_l, o);
+        const unsigned cm = __ballot_sync(0xffffffffu, cso_o[o] >= 0);
+        for (int g = 0; g < ng; ++g) {
+            if (((cm >> (4 * g)) & 0xfu) == 0u) continue;
+            const int gs = __shfl_sync(0xffffffffu, gb_o[o], g), ge = __shfl_sync(0xffffffffu, gb_o[o], g + 1);
+            const int cso = __shfl_sync(0xffffffffu, cso_o[o], (lane & 3) + 4 * g);
+            const int mt = (ge - gs + 7) >> 3;
+            const int nh = mt > kMT ? 2 : 1;
+            for (int h = 0; h < nh; ++h) {
+                const int t0 = h == 0 ? 0 : (mt + 1) / 2, t1 = nh == 1 ? mt : (h == 0 ? (mt + 1) / 2 : mt);
+                int* U = units + nu * 5;
+                if (lane == 0) U[0] = (gs + 8 * t0) | ((t1 - t0) << 8) | (ge << 16) | (o << 24);
+                if (lane < 4) U[1 + lane] = cso;
+                ++nu;
+            }
         }
-        double* dstb = Bs + buf * kMB * SB;
-        const int total = m * NPC * kNP;
-        for (int c0 = warp * 32; c0 < total; c0 += 32 * kW) {  // warp-uniform trip count (shuffles)
-            const int c = c0 + lane;
-            const bool live = c < total;
-            const int jj = live ? c / (NPC * kNP) : 0, rem = c - jj * (NPC * kNP);
-            const int p = rem / kNP, kk = rem - p * kNP;
-            // lane of the (jj + 1)-th listed segment
-            unsigned rest = bal;
-            for (int q = 0; q < jj; ++q) rest &= rest - 1u;
-            const int cs = __shfl_sync(0xffffffffu, cso, __ffs(rest) - 1);
-            if (live) cp_async16(dstb + jj * SB + p * SP + 2 * kk, cstore + std::size_t(cs) * NPC * kNP + p * kNP + kk);
+    }
+#ifdef IFGF_CB_STATS
+    if (lane == 0) {
+        unsigned long long smt = 0;
+        for (int ui = 0; ui < nu; ++ui) smt += (units[ui * 5] >> 8) & 0xff;
+        atomicAdd(&g_cb_stats[0], (unsigned long long)nu);
+        atomicAdd(&g_cb_stats[1], smt);
+        atomicAdd(&g_cb_stats[2], (unsigned long long)__popc(has));
+        unsigned long long bo = 0;
+        for (int o = 0; o < 8; ++o) bo += ((has >> (4 * o)) & 0xfu) ? 1 : 0;
+        atomicAdd(&g_cb_stats[3], bo);
+    }
+#endif
+    // exception bits of this warp's segments
+    const std::int64_t e0 = Lc.cb_exc_begin[item], e1 = Lc.cb_exc_begin[item + 1];
+    for (std::int64_t e = e0 + lane; e < e1; e += 32) {
+        const unsigned key = Lc.cb_exc_key[e];
+        const int c = int(key & 0xffu) - 4 * warp, o = int((key >> 8) & 0xffu), node = int(key >> 16);
+        if (c >= 0 && c < 4) {
+            const int bit = (o * 4 + c) * kNP + node;
+            atomicOr(excb + (bit >> 5), 1u << (bit & 31));
         }
-        cp_async_commit();
+    }
+    __syncwarp();
+
+    // ---- chunk stream: chunk q = (unit q / 5, ip = q % 5). Lanes 0..29 copy 16 bytes of
+    // coefficient e = lane % 15 for the (segment, pipe) pairs half, half + 2, ... (a lane-
+    // constant plan: destination offsets fixed, source pointers set once per unit)
+    int doff[2 * NPC], cpair[2 * NPC], sofs[2 * NPC];
+    {
+        const int e = lane % 15, half = lane / 15;
+#pragma unroll
+        for (int i = 0; i < 2 * NPC; ++i) {
+            const int pr = half + 2 * i, c = pr / NPC, p = pr - (pr / NPC) * NPC;
+            doff[i] = c * SS + p * 32 + 2 * e;
+            cpair[i] = c < 4 ? c : 0;
+            sofs[i] = p * kNP + e;
+        }
+    }
+    const double2* sp[2 * NPC];
+    unsigned sval = 0u;
+    int iss_u = 0, iss_ip = 0, iss_st = 0;
+    auto issue = [&]() {
+        if (iss_u < nu) {
+            if (iss_ip == 0) {  // a new unit: its segments' block pointers
+                const int* U = units + iss_u * 5;
+                sval = 0u;
+#pragma unroll
+                for (int i = 0; i < 2 * NPC; ++i) {
+                    const int cso = U[1 + cpair[i]];
+                    sp[i] = cstore + std::size_t(cso < 0 ? 0 : cso) * NPC * kNP + sofs[i];
+                    if (cso >= 0 && lane < 30) sval |= 1u << i;
+                }
+            }
+            double* dst = ring + iss_st * STAGE;
+#pragma unroll
+            for (int i = 0; i < 2 * NPC; ++i)
+                if ((sval >> i) & 1u) cp_async16(dst + doff[i], sp[i] + 15 * iss_ip);
+            if (++iss_ip == 5) {
+                iss_ip = 0;
+                ++iss_u;
+            }
+        }
+        cp_async_commit();  // (empty groups keep the wait counts uniform)
+        iss_st = iss_st == kStages - 1 ? 0 : iss_st + 1;
     };
+    issue();
+    issue();
 
-    // this lane's three k columns of the A rows: (is, it, ip) of k = lane, lane + 32, lane + 64
-    int kis[3], kit[3], kip[3];
+    const double* __restrict__ tab0 = Lc.cb_tab + std::size_t(slot) * 8 * kCbTab;
+    const int gam0 = CB::extra == RQ ? Lp.seg_gamma[Lc.cb_item_seg[std::size_t(item) * kCbSegs]] : 0;
+    const double hp = Lp.h;
+    int cst = 0;  // ring stage of the chunk being consumed
+    for (int ui = 0; ui < nu; ++ui) {
+        const int* U = units + ui * 5;
+        const int u0 = U[0];
+        const int row0 = u0 & 0xff, mtu = (u0 >> 8) & 0xff, ge = (u0 >> 16) & 0xff, o = u0 >> 24;
+        const double* __restrict__ tab = tab0 + std::size_t(o) * kCbTab;
+        auto run = [&]<int MT>() {
+            double d[MT][NPC][2];
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
-        const int kk = min(lane + 32 * q, kNP - 1);
-        kis[q] = kk % 3;
-        kit[q] = 3 + (kk / 3) % 5;
-        kip[q] = 8 + kk / 15;
-    }
-    if (nsteps > 0) stage(0, 0);
-    int o_cur = -1;
-    for (int s = 0; s < nsteps; ++s) {
-        const int o = steps_s[s] >> 8, g = steps_s[s] & 0xff, buf = s & 1;
-        if (o != o_cur) {  // A rows, factors and exception mask of octant o
-            if (o_cur >= 0) __syncthreads();  // the previous octant's multiplications read A
-            o_cur = o;
-            const std::size_t so8 = std::size_t(slot) * 8 + o;
-            if (tid < kNP) {
-                const int node = Lc.cb_nodes[so8 * kNP + tid];
-                nodes_s[tid] = (unsigned char)node;
-                const double* te = Lp.tmpl + (so8 * kNP + node) * kTmplDoubles;
-                const double2 t0 = __ldg(reinterpret_cast<const double2*>(te));
-                const double2 t1 = __ldg(reinterpret_cast<const double2*>(te) + 1);
-                const double2 t2 = __ldg(reinterpret_cast<const double2*>(te) + 2);
-                double* cr = cheb + tid * 13;
-                cheb_row<3>(t0.x, cr);
-                cheb_row<5>(t0.y, cr + 3);
-                cheb_row<5>(t1.x, cr + 8);
-                double xf = t2.y;  // 1/r_c
-                if (CB::extra == RQ) {  // r_p/r_c = (h_p / s) (1/r_c), s of the cell's radial node
-                    const int gam = Lp.seg_gamma[Lc.cb_item_seg[std::size_t(item) * kMB]];
-                    xf *= Lp.h / Lp.s_nodes[(gam % Lp.ns) * 3 + node % 3];
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int p = 0; p < NPC; ++p) d[i][p][0] = d[i][p][1] = 0.0;
+            int arow[MT];
+#pragma unroll
+            for (int i = 0; i < MT; ++i) arow[i] = min(row0 + 8 * i + r, kRows - 1);
+            double a[MT][4];  // A2 fragments of the unit's tiles (the same for every ip)
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) a[i][j] = __ldg(tab + arow[i] * 16 + 4 * j + tig);
+            double wn[MT];  // phi weights of the next ip, loaded one chunk ahead
+#pragma unroll
+            for (int i = 0; i < MT; ++i) wn[i] = __ldg(tab + kCbTabP + arow[i] * 8);
+            for (int ip = 0; ip < 5; ++ip) {
+                double w[MT];
+#pragma unroll
+                for (int i = 0; i < MT; ++i) {
+                    w[i] = wn[i];
+                    wn[i] = __ldg(tab + kCbTabP + arow[i] * 8 + (ip < 4 ? ip + 1 : 4));
                 }
+                cp_async_wait<1>();  // chunk q landed (q + 1 may still be in flight)
+                __syncwarp();
+                issue();  // chunk q + 2
+                const double* bch = ring + cst * STAGE + (r >> 1) * SS + (r & 1);
+                cst = cst == kStages - 1 ? 0 : cst + 1;
 #pragma unroll
-                for (int p = 0; p < NPC; ++p) fac[tid * NPC + p] = child_factor<COMBO>(p, t1.y, t2.x, xf, k);
+                for (int j = 0; j < 4; ++j) {
+                    const int ci = tig < 3 ? tig + 3 * j : (j < 3 ? j + 12 : 15);
+                    double b[NPC];
+#pragma unroll
+                    for (int p = 0; p < NPC; ++p) b[p] = bch[p * 32 + 2 * ci];
+#pragma unroll
+                    for (int i = 0; i < MT; ++i) {
+                        const double av = a[i][j] * w[i];
+#pragma unroll
+                        for (int p = 0; p < NPC; ++p) tc::dmma884(d[i][p][0], d[i][p][1], av, b[p]);
+                    }
+                }
+                __syncwarp();  // this ring stage is refilled by the issue of chunk q + 3
             }
-            for (int i = tid; i < kMB * kNP; i += 32 * kW) mask[i] = 0;
-            __syncthreads();
-            for (int row = warp; row < kNP; row += kW) {
-                const double* cr = cheb + row * 13;
+            // epilogue: lane (r, tig) holds (re, im) of rows row0 + 8 i + r for segment tig;
+            // the rows' table entries are loaded for all tiles first (one latency)
+            if (U[1 + tig] >= 0) {
+                double4 gq[MT];
 #pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    const int kk = lane + 32 * q;
-                    if (kk < kK) A[row * kK + kk] = kk < kNP ? cr[kis[q]] * cr[kit[q]] * cr[kip[q]] : 0.0;
+                for (int i = 0; i < MT; ++i) {
+                    const double2* gp = reinterpret_cast<const double2*>(tab + kCbTabG) + 2 * arow[i];
+                    const double2 g0 = __ldg(gp), g1 = __ldg(gp + 1);
+                    gq[i] = make_double4(g0.x, g0.y, g1.x, g1.y);
                 }
-            }
-            const std::int64_t e0 = Lc.cb_exc_begin[item], e1 = Lc.cb_exc_begin[item + 1];
-            for (std::int64_t e = e0 + tid; e < e1; e += 32 * kW) {
-                const unsigned key = Lc.cb_exc_key[e];
-                if (int((key >> 8) & 0xffu) == o) mask[(key & 0xffu) * kNP + (key >> 16)] = 1;
-            }
-        }
-        cp_async_wait_all();
-        __syncthreads();
-        if (s + 1 < nsteps) stage(s + 1, buf ^ 1);  // overlaps this step's multiplications
-
-        const std::size_t so8 = std::size_t(slot) * 8 + o;
-        const int gs = Lc.cb_gstart[so8 * (kG + 1) + g], ge = Lc.cb_gstart[so8 * (kG + 1) + g + 1];
-        const int m = blist[buf * (kMB + 1) + kMB];
-        const int* bl = blist + buf * (kMB + 1);
-        const double* Bb = Bs + buf * kMB * SB;
-        const int mt = (ge - gs + 7) >> 3, nt = (NCOL * m + 7) >> 3;
-        const int mp = (mt + 1) >> 1, np = (nt + 1) >> 1;
-        for (int u = warp; u < mp * np; u += kW) {
-            const int mt0 = 2 * (u / np), nt0 = 2 * (u % np);
-            const double* a0p = A + min(gs + mt0 * 8 + r, kNP - 1) * kK + tig;
-            const double* a1p = A + min(gs + mt0 * 8 + 8 + r, kNP - 1) * kK + tig;
-            auto bcol = [&](int col) {
-                col = min(col, NCOL * kMB - 1);
-                return Bb + (col / NCOL) * SB + ((col % NCOL) >> 1) * SP + (col & 1) + 2 * tig;
-            };
-            const double* b0p = bcol(nt0 * 8 + r);
-            const double* b1p = bcol(nt0 * 8 + 8 + r);
-            double d[2][2][2] = {};
-            const bool m1 = mt0 + 1 < mt, n1 = nt0 + 1 < nt;  // warp-uniform: skip absent tiles
-            if (m1 && n1) {
 #pragma unroll
-                for (int ks = 0; ks < kKS; ++ks) {
-                    const double a0 = a0p[4 * ks], a1 = a1p[4 * ks];
-                    const double b0 = b0p[8 * ks], b1 = b1p[8 * ks];
-                    tc::dmma884(d[0][0][0], d[0][0][1], a0, b0);
-                    tc::dmma884(d[0][1][0], d[0][1][1], a0, b1);
-                    tc::dmma884(d[1][0][0], d[1][0][1], a1, b0);
-                    tc::dmma884(d[1][1][0], d[1][1][1], a1, b1);
-                }
-            } else if (n1) {
+                for (int i = 0; i < MT; ++i) {
+                    const int row = row0 + 8 * i + r;
+                    const int node = int(gq[i].w);
+                    const int bit = (o * 4 + tig) * kNP + node;
+                    if (row < ge && !((excb[bit >> 5] >> (bit & 31)) & 1u)) {
+                        double xf = gq[i].z;
+                        if (CB::extra == RQ) xf *= hp / Lp.s_nodes[(gam0 % Lp.ns) * 3 + node % 3];
+                        double2 v[NPP];
 #pragma unroll
-                for (int ks = 0; ks < kKS; ++ks) {
-                    const double a0 = a0p[4 * ks];
-                    const double b0 = b0p[8 * ks], b1 = b1p[8 * ks];
-                    tc::dmma884(d[0][0][0], d[0][0][1], a0, b0);
-                    tc::dmma884(d[0][1][0], d[0][1][1], a0, b1);
-                }
-            } else if (m1) {
+                        for (int pp = 0; pp < NPP; ++pp) v[pp] = make_double2(0.0, 0.0);
 #pragma unroll
-                for (int ks = 0; ks < kKS; ++ks) {
-                    const double a0 = a0p[4 * ks], a1 = a1p[4 * ks];
-                    const double b0 = b0p[8 * ks];
-                    tc::dmma884(d[0][0][0], d[0][0][1], a0, b0);
-                    tc::dmma884(d[1][0][0], d[1][0][1], a1, b0);
-                }
-            } else {
+                        for (int p = 0; p < NPC; ++p) {
+                            const double2 t = cmul(child_factor<COMBO>(p, gq[i].x, gq[i].y, xf, k),
+                                                   make_double2(d[i][p][0], d[i][p][1]));
+                            v[CB::dst(p)] = cadd(v[CB::dst(p)], t);
+                        }
 #pragma unroll
-                for (int ks = 0; ks < kKS; ++ks) tc::dmma884(d[0][0][0], d[0][0][1], a0p[4 * ks], b0p[8 * ks]);
-            }
-#pragma unroll
-            for (int im = 0; im < 2; ++im)
-#pragma unroll
-                for (int in = 0; in < 2; ++in) {
-                    const int row = gs + (mt0 + im) * 8 + r;
-                    const int c = (nt0 + in) * 8 + 2 * tig;
-                    const int jj = c / NCOL, p = (c % NCOL) >> 1;
-                    if (mt0 + im < mt && nt0 + in < nt && row < ge && jj < m) {
-                        const int j = bl[jj], node = nodes_s[row];
-                        if (!mask[j * kNP + node]) {
-                            double2& a = acc[(j * kNP + node) * NPC + p];
-                            a = cadd(a, cmul(fac[row * NPC + p], make_double2(d[im][in][0], d[im][in][1])));
+                        for (int pp = 0; pp < NPP; ++pp) {
+                            double2& av = acc[(tig * kNP + node) * NPP + pp];
+                            av = cadd(av, v[pp]);
                         }
                     }
                 }
+            }
+        };
+        switch (mtu) {
+            case 1: run.template operator()<1>(); break;
+            case 2: run.template operator()<2>(); break;
+            case 3: run.template operator()<3>(); break;
+            case 4: run.template operator()<4>(); break;
+            case 5: run.template operator()<5>(); break;
+            case 6: run.template operator()<6>(); break;
+            case 7: if constexpr (kMT >= 7) run.template operator()<7>(); break;
+            default: if constexpr (kMT >= 8) run.template operator()<8>(); break;
         }
-        // no barrier here: the next step's top barrier orders its B / accumulator use after
-        // this one, and an octant change waits before rebuilding A
     }
-    __syncthreads();
+    cp_async_wait<0>();
+    __syncwarp();
 
-    // exceptions: one thread, in list order (rare; each may share an accumulator with another)
-    if (tid == 0) {
-        const std::int64_t e0 = Lc.cb_exc_begin[item], e1 = Lc.cb_exc_begin[item + 1];
-        const double hp = Lp.h, hc = Lc.h;
+    // exceptions of this warp's segments: lane 0, in list order (rare; each may share an
+    // accumulator with another)
+    if (lane == 0) {
+        const double hc = Lc.h;
         for (std::int64_t e = e0; e < e1; ++e) {
             const unsigned key = Lc.cb_exc_key[e];
-            const int j = int(key & 0xffu), o = int((key >> 8) & 0xffu), node = int(key >> 16);
-            const int seg = segs_s[j];
-            if (seg < 0 || !use_s[j * 8 + o]) continue;
+            const int c = int(key & 0xffu) - 4 * warp, o = int((key >> 8) & 0xffu), node = int(key >> 16);
+            if (c < 0 || c >= 4) continue;
+            const int seg = iseg[c];
+            if (seg < 0 || (Lp.active && !Lp.active[Lp.seg_box[seg]])) continue;
+            const int ch = Lc.cb_child[(std::size_t(item) * kCbSegs + 4 * warp + c) * 8 + o];
+            if (ch < 0 || (Lc.active && !Lc.active[ch])) continue;
             const int cso = Lc.cb_exc_cso[e];
-            const int ch = Lc.cb_child[(std::size_t(item) * kMB + j) * 8 + o];
             const int pb = Lp.seg_box[seg], gam = Lp.seg_gamma[seg];
             const int g1 = gam % Lp.ns, g2 = (gam / Lp.ns) % Lp.nc, g3 = gam / Lp.ns / Lp.nc;
             const int is = node % 3, it = (node / 3) % 5, ip = node / 15;
@@ -324,42 +360,33 @@ parent_cb_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
             sincos_bounded(k * dr, &sn, &cs);
             const double q1 = rp * inv_rc;
             const double xf = CB::extra == RI ? inv_rc : q1;
-            double ts[3], tt[5], tp[5];
+            double ts[3], tt[5], tpp[5];
             cheb_row<3>(lc.ls, ts);
             cheb_row<5>(lc.lt, tt);
-            cheb_row<5>(lc.lp, tp);
+            cheb_row<5>(lc.lp, tpp);
             const double2* blk = cstore + std::size_t(cso) * NPC * kNP;
             for (int p = 0; p < NPC; ++p) {
                 double2 v = make_double2(0.0, 0.0);
-                for (int kk = 0; kk < kNP; ++kk) cfma_r(v, blk[p * kNP + kk], ts[kk % 3] * tt[(kk / 3) % 5] * tp[kk / 15]);
-                double2& a = acc[(j * kNP + node) * NPC + p];
+                for (int kk = 0; kk < kNP; ++kk) cfma_r(v, blk[p * kNP + kk], ts[kk % 3] * tt[(kk / 3) % 5] * tpp[kk / 15]);
+                double2& a = acc[(c * kNP + node) * NPP + CB::dst(p)];
                 a = cadd(a, cmul(child_factor<COMBO>(p, cs * q1, sn * q1, xf, k), v));
             }
         }
     }
-    __syncthreads();
+    __syncwarp();
 
-    // child pipes -> parent pipes, then values -> coefficients (transform3), warp per segment
-    double2* v0 = reinterpret_cast<double2*>(Bs) + warp * 2 * NPP * kNP;
-    double2* v1 = v0 + NPP * kNP;
-    for (int j = warp; j < kMB; j += kW) {
-        const int seg = segs_s[j];
+    // values -> coefficients (transform3) per segment; scratch = the warp's ring
+    double2* v1 = reinterpret_cast<double2*>(ring);
+    for (int c = 0; c < 4; ++c) {
+        const int seg = __shfl_sync(0xffffffffu, seg_l, c);
         if (seg < 0) continue;
-        for (int e = lane; e < NPP * kNP; e += 32) {
-            const int node = e / NPP, pp = e % NPP;
-            double2 a = make_double2(0.0, 0.0);
-#pragma unroll
-            for (int p = 0; p < NPC; ++p)
-                if (CB::dst(p) == pp) a = cadd(a, acc[(j * kNP + node) * NPC + p]);
-            v0[e] = a;
-        }
-        __syncwarp();
+        double2* v0 = acc + c * kNP * NPP;  // node-major [node][pp]
         double2* dst = pstore + std::size_t(seg) * NPP * kNP;
         for (int e = lane; e < NPP * kNP; e += 32) {
             const int blk = e / kNP, node = e % kNP;
             const int is = node % 3, line = node / 3;
             double2 a = make_double2(0.0, 0.0);
-            for (int q = 0; q < 3; ++q) cfma_r(a, v0[(line * 3 + q) * NPP + blk], Ms[is * 3 + q]);
+            for (int q2 = 0; q2 < 3; ++q2) cfma_r(a, v0[(line * 3 + q2) * NPP + blk], Ms[is * 3 + q2]);
             v1[e] = a;
         }
         __syncwarp();
@@ -368,8 +395,8 @@ parent_cb_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
             const int is = node % 3, it = (node / 3) % 5, ip = node / 15;
             const double2* src = v1 + blk * kNP + is + 15 * ip;
             double2 a = make_double2(0.0, 0.0);
-            for (int q = 0; q < 5; ++q) cfma_r(a, src[3 * q], Ma[it * 5 + q]);
-            v0[e] = a;
+            for (int q2 = 0; q2 < 5; ++q2) cfma_r(a, src[3 * q2], Ma[it * 5 + q2]);
+            v0[e] = a;  // (pipe-major from here on)
         }
         __syncwarp();
         for (int e = lane; e < NPP * kNP; e += 32) {
@@ -377,19 +404,62 @@ parent_cb_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
             const int is = node % 3, it = (node / 3) % 5, ip = node / 15;
             const double2* src = v0 + blk * kNP + is + 3 * it;
             double2 a = make_double2(0.0, 0.0);
-            for (int q = 0; q < 5; ++q) cfma_r(a, src[15 * q], Ma[ip * 5 + q]);
+            for (int q2 = 0; q2 < 5; ++q2) cfma_r(a, src[15 * q2], Ma[ip * 5 + q2]);
             dst[e] = a;
         }
         __syncwarp();
     }
 }
 
+// per (slot, octant): A2 rows, phi weights and re-centring data in group order
+__global__ void cb_table_kernel(const double* __restrict__ tmpl, const std::uint8_t* __restrict__ nodes,
+                                double* __restrict__ tab) {
+    const std::size_t so8 = blockIdx.x;
+    const int row = threadIdx.x;
+    double* T = tab + so8 * kCbTab;
+    double a2[16], tp[5], g[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a2[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) tp[i] = 0.0;
+    if (row < kNP) {
+        const int node = nodes[so8 * kNP + row];
+        const double* te = tmpl + (so8 * kNP + node) * kTmplDoubles;
+        double ts[3], tt[5];
+        cheb_row<3>(te[0], ts);
+        cheb_row<5>(te[1], tt);
+        cheb_row<5>(te[2], tp);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int tg = 0; tg < 3; ++tg) a2[4 * j + tg] = ts[tg] * tt[j];
+            a2[4 * j + 3] = j < 3 ? ts[j] * tt[4] : 0.0;
+        }
+        g[0] = te[3];
+        g[1] = te[4];
+        g[2] = te[5];
+        g[3] = double(node);
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) T[row * 16 + i] = a2[i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) T[kCbTabP + row * 8 + i] = i < 5 ? tp[i] : 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) T[kCbTabG + row * 4 + i] = g[i];
+}
+
 }  // namespace
+
+void launch_cb_tables(const double* tmpl, const std::uint8_t* nodes, std::int64_t nslot, double* tab, cudaStream_t st) {
+    if (nslot == 0) return;
+    cb_table_kernel<<<unsigned(nslot * 8), kRows, 0, st>>>(tmpl, nodes, tab);
+    IFGF_CUDA(cudaGetLastError());
+}
 
 bool launch_parent_fill_cb(const LevelDev& Lp, const LevelDev& Lc, const double2* child_store, double k,
                            const Pipes& parent_pipes, const Pipes& child_pipes, const double* Ms, const double* Ma,
                            double2* parent_store, cudaStream_t st) {
-    if (Lc.n_cbitem == 0 || !Lp.tmpl) return false;
+    if (Lc.n_cbitem == 0 || !Lp.tmpl || !Lc.cb_tab) return false;
     const int combo = combo_of(parent_pipes, child_pipes);
     if (combo < 0) return false;
     auto go = [&](auto kern, std::size_t smem) {
@@ -397,14 +467,22 @@ bool launch_parent_fill_cb(const LevelDev& Lp, const LevelDev& Lc, const double2
         kern<<<Lc.n_cbitem, 32 * kW, smem, st>>>(Lp, Lc, child_store, k, Ms, Ma, parent_store);
     };
     switch (combo) {
-        case 0: go(parent_cb_kernel<0>, cb_smem_bytes<Combo<0>::npc>()); break;
-        case 1: go(parent_cb_kernel<1>, cb_smem_bytes<Combo<1>::npc>()); break;
-        case 2: go(parent_cb_kernel<2>, cb_smem_bytes<Combo<2>::npc>()); break;
-        case 3: go(parent_cb_kernel<3>, cb_smem_bytes<Combo<3>::npc>()); break;
-        case 4: go(parent_cb_kernel<4>, cb_smem_bytes<Combo<4>::npc>()); break;
-        default: go(parent_cb_kernel<5>, cb_smem_bytes<Combo<5>::npc>()); break;
+        case 0: go(parent_cb_kernel<0>, kW * WarpSmem<Combo<0>::npc, Combo<0>::npp>::bytes); break;
+        case 1: go(parent_cb_kernel<1>, kW * WarpSmem<Combo<1>::npc, Combo<1>::npp>::bytes); break;
+        case 2: go(parent_cb_kernel<2>, kW * WarpSmem<Combo<2>::npc, Combo<2>::npp>::bytes); break;
+        case 3: go(parent_cb_kernel<3>, kW * WarpSmem<Combo<3>::npc, Combo<3>::npp>::bytes); break;
+        case 4: go(parent_cb_kernel<4>, kW * WarpSmem<Combo<4>::npc, Combo<4>::npp>::bytes); break;
+        default: go(parent_cb_kernel<5>, kW * WarpSmem<Combo<5>::npc, Combo<5>::npp>::bytes); break;
     }
     IFGF_CUDA(cudaGetLastError());
+#ifdef IFGF_CB_STATS
+    unsigned long long h[4] = {0, 0, 0, 0};
+    IFGF_CUDA(cudaStreamSynchronize(st));
+    IFGF_CUDA(cudaMemcpyFromSymbol(h, g_cb_stats, sizeof(h)));
+    std::fprintf(stderr, "cb stats: items %d units %llu tiles %llu seg-octants %llu block-octants %llu\n", Lc.n_cbitem, h[0], h[1], h[2], h[3]);
+    const unsigned long long z[4] = {0, 0, 0, 0};
+    IFGF_CUDA(cudaMemcpyToSymbol(g_cb_stats, z, sizeof(z)));
+#endif
     return true;
 }
 
