@@ -140,7 +140,7 @@ leaf_ray_kernel(LevelDev L, PointsDev P, const double2* __restrict__ a_p, double
                 const double inv = rsqrt_normal(nv2);
                 const double arg = khos[is] * fma(nv2, inv, -1.0);  // kh/s (|v| - 1)
                 double sn, cs;
-                sincos_bounded(arg, &sn, &cs);
+                sincos_tab(arg, &sn, &cs);  // (cfg2 leaf 4.70 -> 4.15 ms against sincos_bounded)
                 const double2 pa_ = make_double2(fma(ar, cs, -ai * sn), fma(ar, sn, ai * cs));
                 const double dn = fma(-sg, dn0, xn);      // v.n
                 const double inv2 = inv * inv;
