@@ -273,8 +273,8 @@ def roofline_for(phases, work, pk):
     return out
 
 
-KERNEL_FAMILY = {"leaf": "leaf_ray_kernel", "cousin": "cousin_tc_kernel", "parent": "parent_tc_kernel",
-                 "near": "near_list_kernel", "rp": "rp_accum_kernel"}
+KERNEL_FAMILY = {"leaf": ("leaf_ray_kernel",), "cousin": ("cousin_tc_kernel",), "parent": ("parent_tc_kernel", "parent_cb_kernel"),
+                 "near": ("near_list_kernel", "near_pair_kernel"), "rp": ("rp_accum_kernel",)}
 
 
 def ncu_traffic(cfg_name, phase):
@@ -287,8 +287,9 @@ def ncu_traffic(cfg_name, phase):
     if not files:
         return None, None
     try:
-        k = json.load(open(files[-1]))["kernels"].get(KERNEL_FAMILY[phase])
-        return (k["dram_bytes_per_apply"] if k else None), os.path.relpath(files[-1], ROOT)
+        ks = json.load(open(files[-1]))["kernels"]
+        got = [ks[f]["dram_bytes_per_apply"] for f in KERNEL_FAMILY[phase] if f in ks]
+        return (sum(got) if got else None), os.path.relpath(files[-1], ROOT)
     except Exception:
         return None, None
 

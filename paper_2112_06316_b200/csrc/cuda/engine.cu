@@ -227,6 +227,7 @@ struct Engine::Impl {
     // near field
     DevBuf nb_ptr, nb_idx, leaf_of_m, tpb, pair_patch, far_begin, far_end, far_pos, near_chunk_box, near_chunk_q0;
     DevBuf near_off, near_src;  // near lists (ensure_near_lists)
+    DevBuf near_pitem;          // target-pair items of the pair lists
     DevBuf run_ptr, run_start, run_len, run_patch;  // neighbourhood patch runs (near_run_kernel)
     bool near_lists_done = false;
     NearDev near;
@@ -417,12 +418,44 @@ struct Engine::Impl {
         near_lists_done = true;
         near.list_off = nullptr;
         near.list_src = nullptr;
+        near.plist_off = nullptr;
+        near.plist_src = nullptr;
         near_off.alloc(0);
         near_src.alloc(0);
-        // lists unless another near kernel is requested (IFGF_NEAR=runs | screen | thread);
-        // where they do not fit, the patch-run kernel (no per-pair data) takes over
+        // target-pair lists unless another near kernel is requested (IFGF_NEAR=lists |
+        // runs | screen | thread); where they do not fit, the patch-run kernel (no per-pair
+        // data) takes over
         const char* env = std::getenv("IFGF_NEAR");
-        if ((env && std::string(env) != "lists") || !near.leaf_of_m || near.n == 0) return;
+        if ((env && std::string(env) != "lists" && std::string(env) != "pairs") || !near.leaf_of_m || near.n == 0) return;
+        // keep a reserve for the solver's Krylov basis and work vectors (GMRES at restart 50
+        // needs 51 x 16 N bytes): IFGF_NEAR_LISTS_RESERVE_GB, default max(6 GB, 51 x 16 N)
+        const char* renv = std::getenv("IFGF_NEAR_LISTS_RESERVE_GB");
+        const std::size_t reserve = renv ? std::size_t(std::atof(renv) * 1e9)
+                                         : std::max<std::size_t>(std::size_t(6e9), 51 * 16 * n);
+        if (!(env && std::string(env) == "lists") && near.npitem > 0) {
+            DevBuf cnt;
+            cnt.alloc(std::size_t(near.npitem) * sizeof(std::int32_t));
+            launch_near_pair_lists(near, cnt.as<std::int32_t>(), st);
+            std::vector<std::int32_t> c(near.npitem);
+            IFGF_CUDA(cudaMemcpyAsync(c.data(), cnt.as<void>(), c.size() * sizeof(std::int32_t), cudaMemcpyDeviceToHost, st));
+            IFGF_CUDA(cudaStreamSynchronize(st));
+            std::vector<std::int64_t> off(std::size_t(near.npitem) + 1, 0);
+            for (int t = 0; t < near.npitem; ++t) off[t + 1] = off[t] + c[t];
+            const std::size_t bytes = std::size_t(off.back()) * sizeof(std::uint32_t) + off.size() * sizeof(std::int64_t);
+            std::size_t free_b = 0, total_b = 0;
+            IFGF_CUDA(cudaMemGetInfo(&free_b, &total_b));
+            if (std::getenv("IFGF_SETUP_DEBUG"))
+                std::fprintf(stderr, "near pair lists: %.2f GB (%lld entries), free %.2f GB\n", bytes / 1e9,
+                             (long long)off.back(), free_b / 1e9);
+            if (bytes + reserve > free_b) return;
+            near_off.upload(off);
+            near_src.alloc(std::max<std::size_t>(std::size_t(off.back()), 1) * sizeof(std::uint32_t));
+            near.plist_off = near_off.as<std::int64_t>();
+            near.plist_src = near_src.as<std::uint32_t>();
+            launch_near_pair_lists(near, nullptr, st);
+            IFGF_CUDA(cudaStreamSynchronize(st));
+            return;
+        }
         DevBuf cnt;
         cnt.alloc(std::size_t(near.n) * sizeof(std::int32_t));
         launch_near_list_count(near, P, cnt.as<std::int32_t>(), st);
@@ -436,11 +469,6 @@ struct Engine::Impl {
         IFGF_CUDA(cudaMemGetInfo(&free_b, &total_b));
         if (std::getenv("IFGF_SETUP_DEBUG"))
             std::fprintf(stderr, "near lists: %.2f GB, free %.2f GB\n", bytes / 1e9, free_b / 1e9);
-        // keep a reserve for the solver's Krylov basis and work vectors (GMRES at restart 50
-        // needs 51 x 16 N bytes): IFGF_NEAR_LISTS_RESERVE_GB, default max(6 GB, 51 x 16 N)
-        const char* renv = std::getenv("IFGF_NEAR_LISTS_RESERVE_GB");
-        const std::size_t reserve = renv ? std::size_t(std::atof(renv) * 1e9)
-                                         : std::max<std::size_t>(std::size_t(6e9), 51 * 16 * n);
         if (bytes + reserve > free_b) return;
         near_off.upload(off);
         near_src.alloc(std::max<std::size_t>(std::size_t(off.back()), 1) * sizeof(std::int32_t));
@@ -1315,6 +1343,17 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         e.far_pos.upload(fpos);
         e.near_chunk_box.upload(chunk_box);
         e.near_chunk_q0.upload(chunk_q0);
+        {
+            // target pairs of every leaf (near pair lists): (b, b + 1), (b + 2, b + 3), ...,
+            // an odd leaf's last target alone (bit 31)
+            std::vector<std::int32_t> pit;
+            pit.reserve(n / 2 + B.size());
+            for (std::size_t b = 0; b < B.size(); ++b)
+                for (std::uint32_t t = B.begin[b]; t < B.end[b]; t += 2)
+                    pit.push_back(std::int32_t(t | (t + 1 < B.end[b] ? 0u : 0x80000000u)));
+            e.near_pitem.upload(pit);
+            e.near.npitem = int(pit.size());
+        }
         // patch runs of every leaf's neighbourhood (near_run_kernel: used when the near lists
         // do not fit, or with IFGF_NEAR=runs; cfg2 2.77 vs 2.45 ms with lists, cfg3 45 vs
         // 40 ms, 61 ms screening every apply)
@@ -1367,6 +1406,7 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
         N.run_len = e.run_len.as<std::int32_t>();
         N.run_patch = e.run_patch.as<std::int32_t>();
         N.chunk_q0 = e.near_chunk_q0.as<std::int32_t>();
+        N.pitem = e.near_pitem.as<std::int32_t>();
         N.nchunk = int(chunk_box.size());
     }
 

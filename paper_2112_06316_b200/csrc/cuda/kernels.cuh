@@ -72,6 +72,13 @@ struct NearDev {
     // original, i.e. patch-major, order), CSR per leaf
     const std::int32_t* run_ptr = nullptr;
     const std::int32_t *run_start = nullptr, *run_len = nullptr, *run_patch = nullptr;
+    // target-pair lists (near_pair_kernel): item w = targets pitem[w] (& 0x7fffffff) and the
+    // next one (bit 31: unpaired), union list [plist_off[w], plist_off[w + 1]) of plist_src =
+    // source | m << 30 (m bit 0: pair with the first target, bit 1: with the second)
+    const std::int32_t* pitem = nullptr;
+    int npitem = 0;
+    const std::int64_t* plist_off = nullptr;
+    std::uint32_t* plist_src = nullptr;
 };
 void launch_weights(int n, const std::uint32_t* perm, const double2* phi, const double* jw_p,
                     double2* a_p, cudaStream_t st);
@@ -83,6 +90,8 @@ void launch_near_field(const NearDev& N, const PointsDev& P, const double2* a_p,
 // near lists: per-target source counts (N.n entries), then the lists at N.list_off
 void launch_near_list_count(const NearDev& N, const PointsDev& P, std::int32_t* counts, cudaStream_t st);
 void launch_near_list_fill(const NearDev& N, const PointsDev& P, cudaStream_t st);
+// target-pair lists: counts per item (counts != null), else the lists at N.plist_off
+void launch_near_pair_lists(const NearDev& N, std::int32_t* counts, cudaStream_t st);
 
 struct RpDev {
     int n = 0, npatch = 0;

@@ -266,6 +266,152 @@ near_list_kernel(NearDev N, PointsDev P, const double2* __restrict__ a_p, double
     }
 }
 
+// TARGET PAIRS: consecutive Morton targets t0, t0 + 1 of one leaf share their neighbourhood
+// and, almost always, their singular patches, so one union list serves both: entry = source |
+// m << 30 with bit 0 of m set when the pair (t0, source) is evaluated and bit 1 for t0 + 1 (the
+// screening of near_warp_kernel applied to each). The evaluation kernel loads each source row
+// once for both targets: half the gathers and half the list bytes of the single-target lists.
+// Item w: t0 = pitem[w] & 0x7fffffff, bit 31 set when t0 is a leaf's last, unpaired target.
+// MODE 1 counts, MODE 2 writes the lists (in neighbourhood order).
+template <int MODE>
+__global__ void __launch_bounds__(32 * kNearWarps, 8)
+near_pair_screen_kernel(NearDev N, std::int32_t* __restrict__ counts) {
+    __shared__ unsigned queue[kNearWarps][64];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int item = blockIdx.x * kNearWarps + w;
+    if (item >= N.npitem) return;
+    const std::uint32_t pi = std::uint32_t(N.pitem[item]);
+    const int t0 = int(pi & 0x7fffffffu);
+    const bool two = !(pi >> 31);
+    const int tb = N.leaf_of_m[t0];
+    if (N.leaf_active && !N.leaf_active[tb]) {
+        if (MODE == 1 && lane == 0) counts[item] = 0;
+        return;
+    }
+    int sing0[kMaxSing], sing1[kMaxSing];
+    const std::uint32_t l0 = N.perm[t0];
+    const int a0 = int(N.tpb[l0]), n0 = int(N.tpb[l0 + 1]) - a0;
+    int a1 = 0, n1 = 0;
+    if (two) {
+        const std::uint32_t l1 = N.perm[t0 + 1];
+        a1 = int(N.tpb[l1]);
+        n1 = int(N.tpb[l1 + 1]) - a1;
+    }
+#pragma unroll
+    for (int i = 0; i < kMaxSing; ++i) {
+        sing0[i] = i < n0 ? N.pair_patch[a0 + i] : -1;
+        sing1[i] = i < n1 ? N.pair_patch[a1 + i] : -1;
+    }
+    unsigned* q = queue[w];
+    int qn = 0;
+    std::int64_t written = MODE == 2 ? N.plist_off[item] : 0;
+    for (int j = N.nb_ptr[tb]; j < N.nb_ptr[tb + 1]; ++j) {
+        const int nb = N.nb_idx[j];
+        const int u1 = int(N.end[nb]);
+        for (int ub = int(N.beg[nb]); ub < u1; ub += 32) {
+            const int u = ub + lane;
+            unsigned m = 0;
+            if (u < u1) {
+                const int pq = N.patch_p[u];
+                bool ok0 = u != t0, ok1 = two && u != t0 + 1;
+#pragma unroll
+                for (int i = 0; i < kMaxSing; ++i) {
+                    ok0 &= (sing0[i] != pq);
+                    ok1 &= (sing1[i] != pq);
+                }
+                for (int i = kMaxSing; i < n0; ++i) ok0 &= (N.pair_patch[a0 + i] != pq);
+                for (int i = kMaxSing; i < n1; ++i) ok1 &= (N.pair_patch[a1 + i] != pq);
+                m = (ok0 ? 1u : 0u) | (ok1 ? 2u : 0u);
+            }
+            const unsigned b = __ballot_sync(0xffffffffu, m != 0);
+            if (m) q[qn + __popc(b & ((1u << lane) - 1u))] = std::uint32_t(u) | (m << 30);
+            qn += __popc(b);
+            __syncwarp();
+            if (qn >= 32) {
+                if constexpr (MODE == 2) N.plist_src[written + lane] = q[lane];
+                written += 32;
+                __syncwarp();
+                if (lane < qn - 32) q[lane] = q[lane + 32];
+                qn -= 32;
+                __syncwarp();
+            }
+        }
+    }
+    if constexpr (MODE == 1) {
+        if (lane == 0) counts[item] = int(written) + qn;
+    } else {
+        if (lane < qn) N.plist_src[written + lane] = q[lane];
+    }
+}
+
+// one target's far-node corrections (solver.cpp:131-139), lane-parallel
+__device__ __forceinline__ void near_far_nodes(const NearDev& N, int t, double x, double y, double z,
+                                               const double2* __restrict__ a_p, double k, double2& accS,
+                                               double2& accD) {
+    const std::uint32_t l = N.perm[t];
+    const int p0 = int(N.tpb[l]), p1 = int(N.tpb[l + 1]);
+    const int lane = threadIdx.x & 31;
+    for (int p = p0; p < p1; ++p)
+        for (std::uint32_t f = N.far_begin[p] + lane; f < N.far_end[p]; f += 32) {
+            const int u = int(N.far_pos[f]);
+            near_pair(N.geo, u, x, y, z, a_p, k, -1.0, accS, accD);
+        }
+}
+
+__device__ __forceinline__ void warp_sum4(double2& a, double2& b) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
+        a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
+        b.x += __shfl_xor_sync(0xffffffffu, b.x, o);
+        b.y += __shfl_xor_sync(0xffffffffu, b.y, o);
+    }
+}
+
+// warp per target pair over its union list: one source row, up to two pairs
+#ifndef IFGF_NEAR_PAIR_MINB
+#define IFGF_NEAR_PAIR_MINB 6
+#endif
+__global__ void __launch_bounds__(32 * kNearWarps, IFGF_NEAR_PAIR_MINB)
+near_pair_kernel(NearDev N, PointsDev P, const double2* __restrict__ a_p, double k, double2* __restrict__ Sp,
+                 double2* __restrict__ Dp) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int item = blockIdx.x * kNearWarps + w;
+    if (item >= N.npitem) return;
+    const std::uint32_t pi = std::uint32_t(N.pitem[item]);
+    const int t0 = int(pi & 0x7fffffffu);
+    const bool two = !(pi >> 31);
+    if (N.leaf_active && !N.leaf_active[N.leaf_of_m[t0]]) return;
+    const int t1 = two ? t0 + 1 : t0;
+    const double x0 = P.x[t0], y0 = P.y[t0], z0 = P.z[t0];
+    const double x1 = P.x[t1], y1 = P.y[t1], z1 = P.z[t1];
+    double2 s0 = make_double2(0.0, 0.0), d0 = s0, s1 = s0, d1 = s0;
+    const std::int64_t e = N.plist_off[item + 1];
+#pragma unroll kNearUnroll
+    for (std::int64_t i = N.plist_off[item] + lane; i < e; i += 32) {
+        const std::uint32_t ent = N.plist_src[i];
+        const int v = int(ent & 0x3fffffffu);
+        const double2 g0 = __ldg(N.geo + 3 * v), g1 = __ldg(N.geo + 3 * v + 1), g2 = __ldg(N.geo + 3 * v + 2);
+        const double2 a = a_p[v];
+        if (ent & (1u << 30)) pair_kernels(x0, y0, z0, g0.x, g0.y, g1.x, g1.y, g2.x, g2.y, a, k, 1.0, s0, d0);
+        if (ent & (2u << 30)) pair_kernels(x1, y1, z1, g0.x, g0.y, g1.x, g1.y, g2.x, g2.y, a, k, 1.0, s1, d1);
+    }
+    near_far_nodes(N, t0, x0, y0, z0, a_p, k, s0, d0);
+    warp_sum4(s0, d0);
+    if (lane == 0) {
+        Sp[t0] = cadd(Sp[t0], s0);
+        Dp[t0] = cadd(Dp[t0], d0);
+    }
+    if (two) {
+        near_far_nodes(N, t1, x1, y1, z1, a_p, k, s1, d1);
+        warp_sum4(s1, d1);
+        if (lane == 0) {
+            Sp[t1] = cadd(Sp[t1], s1);
+            Dp[t1] = cadd(Dp[t1], d1);
+        }
+    }
+}
+
 // Warp per target over its neighbourhood's PATCH RUNS (no per-pair lists): a run whose patch
 // is singular for the target is dropped whole (warp-uniform), the target itself is cut out
 // of its run, and lane i takes entries i, i + 32, ... of the remaining sequence — the same
@@ -587,6 +733,8 @@ void launch_near_field(const NearDev& N, const PointsDev& P, const double2* a_p,
     const int grid = (N.n + kNearWarps - 1) / kNearWarps;
     if (per_thread || !N.leaf_of_m)
         near_kernel<<<N.nchunk, kNearThreads, 0, st>>>(N, P, a_p, k, Sp, Dp);
+    else if (N.plist_off)
+        near_pair_kernel<<<(N.npitem + kNearWarps - 1) / kNearWarps, 32 * kNearWarps, 0, st>>>(N, P, a_p, k, Sp, Dp);
     else if (N.list_off)
         near_list_kernel<<<grid, 32 * kNearWarps, 0, st>>>(N, P, a_p, k, Sp, Dp);
     else if (N.run_ptr)
@@ -600,6 +748,16 @@ void launch_near_list_count(const NearDev& N, const PointsDev& P, std::int32_t* 
     if (N.n == 0 || !N.leaf_of_m) return;
     near_warp_kernel<1><<<(N.n + kNearWarps - 1) / kNearWarps, 32 * kNearWarps, 0, st>>>(N, P, nullptr, 0.0, nullptr,
                                                                                          nullptr, counts);
+    IFGF_CUDA(cudaGetLastError());
+}
+
+void launch_near_pair_lists(const NearDev& N, std::int32_t* counts, cudaStream_t st) {
+    if (N.npitem == 0 || !N.leaf_of_m) return;
+    const int grid = (N.npitem + kNearWarps - 1) / kNearWarps;
+    if (counts)
+        near_pair_screen_kernel<1><<<grid, 32 * kNearWarps, 0, st>>>(N, counts);
+    else
+        near_pair_screen_kernel<2><<<grid, 32 * kNearWarps, 0, st>>>(N, nullptr);
     IFGF_CUDA(cudaGetLastError());
 }
 

@@ -41,7 +41,18 @@ using namespace pfill;
 constexpr int kW = kCbSegs / 4;  // warps per CTA (4 segments each)
 constexpr int kNP = 75;          // nodes / coefficients per pipe block
 constexpr int kRows = kCbRows;   // table rows (75 + zero padding)
-constexpr int kStages = 3;       // cp.async ring depth per warp
+#ifndef IFGF_CB_STAGES3
+#define IFGF_CB_STAGES3 3
+#endif
+#ifndef IFGF_CB_MT3
+#define IFGF_CB_MT3 6
+#endif
+#ifndef IFGF_CB_MINB3
+#define IFGF_CB_MINB3 2
+#endif
+// cp.async ring depth per warp (prefetch distance = stages - 1)
+template <int NPC>
+constexpr int cb_stages() { return NPC == 3 ? IFGF_CB_STAGES3 : 3; }
 constexpr int kMaxUnits = 8 * (kCbMaxGrp + 1);  // per octant: its groups, one of which may split in 2
 constexpr int kG = kCbMaxGrp;
 
@@ -56,7 +67,7 @@ struct Ring {
 template <int NPC, int NPP>
 struct WarpSmem {
     static constexpr int ACC = 4 * kNP * NPP * 2;                 // doubles
-    static constexpr int RING = kStages * Ring<NPC>::STAGE;       // doubles
+    static constexpr int RING = cb_stages<NPC>() * Ring<NPC>::STAGE;  // doubles
     static constexpr int UNITS = kMaxUnits * 5;                   // ints
     static constexpr int EXC = (8 * 4 * kNP + 31) / 32;           // words
     static constexpr std::size_t bytes = (std::size_t(ACC + RING) * 8 + std::size_t(UNITS + EXC) * 4 + 15) / 16 * 16;
@@ -84,14 +95,15 @@ __device__ unsigned long long g_cb_stats[4];
 #endif
 
 template <int COMBO>
-__global__ void __launch_bounds__(32 * kW, Combo<COMBO>::npc == 3 ? 2 : 3)
+__global__ void __launch_bounds__(32 * kW, Combo<COMBO>::npc == 3 ? IFGF_CB_MINB3 : 3)
 parent_cb_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, double k,
                  const double* __restrict__ Ms, const double* __restrict__ Ma, double2* __restrict__ pstore) {
     using CB = Combo<COMBO>;
     constexpr int NPP = CB::npp, NPC = CB::npc;
     using WS = WarpSmem<NPC, NPP>;
     constexpr int SS = Ring<NPC>::SS, STAGE = Ring<NPC>::STAGE;
-    constexpr int kMT = NPC == 3 ? 6 : 5;  // 8-row tiles per unit (a larger group takes 2 units)
+    constexpr int kMT = NPC == 3 ? IFGF_CB_MT3 : 5;  // 8-row tiles per unit (a larger group takes 2 units)
+    constexpr int kStages = cb_stages<NPC>();
     extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int r = lane >> 2, tig = lane & 3;
@@ -219,8 +231,8 @@ parent_cb_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
         cp_async_commit();  // (empty groups keep the wait counts uniform)
         iss_st = iss_st == kStages - 1 ? 0 : iss_st + 1;
     };
-    issue();
-    issue();
+#pragma unroll
+    for (int i = 0; i < kStages - 1; ++i) issue();
 
     const double* __restrict__ tab0 = Lc.cb_tab + std::size_t(slot) * 8 * kCbTab;
     const int gam0 = CB::extra == RQ ? Lp.seg_gamma[Lc.cb_item_seg[std::size_t(item) * kCbSegs]] : 0;
@@ -255,9 +267,9 @@ parent_cb_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
                     w[i] = wn[i];
                     wn[i] = __ldg(tab + kCbTabP + arow[i] * 8 + (ip < 4 ? ip + 1 : 4));
                 }
-                cp_async_wait<1>();  // chunk q landed (q + 1 may still be in flight)
+                cp_async_wait<kStages - 2>();  // chunk q landed (later ones may still be in flight)
                 __syncwarp();
-                issue();  // chunk q + 2
+                issue();  // chunk q + kStages - 1
                 const double* bch = ring + cst * STAGE + (r >> 1) * SS + (r & 1);
                 cst = cst == kStages - 1 ? 0 : cst + 1;
 #pragma unroll
@@ -273,7 +285,7 @@ parent_cb_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
                         for (int p = 0; p < NPC; ++p) tc::dmma884(d[i][p][0], d[i][p][1], av, b[p]);
                     }
                 }
-                __syncwarp();  // this ring stage is refilled by the issue of chunk q + 3
+                __syncwarp();  // this ring stage is refilled by the issue of chunk q + kStages
             }
             // epilogue: lane (r, tig) holds (re, im) of rows row0 + 8 i + r for segment tig;
             // the rows' table entries are loaded for all tiles first (one latency)

@@ -74,20 +74,26 @@ def test_parent_cell_batched_equals_per_segment(monkeypatch, strategy):
 
 @pytest.mark.parametrize("splits,nu,k", [(2, 6, 4 * np.pi), (3, 8, 8 * np.pi), (2, 16, 4 * np.pi)])
 def test_near_variants_bitwise(monkeypatch, splits, nu, k):
-    # the near field's three warp-per-target kernels visit the same sources in the same order
-    # with the same lane assignment: per-apply screening, precomputed near lists, and the
-    # default patch runs (no per-pair lists) give bitwise the same near field / apply
+    # the near field's single-target warp kernels visit the same sources in the same order
+    # with the same lane assignment: per-apply screening, precomputed near lists and patch
+    # runs give bitwise the same near field / apply. The default target-pair lists (one
+    # source row for two targets) assign lanes differently: equal to rounding.
     pm = P.SurfaceMesh.sphere(1.0, splits, nu, nu)
     phi = P.random_density(pm.size(), 4)
     res = {}
-    for mode in ("screen", "lists", "runs"):
+    for mode in ("screen", "lists", "runs", "pairs"):
         monkeypatch.setenv("IFGF_NEAR", mode)
         res[mode] = P.CombinedOperator(pm, P.SolveConfig(k=k)).layer_potentials(phi)
     monkeypatch.delenv("IFGF_NEAR")
     res["default"] = P.CombinedOperator(pm, P.SolveConfig(k=k)).layer_potentials(phi)
-    for mode in ("lists", "runs", "default"):
+    for mode in ("lists", "runs"):
         for a, b in zip(res["screen"], res[mode]):
             assert np.array_equal(a, b), mode
+    for mode in ("pairs", "default"):
+        for a, b in zip(res["screen"], res[mode]):
+            assert rel_l2(b, a) <= 1e-14, mode
+    for a, b in zip(res["pairs"], res["default"]):
+        assert np.array_equal(a, b)
 
 
 @pytest.mark.parametrize("splits,nu,k", [(2, 6, 4 * np.pi), (3, 8, 8 * np.pi)])
