@@ -355,17 +355,25 @@ struct Engine::Impl {
         IFGF_CUDA(cudaMemsetAsync(Dn.as<void>(), 0, vb, st));
         launch_weights(int(n), perm.as<std::uint32_t>(), phi, jw_p.as<double>(), a_p.as<double2>(), st);
         ++launches;
-        static const bool one_stream = [] {
+        // IFGF_SIDE_STREAM: 0 (default) = everything on st; 1 = near field and RP on the side
+        // stream; rp = only the (HBM-bound) RP on the side stream. Measured: cfg3 456.7 ms
+        // serial against 462.4 (1) and 461.9 (rp): every kernel fills the GPU on its own and
+        // the concurrent ones slow each other; cfg2 20.48 / 20.40 / 20.44 ms
+        static const int side_mode = [] {
             const char* e = std::getenv("IFGF_SIDE_STREAM");
-            return e && e[0] == '0';
+            if (e && e[0] == '1') return 1;
+            if (e && std::string(e) == "rp") return 2;
+            return 0;
         }();
+        const bool one_stream = side_mode == 0;
         cudaStream_t side = one_stream ? st : st2;
+        cudaStream_t near_st = side_mode == 1 ? side : st;
         if (!one_stream) {
             IFGF_CUDA(cudaEventRecord(ev_fork, st));
             IFGF_CUDA(cudaStreamWaitEvent(st2, ev_fork, 0));
         }
         auto side_work = [&] {
-            launch_near_field(near, P, a_p.as<double2>(), k, Sn.as<double2>(), Dn.as<double2>(), side);
+            launch_near_field(near, P, a_p.as<double2>(), k, Sn.as<double2>(), Dn.as<double2>(), near_st);
             launch_density_coeffs(rp, phi, coeffs.as<double2>(), side);
             launch_rp_accum(rp, coeffs.as<double2>(), Sn.as<double2>(), Dn.as<double2>(), side);
             IFGF_CUDA(cudaEventRecord(ev_join, side));

@@ -31,7 +31,8 @@ def test_nondefault_orders(ref, ps, pang):
 
 @pytest.mark.parametrize("env,value", [("IFGF_PARENT_TEMPLATES", "force"), ("IFGF_PARENT_TEMPLATES", "0"),
                                        ("IFGF_COUSIN_TC", "0"), ("IFGF_PARENT_CB", "1"),
-                                       ("IFGF_PARENT_CB", "force")])
+                                       ("IFGF_PARENT_CB", "force"), ("IFGF_SIDE_STREAM", "1"),
+                                       ("IFGF_SIDE_STREAM", "rp")])
 @pytest.mark.parametrize("splits,nu,k", [(2, 6, 4 * np.pi), (2, 16, 4 * np.pi), (3, 6, 8 * np.pi)])
 def test_kernel_variants(ref, monkeypatch, env, value, splits, nu, k):
     monkeypatch.setenv(env, value)  # read when the operator (and its kernels) are set up
