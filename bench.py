@@ -283,7 +283,13 @@ def ncu_traffic(cfg_name, phase):
     tools/ncu_launches.py); None when there is none."""
     import glob
 
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_launches_{cfg_name}.json")))
+    def tag_key(f):  # r02g < r02z < r02aa < r02ad: round, then tag length, then tag
+        import re
+
+        m = re.match(r"r(\d+)([a-z]*)_", os.path.basename(f))
+        return (int(m.group(1)), len(m.group(2)), m.group(2)) if m else (0, 0, "")
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_launches_{cfg_name}.json")), key=tag_key)
     if not files:
         return None, None
     try:
