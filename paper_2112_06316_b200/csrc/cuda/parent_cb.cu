@@ -388,38 +388,11 @@ parent_cb_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
     __syncwarp();
 
     // values -> coefficients (transform3) per segment; scratch = the warp's ring
-    double2* v1 = reinterpret_cast<double2*>(ring);
     for (int c = 0; c < 4; ++c) {
         const int seg = __shfl_sync(0xffffffffu, seg_l, c);
         if (seg < 0) continue;
-        double2* v0 = acc + c * kNP * NPP;  // node-major [node][pp]
-        double2* dst = pstore + std::size_t(seg) * NPP * kNP;
-        for (int e = lane; e < NPP * kNP; e += 32) {
-            const int blk = e / kNP, node = e % kNP;
-            const int is = node % 3, line = node / 3;
-            double2 a = make_double2(0.0, 0.0);
-            for (int q2 = 0; q2 < 3; ++q2) cfma_r(a, v0[(line * 3 + q2) * NPP + blk], Ms[is * 3 + q2]);
-            v1[e] = a;
-        }
-        __syncwarp();
-        for (int e = lane; e < NPP * kNP; e += 32) {
-            const int blk = e / kNP, node = e % kNP;
-            const int is = node % 3, it = (node / 3) % 5, ip = node / 15;
-            const double2* src = v1 + blk * kNP + is + 15 * ip;
-            double2 a = make_double2(0.0, 0.0);
-            for (int q2 = 0; q2 < 5; ++q2) cfma_r(a, src[3 * q2], Ma[it * 5 + q2]);
-            v0[e] = a;  // (pipe-major from here on)
-        }
-        __syncwarp();
-        for (int e = lane; e < NPP * kNP; e += 32) {
-            const int blk = e / kNP, node = e % kNP;
-            const int is = node % 3, it = (node / 3) % 5, ip = node / 15;
-            const double2* src = v0 + blk * kNP + is + 3 * it;
-            double2 a = make_double2(0.0, 0.0);
-            for (int q2 = 0; q2 < 5; ++q2) cfma_r(a, src[15 * q2], Ma[ip * 5 + q2]);
-            dst[e] = a;
-        }
-        __syncwarp();
+        transform3_warp<NPP>(acc + c * kNP * NPP, reinterpret_cast<double2*>(ring),
+                             pstore + std::size_t(seg) * NPP * kNP, Ms, Ma, lane);
     }
 }
 

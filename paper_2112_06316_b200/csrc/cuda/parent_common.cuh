@@ -5,6 +5,7 @@
 
 #include <initializer_list>
 
+#include "dev_common.cuh"
 #include "kernels.cuh"
 
 namespace ifgfb200 {
@@ -70,6 +71,71 @@ inline int combo_of(const Pipes& pp, const Pipes& pc) {
     return -1;
 }
 
+
+// values -> coefficients of one parent segment (transform3, ifgf.cpp:560-562) by one warp:
+// v0 holds the node values node-major ([node][NPP], node = is + 3 (it + 5 ip)); v1 is a
+// scratch of NPP x 75; dst receives the pipe-major coefficient block. Each lane transforms
+// whole lines with the 3x3 (s) and 5x5 (theta, phi) matrices held in registers, adding the
+// terms in the same order as the element-wise form (bitwise the same results). v0 is
+// overwritten (pipe-major after the second pass).
+template <int NPP>
+__device__ __forceinline__ void transform3_warp(double2* v0, double2* v1, double2* __restrict__ dst,
+                                                const double* __restrict__ Ms, const double* __restrict__ Ma,
+                                                int lane) {
+    constexpr int kNP = 75;
+    double ms[9], ma[25];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) ms[i] = __ldg(Ms + i);
+#pragma unroll
+    for (int i = 0; i < 25; ++i) ma[i] = __ldg(Ma + i);
+    // s: line = (it, ip) of pipe pp
+    for (int l = lane; l < 25 * NPP; l += 32) {
+        const int pp = l / 25, line = l - pp * 25;
+        double2 in[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) in[q] = v0[(line * 3 + q) * NPP + pp];
+#pragma unroll
+        for (int is = 0; is < 3; ++is) {
+            double2 a = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) dev::cfma_r(a, in[q], ms[is * 3 + q]);
+            v1[pp * kNP + is + 3 * line] = a;
+        }
+    }
+    __syncwarp();
+    // theta: line = (is, ip) of pipe pp
+    for (int l = lane; l < 15 * NPP; l += 32) {
+        const int pp = l / 15, rem = l - pp * 15, is = rem % 3, ip = rem / 3;
+        const double2* src = v1 + pp * kNP + is + 15 * ip;
+        double2 in[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) in[q] = src[3 * q];
+#pragma unroll
+        for (int it = 0; it < 5; ++it) {
+            double2 a = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < 5; ++q) dev::cfma_r(a, in[q], ma[it * 5 + q]);
+            v0[pp * kNP + is + 3 * it + 15 * ip] = a;
+        }
+    }
+    __syncwarp();
+    // phi: line = (is, it) of pipe pp
+    for (int l = lane; l < 15 * NPP; l += 32) {
+        const int pp = l / 15, rem = l - pp * 15;  // rem = is + 3 it
+        const double2* src = v0 + pp * kNP + rem;
+        double2 in[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) in[q] = src[15 * q];
+#pragma unroll
+        for (int ip = 0; ip < 5; ++ip) {
+            double2 a = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < 5; ++q) dev::cfma_r(a, in[q], ma[ip * 5 + q]);
+            dst[pp * kNP + rem + 15 * ip] = a;
+        }
+    }
+    __syncwarp();
+}
 
 }  // namespace pfill
 }  // namespace ifgfb200

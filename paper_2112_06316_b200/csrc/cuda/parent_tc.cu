@@ -212,36 +212,8 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
     for (int w = 0; w < kParentMergeMax; ++w) {
         if (segs[w] < 0) break;
         __syncwarp();
-        double2* v0 = acc + w * kNP * NPP;
-        double2* v1 = reinterpret_cast<double2*>(geo);
-        double2* dst = pstore + std::size_t(segs[w]) * NPP * kNP;
-        // acc is node-major (node * NPP + i); transpose into pipe-major blocks while applying
-        // the s-direction transform, then theta, then phi
-        for (int e = lane; e < NPP * kNP; e += 32) {
-            const int blk = e / kNP, node = e % kNP;
-            const int is = node % kPS, line = node / kPS;
-            double2 a = make_double2(0.0, 0.0);
-            for (int q = 0; q < kPS; ++q) cfma_r(a, v0[(line * kPS + q) * NPP + blk], Ms[is * kPS + q]);
-            v1[e] = a;
-        }
-        __syncwarp();
-        for (int e = lane; e < NPP * kNP; e += 32) {
-            const int blk = e / kNP, node = e % kNP;
-            const int is = node % kPS, it = (node / kPS) % kPA, ip = node / (kPS * kPA);
-            const double2* src = v1 + blk * kNP + is + kPS * kPA * ip;
-            double2 a = make_double2(0.0, 0.0);
-            for (int q = 0; q < kPA; ++q) cfma_r(a, src[kPS * q], Ma[it * kPA + q]);
-            v0[e] = a;
-        }
-        __syncwarp();
-        for (int e = lane; e < NPP * kNP; e += 32) {
-            const int blk = e / kNP, node = e % kNP;
-            const int is = node % kPS, it = (node / kPS) % kPA, ip = node / (kPS * kPA);
-            const double2* src = v0 + blk * kNP + is + kPS * it;
-            double2 a = make_double2(0.0, 0.0);
-            for (int q = 0; q < kPA; ++q) cfma_r(a, src[kPS * kPA * q], Ma[ip * kPA + q]);
-            dst[e] = a;
-        }
+        transform3_warp<NPP>(acc + w * kNP * NPP, reinterpret_cast<double2*>(geo),
+                             pstore + std::size_t(segs[w]) * NPP * kNP, Ms, Ma, lane);
     }
 }
 
