@@ -331,41 +331,61 @@ __device__ inline void block_transform(double2* v0, double2* v1, int nblk, int p
     }
 }
 
-// the same transform with compile-time orders (index arithmetic by constants, loops unrolled);
-// identical arithmetic, so identical results
+// the same transform with compile-time orders, CTA-wide and line by line: each thread
+// transforms whole lines (PS or PA values in, as many out) with the matrices in registers;
+// the same terms in the same order as the element-wise form, so identical results
 template <int PS, int PA>
 __device__ inline void block_transform_c(double2* v0, double2* v1, int nblk, const double* __restrict__ Ms,
                                          const double* __restrict__ Ma, double2* __restrict__ dst) {
     constexpr int P = PS * PA * PA;
-    const int total = nblk * P;
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {  // along s
-        const int blk = e / P, node = e % P;
-        const int is = node % PS, line = node / PS;
+    double ms[PS * PS], ma[PA * PA];
+#pragma unroll
+    for (int i = 0; i < PS * PS; ++i) ms[i] = __ldg(Ms + i);
+#pragma unroll
+    for (int i = 0; i < PA * PA; ++i) ma[i] = __ldg(Ma + i);
+    for (int l = threadIdx.x; l < nblk * PA * PA; l += blockDim.x) {  // along s: line (it, ip)
+        const int blk = l / (PA * PA), line = l - blk * (PA * PA);
         const double2* src = v0 + blk * P + line * PS;
-        double2 acc = make_double2(0.0, 0.0);
+        double2 in[PS];
 #pragma unroll
-        for (int q = 0; q < PS; ++q) cfma_r(acc, src[q], Ms[is * PS + q]);
-        v1[e] = acc;
+        for (int q = 0; q < PS; ++q) in[q] = src[q];
+#pragma unroll
+        for (int is = 0; is < PS; ++is) {
+            double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < PS; ++q) cfma_r(acc, in[q], ms[is * PS + q]);
+            v1[blk * P + line * PS + is] = acc;
+        }
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {  // along theta
-        const int blk = e / P, node = e % P;
-        const int is = node % PS, it = (node / PS) % PA, ip = node / (PS * PA);
+    for (int l = threadIdx.x; l < nblk * PS * PA; l += blockDim.x) {  // along theta: line (is, ip)
+        const int blk = l / (PS * PA), rem = l - blk * (PS * PA), is = rem % PS, ip = rem / PS;
         const double2* src = v1 + blk * P + is + PS * PA * ip;
-        double2 acc = make_double2(0.0, 0.0);
+        double2 in[PA];
 #pragma unroll
-        for (int q = 0; q < PA; ++q) cfma_r(acc, src[PS * q], Ma[it * PA + q]);
-        v0[e] = acc;
+        for (int q = 0; q < PA; ++q) in[q] = src[PS * q];
+#pragma unroll
+        for (int it = 0; it < PA; ++it) {
+            double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < PA; ++q) cfma_r(acc, in[q], ma[it * PA + q]);
+            v0[blk * P + is + PS * it + PS * PA * ip] = acc;
+        }
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {  // along phi
-        const int blk = e / P, node = e % P;
-        const int is = node % PS, it = (node / PS) % PA, ip = node / (PS * PA);
-        const double2* src = v0 + blk * P + is + PS * it;
-        double2 acc = make_double2(0.0, 0.0);
+    for (int l = threadIdx.x; l < nblk * PS * PA; l += blockDim.x) {  // along phi: line (is, it)
+        const int blk = l / (PS * PA), rem = l - blk * (PS * PA);  // rem = is + PS it
+        const double2* src = v0 + blk * P + rem;
+        double2 in[PA];
 #pragma unroll
-        for (int q = 0; q < PA; ++q) cfma_r(acc, src[PS * PA * q], Ma[ip * PA + q]);
-        dst[e] = acc;
+        for (int q = 0; q < PA; ++q) in[q] = src[PS * PA * q];
+#pragma unroll
+        for (int ip = 0; ip < PA; ++ip) {
+            double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < PA; ++q) cfma_r(acc, in[q], ma[ip * PA + q]);
+            dst[blk * P + rem + PS * PA * ip] = acc;
+        }
     }
 }
 

@@ -163,7 +163,7 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
                     row[kRowLen + 2 * pc] = fx;
                     row[kRowLen + 2 * pc + 1] = fy;
                 }
-                row[kNode] = double(node + kNP * ws);  // accumulator row of (segment, node)
+                row[kNode] = __longlong_as_double((long long)(node + kNP * ws));  // accumulator row of (segment, node), as integer bits
             }
             __syncwarp();
             // 2. 8-evaluation tensor-core tiles against the child block (issuing the next
@@ -196,7 +196,7 @@ parent_tc_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
 #pragma unroll
                     for (int pc = 0; pc < NPC; ++pc)
                         if (tig == pc) dst = CB::dst(pc);
-                    double2& a = acc[int(gp[kNode]) * NPP + dst];
+                    double2& a = acc[int(__double_as_longlong(gp[kNode])) * NPP + dst];
                     a = cadd(a, ctb);
                 }
             };
