@@ -369,9 +369,16 @@ __device__ __forceinline__ void warp_sum4(double2& a, double2& b) {
 }
 
 // warp per target pair over its union list: one source row, up to two pairs
+// 8 CTAs (32 warps) per SM at 64 registers (a few spills) and 3 list entries in flight per
+// lane measured best (cfg2 near 2.46 -> 2.21 ms; 6 CTAs at 78 registers, unroll 2: 2.46 ms;
+// 10 CTAs: 2.63 ms)
 #ifndef IFGF_NEAR_PAIR_MINB
-#define IFGF_NEAR_PAIR_MINB 6
+#define IFGF_NEAR_PAIR_MINB 8
 #endif
+#ifndef IFGF_NEAR_PAIR_UNROLL
+#define IFGF_NEAR_PAIR_UNROLL 3
+#endif
+constexpr int kNearPairUnroll = IFGF_NEAR_PAIR_UNROLL;
 __global__ void __launch_bounds__(32 * kNearWarps, IFGF_NEAR_PAIR_MINB)
 near_pair_kernel(NearDev N, PointsDev P, const double2* __restrict__ a_p, double k, double2* __restrict__ Sp,
                  double2* __restrict__ Dp) {
@@ -387,7 +394,7 @@ near_pair_kernel(NearDev N, PointsDev P, const double2* __restrict__ a_p, double
     const double x1 = P.x[t1], y1 = P.y[t1], z1 = P.z[t1];
     double2 s0 = make_double2(0.0, 0.0), d0 = s0, s1 = s0, d1 = s0;
     const std::int64_t e = N.plist_off[item + 1];
-#pragma unroll kNearUnroll
+#pragma unroll kNearPairUnroll
     for (std::int64_t i = N.plist_off[item] + lane; i < e; i += 32) {
         const std::uint32_t ent = N.plist_src[i];
         const int v = int(ent & 0x3fffffffu);
