@@ -12,6 +12,8 @@
 //      step 1), adds the D pipes of each evaluation (one shuffle) and accumulates into the
 //      target's shared accumulators.
 // Every target gets its cousins' contributions in cousin-list order: deterministic.
+#include <cstdlib>
+
 #include "ifgf_device.cuh"
 #include "kernels.cuh"
 #include "tc_common.cuh"
@@ -28,7 +30,7 @@ constexpr int kCG = kRowLen + 6;  // A slots, T(phi), the pipe factors (3 comple
 
 // CODE = f0 f1 f2 as decimal digits (factor codes of the pipes) for the common pipe sets, so the
 // pipe logic folds at compile time; 0 = read them from pp
-template <int NPC, int CODE>
+template <int NPC, int CODE, bool BPRE>
 __global__ void __launch_bounds__(kThreads, 4)
 cousin_tc_kernel(LevelDev L, PointsDev P, const double2* __restrict__ store, double k, Pipes pp,
                  double2* __restrict__ Sp, double2* __restrict__ Dp) {
@@ -68,6 +70,16 @@ cousin_tc_kernel(LevelDev L, PointsDev P, const double2* __restrict__ store, dou
         const int sb = L.cz_idx[j];
         if (L.active && !L.active[sb]) continue;  // source box owned by another rank
         const int so = act ? L.cev_seg[ev0 + std::int64_t(j - j0) * n_t] : -1;
+        // BPRE: the first group's B fragments (the first active lane's segment) are loaded
+        // before the geometry step, so their latency hides behind it
+        unsigned pending = __ballot_sync(0xffffffffu, act);
+        double bq0[LY::NB];
+        if constexpr (BPRE) {
+            if (pending) {
+                const int seg0 = __shfl_sync(0xffffffffu, so, __ffs(pending) - 1);
+                load_b<NPC>(store + std::size_t(seg0) * NPC * kNP, lane, bq0);
+            }
+        }
         if (act) {
             const double vx = x - L.cx[sb], vy = y - L.cy[sb], vz = z - L.cz[sb];
             const double r2 = fma(vx, vx, fma(vy, vy, vz * vz));
@@ -89,7 +101,7 @@ cousin_tc_kernel(LevelDev L, PointsDev P, const double2* __restrict__ store, dou
             }
         }
         __syncwarp();
-        unsigned pending = __ballot_sync(0xffffffffu, act);
+        bool first = true;
         while (pending) {
             const int seg = __shfl_sync(0xffffffffu, so, __ffs(pending) - 1);
             const unsigned gmask = __ballot_sync(0xffffffffu, act && so == seg);
@@ -98,7 +110,13 @@ cousin_tc_kernel(LevelDev L, PointsDev P, const double2* __restrict__ store, dou
             __syncwarp();
             const int count = __popc(gmask);
             double bq[LY::NB];
-            load_b<NPC>(store + std::size_t(seg) * NPC * kNP, lane, bq);
+            if (BPRE && first) {
+#pragma unroll
+                for (int i = 0; i < LY::NB; ++i) bq[i] = bq0[i];
+            } else {
+                load_b<NPC>(store + std::size_t(seg) * NPC * kNP, lane, bq);
+            }
+            first = false;
             for (int t0 = 0; t0 < count; t0 += 8) {
                 const bool valid = t0 + r < count;
                 const int src = valid ? slist[warp][t0 + r] : 0;
@@ -134,15 +152,24 @@ bool launch_cousin_eval_tc(const LevelDev& L, const PointsDev& P, const double2*
     if (L.nwchunk == 0) return true;
     const int grid = (L.nwchunk + kWarps - 1) / kWarps;
     const int code = pipes.f[0] * 100 + (pipes.n > 1 ? pipes.f[1] * 10 : 0) + (pipes.n > 2 ? pipes.f[2] : 0);
+    // IFGF_COUSIN_BPRE=0|1 (default 1): first group's coefficients loaded before the geometry
+    static const bool bpre = [] {
+        const char* e = std::getenv("IFGF_COUSIN_BPRE");
+        return !(e && e[0] == '0');
+    }();
+    auto go = [&](auto kpre, auto kplain) {
+        if (bpre) kpre<<<grid, kThreads, 0, st>>>(L, P, store, k, pipes, Sp, Dp);
+        else kplain<<<grid, kThreads, 0, st>>>(L, P, store, k, pipes, Sp, Dp);
+    };
     switch (code) {
-        case 123: cousin_tc_kernel<3, 123><<<grid, kThreads, 0, st>>>(L, P, store, k, pipes, Sp, Dp); break;
-        case 140: cousin_tc_kernel<2, 140><<<grid, kThreads, 0, st>>>(L, P, store, k, pipes, Sp, Dp); break;
-        case 100: cousin_tc_kernel<1, 100><<<grid, kThreads, 0, st>>>(L, P, store, k, pipes, Sp, Dp); break;
+        case 123: go(cousin_tc_kernel<3, 123, true>, cousin_tc_kernel<3, 123, false>); break;
+        case 140: go(cousin_tc_kernel<2, 140, true>, cousin_tc_kernel<2, 140, false>); break;
+        case 100: go(cousin_tc_kernel<1, 100, true>, cousin_tc_kernel<1, 100, false>); break;
         default:
             switch (pipes.n) {
-                case 1: cousin_tc_kernel<1, 0><<<grid, kThreads, 0, st>>>(L, P, store, k, pipes, Sp, Dp); break;
-                case 2: cousin_tc_kernel<2, 0><<<grid, kThreads, 0, st>>>(L, P, store, k, pipes, Sp, Dp); break;
-                default: cousin_tc_kernel<3, 0><<<grid, kThreads, 0, st>>>(L, P, store, k, pipes, Sp, Dp); break;
+                case 1: go(cousin_tc_kernel<1, 0, true>, cousin_tc_kernel<1, 0, false>); break;
+                case 2: go(cousin_tc_kernel<2, 0, true>, cousin_tc_kernel<2, 0, false>); break;
+                default: go(cousin_tc_kernel<3, 0, true>, cousin_tc_kernel<3, 0, false>); break;
             }
     }
     IFGF_CUDA(cudaGetLastError());
