@@ -19,6 +19,13 @@ constexpr int kCbTabP = kCbRows * 16;            // table: A2 [80][16], then phi
 constexpr int kCbTabG = kCbTabP + kCbRows * 8;   // then re-centring data [80][4] (ratio1, 1/r_c)
 constexpr int kCbTab = kCbTabG + kCbRows * 4;    // doubles per (slot, octant)
 constexpr int kCbMaxGrp = 8;        // child-cell groups per (parent cell, octant) in a batched item
+#ifndef IFGF_CB_MT3
+#define IFGF_CB_MT3 6
+#endif
+// 8-row tiles per unit of the cell-batched kernel (a larger child-cell group is split in two
+// units): IFGF_CB_MT3 where the children carry 3 pipes, 5 otherwise
+constexpr int kCbMaxTiles3 = IFGF_CB_MT3, kCbMaxTiles = 5;
+constexpr int kCbMaxUnits = 8 * (kCbMaxGrp + 1);  // per warp: per octant its groups, one of which may split
 
 struct LevelDev {
     int d = 0;
@@ -57,13 +64,16 @@ struct LevelDev {
     // = up to kCbSegs parent segments of ONE parent cone cell (template slot cb_item_slot[i],
     // segments cb_item_seg[i * kCbSegs + j], -1: none). Per (slot, octant): the 75 nodes in
     // child-cell group order (cb_nodes), group starts (cb_gstart, kCbMaxGrp + 1 entries) and
-    // count (cb_ngrp). Per (item, j, octant): child box (cb_child) and per group the child
-    // segment (cb_cso, -1: none). Evaluations whose host-decided child segment differs from
-    // the template's group (ties) are exceptions: key j | octant << 8 | node << 16, cso.
+    // count (host only). Per (item, j, octant): child box (cb_child). Per (item, warp) the
+    // host lists the warp's UNITS (cb_unit_begin, 5 ints each in cb_unit): first table row |
+    // tiles << 8 | group end row << 16 | octant << 24, then the child segment of each of the
+    // warp's 4 parent segments in that (octant, child-cell group) (-1: none). Evaluations
+    // whose host-decided child segment differs from the template's group (ties) are
+    // exceptions: key j | octant << 8 | node << 16, cso.
     int n_cbitem = 0;
     const std::int32_t *cb_item_slot = nullptr, *cb_item_seg = nullptr;
-    const std::uint8_t *cb_nodes = nullptr, *cb_gstart = nullptr, *cb_ngrp = nullptr;
-    const std::int32_t *cb_child = nullptr, *cb_cso = nullptr;
+    const std::uint8_t* cb_nodes = nullptr;
+    const std::int32_t *cb_child = nullptr, *cb_unit_begin = nullptr, *cb_unit = nullptr;
     const std::int64_t* cb_exc_begin = nullptr;
     const std::uint32_t* cb_exc_key = nullptr;
     const std::int32_t* cb_exc_cso = nullptr;

@@ -156,7 +156,7 @@ struct LevelBufs {
         box_seg_begin, pev_begin, pev_seg, pev_perm, pgrp_begin, pgrp_seg, pgrp_start, pgrp_count, ch_ptr, ch_idx, s_nodes, th_nodes, ph_nodes, th_sin, th_cos, ph_sin, ph_cos, thc_cos, thc_sin, phc_cos, phc_sin,
         chunk_box, chunk_q0, wchunk_box, wchunk_q0, tmpl_slot, tmpl, seg_code, litem_seg0,
         litem_nseg, litem_split, litem_box0, litem_box1, pgrp_rec, pitem_seg, pitem_grp, pitem_ev;
-    DevBuf cb_item_slot, cb_item_seg, cb_nodes, cb_gstart, cb_ngrp, cb_child, cb_cso, cb_exc_begin, cb_exc_key,
+    DevBuf cb_item_slot, cb_item_seg, cb_nodes, cb_child, cb_unit_begin, cb_unit, cb_exc_begin, cb_exc_key,
         cb_exc_cso, cb_tab;
 };
 
@@ -1118,6 +1118,53 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
                     }
                 }
             }
+            // unit lists (parent_cb.cu): per (item, warp of 4 segments), per octant with a child
+            // and per child-cell group met by one of the 4, the rows [gs, ge) in at most
+            // max_tiles 8-row tiles per unit (a larger group: two units) and the 4 child segments
+            constexpr int kW = kCbSegs / 4;
+            const int max_tiles = e.pipes_at(d, true, true, e.strategy).size() == 3 ? kCbMaxTiles3 : kCbMaxTiles;
+            std::vector<std::vector<std::int32_t>> ulist(static_cast<std::size_t>(n_item) * kW);
+#pragma omp parallel for schedule(dynamic, 256)
+            for (std::int64_t it = 0; it < n_item; ++it) {
+                const int sl = item_slot[it];
+                for (int w = 0; w < kW; ++w) {
+                    std::vector<std::int32_t>& U = ulist[std::size_t(it) * kW + w];
+                    for (int o = 0; o < 8; ++o) {
+                        const std::size_t so8 = std::size_t(sl) * 8 + o;
+                        for (int g = 0; g < ngrp[so8]; ++g) {
+                            std::int32_t c4[4];
+                            bool any = false;
+                            for (int c = 0; c < 4; ++c) {
+                                const std::size_t j = std::size_t(it) * kCbSegs + 4 * w + c;
+                                c4[c] = child[j * 8 + o] >= 0 ? cso[(j * 8 + o) * kCbMaxGrp + g] : -1;
+                                any = any || c4[c] >= 0;
+                            }
+                            if (!any) continue;
+                            const int gs = gstart[so8 * (kCbMaxGrp + 1) + g], ge = gstart[so8 * (kCbMaxGrp + 1) + g + 1];
+                            const int mt = (ge - gs + 7) >> 3;
+                            const int nh = mt > max_tiles ? 2 : 1;
+                            for (int h = 0; h < nh; ++h) {
+                                const int t0 = h == 0 ? 0 : (mt + 1) / 2, t1 = nh == 1 ? mt : (h == 0 ? (mt + 1) / 2 : mt);
+                                U.push_back((gs + 8 * t0) | ((t1 - t0) << 8) | (ge << 16) | (o << 24));
+                                U.insert(U.end(), c4, c4 + 4);
+                            }
+                        }
+                    }
+                    if (U.size() > std::size_t(kCbMaxUnits) * 5) throw std::logic_error("cell-batched unit list too long");
+                }
+            }
+            std::vector<std::int32_t> unit_begin(ulist.size() + 1, 0);
+            for (std::size_t i = 0; i < ulist.size(); ++i) {
+                const std::size_t nxt = std::size_t(unit_begin[i]) + ulist[i].size() / 5;
+                if (nxt > std::size_t(std::numeric_limits<std::int32_t>::max())) throw std::logic_error("cell-batched unit count overflow");
+                unit_begin[i + 1] = std::int32_t(nxt);
+            }
+            std::vector<std::int32_t> unit(std::size_t(unit_begin.back()) * 5);
+#pragma omp parallel for schedule(static)
+            for (std::int64_t i = 0; i < std::int64_t(ulist.size()); ++i)
+                std::copy(ulist[i].begin(), ulist[i].end(), unit.begin() + std::size_t(unit_begin[i]) * 5);
+            ulist.clear();
+            ulist.shrink_to_fit();
             std::vector<std::int64_t> exc_begin(n_item + 1, 0);
             for (std::int64_t it = 0; it < n_item; ++it) exc_begin[it + 1] = exc_begin[it] + std::int64_t(exc[it].size());
             std::vector<std::uint32_t> exc_key(static_cast<std::size_t>(exc_begin[n_item]));
@@ -1150,10 +1197,9 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
             b.cb_item_slot.upload(item_slot);
             b.cb_item_seg.upload(item_seg);
             b.cb_nodes.upload(nodes);
-            b.cb_gstart.upload(gstart);
-            b.cb_ngrp.upload(ngrp);
             b.cb_child.upload(child);
-            b.cb_cso.upload(cso);
+            b.cb_unit_begin.upload(unit_begin);
+            b.cb_unit.upload(unit);
             b.cb_exc_begin.upload(exc_begin);
             b.cb_exc_key.upload(exc_key);
             b.cb_exc_cso.upload(exc_cso);
@@ -1162,10 +1208,9 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
             L.cb_item_slot = b.cb_item_slot.as<std::int32_t>();
             L.cb_item_seg = b.cb_item_seg.as<std::int32_t>();
             L.cb_nodes = b.cb_nodes.as<std::uint8_t>();
-            L.cb_gstart = b.cb_gstart.as<std::uint8_t>();
-            L.cb_ngrp = b.cb_ngrp.as<std::uint8_t>();
             L.cb_child = b.cb_child.as<std::int32_t>();
-            L.cb_cso = b.cb_cso.as<std::int32_t>();
+            L.cb_unit_begin = b.cb_unit_begin.as<std::int32_t>();
+            L.cb_unit = b.cb_unit.as<std::int32_t>();
             L.cb_exc_begin = b.cb_exc_begin.as<std::int64_t>();
             L.cb_exc_key = b.cb_exc_key.as<std::uint32_t>();
             L.cb_exc_cso = b.cb_exc_cso.as<std::int32_t>();

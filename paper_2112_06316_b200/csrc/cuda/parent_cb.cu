@@ -44,17 +44,13 @@ constexpr int kRows = kCbRows;   // table rows (75 + zero padding)
 #ifndef IFGF_CB_STAGES3
 #define IFGF_CB_STAGES3 3
 #endif
-#ifndef IFGF_CB_MT3
-#define IFGF_CB_MT3 6
-#endif
 #ifndef IFGF_CB_MINB3
 #define IFGF_CB_MINB3 2
 #endif
 // cp.async ring depth per warp (prefetch distance = stages - 1)
 template <int NPC>
 constexpr int cb_stages() { return NPC == 3 ? IFGF_CB_STAGES3 : 3; }
-constexpr int kMaxUnits = 8 * (kCbMaxGrp + 1);  // per octant: its groups, one of which may split in 2
-constexpr int kG = kCbMaxGrp;
+constexpr int kMaxUnits = kCbMaxUnits;
 
 template <int NPC>
 struct Ring {
@@ -102,7 +98,7 @@ parent_cb_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
     constexpr int NPP = CB::npp, NPC = CB::npc;
     using WS = WarpSmem<NPC, NPP>;
     constexpr int SS = Ring<NPC>::SS, STAGE = Ring<NPC>::STAGE;
-    constexpr int kMT = NPC == 3 ? IFGF_CB_MT3 : 5;  // 8-row tiles per unit (a larger group takes 2 units)
+    constexpr int kMT = kCbMaxTiles3 > kCbMaxTiles ? kCbMaxTiles3 : kCbMaxTiles;  // 8-row tiles per unit (host-split)
     constexpr int kStages = cb_stages<NPC>();
     extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -121,49 +117,24 @@ parent_cb_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
     for (int i = lane; i < WS::ACC / 2; i += 32) acc[i] = make_double2(0.0, 0.0);
     for (int i = lane; i < WS::EXC; i += 32) excb[i] = 0u;
 
-    // ---- unit list: lane = c + 4 o holds segment c's child in octant o, then per octant
-    // lane = c + 4 g the child segment of segment c in group g
-    const int c_l = lane & 3, o_l = lane >> 2;
+    // ---- unit list of this warp (host-built, engine.cu "cell-batched parent items")
+    const int c_l = lane & 3;
     int seg_l = iseg[c_l];
     if (seg_l >= 0 && Lp.active && !Lp.active[Lp.seg_box[seg_l]]) seg_l = -1;
-    int ch_l = -1;
-    if (seg_l >= 0) {
-        ch_l = Lc.cb_child[(std::size_t(item) * kCbSegs + 4 * warp + c_l) * 8 + o_l];
-        if (ch_l >= 0 && Lc.active && !Lc.active[ch_l]) ch_l = -1;
-    }
-    const unsigned has = __ballot_sync(0xffffffffu, ch_l >= 0);
-    // all octants' child segments and group bounds at once (independent loads)
-    int cso_o[8], gb_o[8];
-    int ng_l = lane < 8 ? Lc.cb_ngrp[std::size_t(slot) * 8 + lane] : 0;
-#pragma unroll
-    for (int o = 0; o < 8; ++o) {
-        const int ng = __shfl_sync(0xffffffffu, ng_l, o);
-        const int chc = __shfl_sync(0xffffffffu, ch_l, c_l + 4 * o);
-        const int g = lane >> 2;
-        cso_o[o] = (g < ng && chc >= 0)
-                       ? Lc.cb_cso[((std::size_t(item) * kCbSegs + 4 * warp + c_l) * 8 + o) * kG + g]
-                       : -1;
-        gb_o[o] = lane <= ng ? Lc.cb_gstart[(std::size_t(slot) * 8 + o) * (kG + 1) + lane] : 0;
-    }
-    int nu = 0;
-#pragma unroll
-    for (int o = 0; o < 8; ++o) {
-        if (((has >> (4 * o)) & 0xfu) == 0u) continue;
-        const int ng = __shfl_sync(0xffffffffu, ng_l, o);
-        const unsigned cm = __ballot_sync(0xffffffffu, cso_o[o] >= 0);
-        for (int g = 0; g < ng; ++g) {
-            if (((cm >> (4 * g)) & 0xfu) == 0u) continue;
-            const int gs = __shfl_sync(0xffffffffu, gb_o[o], g), ge = __shfl_sync(0xffffffffu, gb_o[o], g + 1);
-            const int cso = __shfl_sync(0xffffffffu, cso_o[o], (lane & 3) + 4 * g);
-            const int mt = (ge - gs + 7) >> 3;
-            const int nh = mt > kMT ? 2 : 1;
-            for (int h = 0; h < nh; ++h) {
-                const int t0 = h == 0 ? 0 : (mt + 1) / 2, t1 = nh == 1 ? mt : (h == 0 ? (mt + 1) / 2 : mt);
-                int* U = units + nu * 5;
-                if (lane == 0) U[0] = (gs + 8 * t0) | ((t1 - t0) << 8) | (ge << 16) | (o << 24);
-                if (lane < 4) U[1 + lane] = cso;
-                ++nu;
+    const int ub = Lc.cb_unit_begin[item * kW + warp];
+    const int nu = Lc.cb_unit_begin[item * kW + warp + 1] - ub;
+    for (int i = lane; i < nu * 5; i += 32) units[i] = Lc.cb_unit[std::size_t(ub) * 5 + i];
+    if (Lp.active || Lc.active) {  // multi-GPU: children without sources of this rank drop out
+        __syncwarp();
+        for (int i = lane; i < nu * 4; i += 32) {
+            const int u = i >> 2, c = i & 3, o = units[u * 5] >> 24;
+            const int seg = iseg[c];
+            bool ok = seg >= 0 && !(Lp.active && !Lp.active[Lp.seg_box[seg]]);
+            if (ok) {
+                const int ch = Lc.cb_child[(std::size_t(item) * kCbSegs + 4 * warp + c) * 8 + o];
+                ok = ch >= 0 && !(Lc.active && !Lc.active[ch]);
             }
+            if (!ok) units[u * 5 + 1 + c] = -1;
         }
     }
 #ifdef IFGF_CB_STATS
@@ -172,10 +143,6 @@ parent_cb_kernel(LevelDev Lp, LevelDev Lc, const double2* __restrict__ cstore, d
         for (int ui = 0; ui < nu; ++ui) smt += (units[ui * 5] >> 8) & 0xff;
         atomicAdd(&g_cb_stats[0], (unsigned long long)nu);
         atomicAdd(&g_cb_stats[1], smt);
-        atomicAdd(&g_cb_stats[2], (unsigned long long)__popc(has));
-        unsigned long long bo = 0;
-        for (int o = 0; o < 8; ++o) bo += ((has >> (4 * o)) & 0xfu) ? 1 : 0;
-        atomicAdd(&g_cb_stats[3], bo);
     }
 #endif
     // exception bits of this warp's segments
