@@ -1,6 +1,8 @@
 #include "surface.hpp"
 
 #include <algorithm>
+#include <cstdint>
+#include <exception>
 #include <functional>
 #include <limits>
 
@@ -9,6 +11,27 @@
 namespace ifgfb200 {
 
 namespace {
+
+// patches are independent: loops over them run in parallel; the exception of the lowest
+// failing patch is rethrown, as the serial loop would have thrown it
+template <class F>
+void for_each_patch(std::size_t n, F&& body) {
+    std::exception_ptr err;
+    std::size_t err_at = n;
+#pragma omp parallel for schedule(dynamic, 16)
+    for (std::int64_t q = 0; q < std::int64_t(n); ++q) {
+        try {
+            body(std::size_t(q));
+        } catch (...) {
+#pragma omp critical(ifgf_surface_error)
+            if (std::size_t(q) < err_at) {
+                err_at = std::size_t(q);
+                err = std::current_exception();
+            }
+        }
+    }
+    if (err) std::rethrow_exception(err);
+}
 
 void derive_series(Patch& p) {
     for (int c = 0; c < 3; ++c) {
@@ -106,7 +129,7 @@ Surface assemble_surface(std::vector<Patch> patches, const Vec3& interior) {
     Surface s;
     s.patches = std::move(patches);
     s.interior = interior;
-    for (std::size_t q = 0; q < s.patches.size(); ++q) {
+    for_each_patch(s.patches.size(), [&](std::size_t q) {
         Patch& p = s.patches[q];
         if (p.nu < 1 || p.nv < 1 || p.du < 1 || p.dv < 1)
             throw InvalidArgument("assemble_surface: nonpositive patch dimensions");
@@ -121,7 +144,7 @@ Surface assemble_surface(std::vector<Patch> patches, const Vec3& interior) {
                                      std::to_string(q) + ")");
         }
         if (dot3(n, patch_point(p, 0.0, 0.0) - interior) < 0.0) p.orient = -1.0;
-    }
+    });
     s.patch_start.assign(s.patches.size() + 1, 0);
     for (std::size_t q = 0; q < s.patches.size(); ++q)
         s.patch_start[q + 1] = s.patch_start[q] + std::size_t(s.patches[q].nu) * s.patches[q].nv;
@@ -133,7 +156,7 @@ Surface assemble_surface(std::vector<Patch> patches, const Vec3& interior) {
     s.pu.resize(n);
     s.pv.resize(n);
     s.patch_of.resize(n);
-    for (std::size_t q = 0; q < s.patches.size(); ++q) {
+    for_each_patch(s.patches.size(), [&](std::size_t q) {
         const Patch& p = s.patches[q];
         std::vector<double> un, uw, vn, vw;
         cheb::fejer(p.nu, un, uw);
@@ -154,7 +177,7 @@ Surface assemble_surface(std::vector<Patch> patches, const Vec3& interior) {
                 s.pv[l] = vn[j];
                 s.patch_of[l] = int(q);
             }
-    }
+    });
     return s;
 }
 
@@ -167,11 +190,9 @@ std::vector<Patch> cube_sphere_patches(double radius, int splits, int nu, int nv
     const int axis[6] = {0, 0, 1, 1, 2, 2};
     const double sign[6] = {1, -1, 1, -1, 1, -1};
     const int m = 1 << splits;
-    std::vector<Patch> out;
-    out.reserve(6 * std::size_t(m) * m);
-    for (int f = 0; f < 6; ++f)
-        for (int a = 0; a < m; ++a)
-            for (int b = 0; b < m; ++b) {
+    std::vector<Patch> out(6 * std::size_t(m) * m);
+    for_each_patch(out.size(), [&](std::size_t idx) {
+                const int f = int(idx / (std::size_t(m) * m)), a = int(idx / m % m), b = int(idx % m);
                 const double alo = -1.0 + 2.0 * a / m, ahi = alo + 2.0 / m;
                 const double blo = -1.0 + 2.0 * b / m, bhi = blo + 2.0 / m;
                 const int ax = axis[f];
@@ -182,8 +203,8 @@ std::vector<Patch> cube_sphere_patches(double radius, int splits, int nu, int nv
                     const Vec3 c = ax == 0 ? Vec3{sg, s, t} : (ax == 1 ? Vec3{t, sg, s} : Vec3{s, t, sg});
                     return c * (radius / len(c));
                 };
-                out.push_back(fit(map, nu, nv, 1e-12));
-            }
+                out[idx] = fit(map, nu, nv, 1e-12);
+    });
     return out;
 }
 
