@@ -152,10 +152,12 @@ bool launch_cousin_eval_tc(const LevelDev& L, const PointsDev& P, const double2*
     if (L.nwchunk == 0) return true;
     const int grid = (L.nwchunk + kWarps - 1) / kWarps;
     const int code = pipes.f[0] * 100 + (pipes.n > 1 ? pipes.f[1] * 10 : 0) + (pipes.n > 2 ? pipes.f[2] : 0);
-    // IFGF_COUSIN_BPRE=0|1 (default 1): first group's coefficients loaded before the geometry
+    // IFGF_COUSIN_BPRE=1: the first group's coefficients are loaded before the geometry step.
+    // Off by default: measured slower (cfg3 cousins 105 -> 117 ms, cfg2 4.87 -> 5.45 ms; the 24
+    // extra live registers across the geometry step cost more than the hidden latency)
     static const bool bpre = [] {
         const char* e = std::getenv("IFGF_COUSIN_BPRE");
-        return !(e && e[0] == '0');
+        return e && e[0] == '1';
     }();
     auto go = [&](auto kpre, auto kplain) {
         if (bpre) kpre<<<grid, kThreads, 0, st>>>(L, P, store, k, pipes, Sp, Dp);
