@@ -66,7 +66,10 @@ def make_mesh(cfg_name, module):
 
 
 def peaks():
-    p = {"hbm_gbs": 6551.4, "fp64_tflops": 34.2, "source_fp64": "tools/fp64_peak.cu DFMA chain on this pool's B200 (profiles/r01_box_probe.txt)"}
+    p = {"hbm_gbs": 6551.4, "fp64_tflops": 36.9,
+         "source_fp64": "highest FP64 rate measured on this pool's B200: 8 DMMA chains per warp, tools/fp64_mix.cu "
+                        "(profiles/r02ag_fp64_mix.json: DMMA 36.9, DFMA 36.4 TF/s, one shared pipe; "
+                        "tools/fp64_peak.cu had 34.2 with 8 DFMA chains)"}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             m = json.load(f)

@@ -5,7 +5,8 @@
 // 48.9 KB shared per CTA), in variants that drop or restructure one part each:
 //   0 as the product      1 no accumulator update      2 no epilogue at all (DMMAs + A loads)
 //   3 two tiles per step: both tiles' DMMAs, then both epilogues
-//   4 DMMAs only (A from registers)
+//   4 DMMAs only (A from registers; the compiler hoists loop-invariant tiles: ignore)
+//   5 next tile's A slots loaded ahead   6 DMMAs of tile t before the epilogue of tile t-1
 // Prints the DMMA rate of each as a fraction of the 36.9 TF/s peak.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++20 --expt-relaxed-constexpr \
 //        -Ipaper_2112_06316_b200/csrc/cuda -o tools/tile_probe tools/tile_probe.cu
@@ -79,7 +80,39 @@ __global__ void __launch_bounds__(32 * kWarps, 4) probe(const double* __restrict
                 a = cadd(a, ctb);
             }
         };
-        if constexpr (V == 3) {
+        if constexpr (V == 5) {
+            // the next tile's A slots are loaded before this tile's DMMAs
+            double an[kKS];
+#pragma unroll
+            for (int j = 0; j < kKS; ++j) an[j] = geo[r * kRow + 4 * j + tig];
+            for (int t = 0; t < tiles; ++t) {
+                double a[kKS], d[LY::NQ][2];
+#pragma unroll
+                for (int j = 0; j < kKS; ++j) a[j] = an[j];
+                const int tn = ((t + 1) & 3) * 8;
+#pragma unroll
+                for (int j = 0; j < kKS; ++j) an[j] = geo[(tn + r) * kRow + 4 * j + tig];
+#pragma unroll
+                for (int q = 0; q < LY::NQ; ++q) d[q][0] = d[q][1] = 0.0;
+#pragma unroll
+                for (int j = 0; j < kKS; ++j)
+#pragma unroll
+                    for (int q = 0; q < LY::NQ; ++q) dmma884(d[q][0], d[q][1], a[j], bq[q * kKS + j]);
+                epilogue((t & 3) * 8, d);
+            }
+        } else if constexpr (V == 6) {
+            // tile t's DMMAs are issued before tile t-1's epilogue
+            double dp[LY::NQ][2];
+            mma(0, dp);
+            for (int t = 1; t < tiles; ++t) {
+                double d[LY::NQ][2];
+                mma((t & 3) * 8, d);
+                epilogue(((t - 1) & 3) * 8, dp);
+#pragma unroll
+                for (int q = 0; q < LY::NQ; ++q) dp[q][0] = d[q][0], dp[q][1] = d[q][1];
+            }
+            epilogue(((tiles - 1) & 3) * 8, dp);
+        } else if constexpr (V == 3) {
             for (int t = 0; t < tiles; t += 2) {
                 double d0[LY::NQ][2], d1[LY::NQ][2];
                 mma((t & 3) * 8, d0);
@@ -142,6 +175,8 @@ int main() {
         run<2>(bsrc, out, blocks, groups, tiles, "no epilogue");
         run<3>(bsrc, out, blocks, groups, tiles, "two tiles per step");
         run<4>(bsrc, out, blocks, groups, tiles, "DMMAs only");
+        run<5>(bsrc, out, blocks, groups, tiles, "next tile's A slots loaded ahead");
+        run<6>(bsrc, out, blocks, groups, tiles, "DMMAs of tile t before the epilogue of t-1");
     }
     return 0;
 }
