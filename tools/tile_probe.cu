@@ -7,6 +7,7 @@
 //   3 two tiles per step: both tiles' DMMAs, then both epilogues
 //   4 DMMAs only (A from registers; the compiler hoists loop-invariant tiles: ignore)
 //   5 next tile's A slots loaded ahead   6 DMMAs of tile t before the epilogue of tile t-1
+//   7 / 8 as 0 plus the per-group geometry rows (fill_row + factors + barrier) from registers
 // Prints the DMMA rate of each as a fraction of the 36.9 TF/s peak.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++20 --expt-relaxed-constexpr \
 //        -Ipaper_2112_06316_b200/csrc/cuda -o tools/tile_probe tools/tile_probe.cu
@@ -48,6 +49,22 @@ __global__ void __launch_bounds__(32 * kWarps, 4) probe(const double* __restrict
         double bq[LY::NB];
 #pragma unroll
         for (int i = 0; i < LY::NB; ++i) bq[i] = bsrc[(g * 37 + i * 32 + lane) & 4095];
+        if constexpr (V == 7 || V == 8) {
+            // the per-group geometry step of the template path without its global loads: the
+            // row's A slots, T(phi), factors and node written by each lane, then the barrier
+            if (V == 7 || lane < 8 * tiles) {
+                double* row = geo + lane * kRow;
+                const double x = 1e-3 * g;
+                fill_row(0.1 + 0.01 * lane + x, -0.2 + 0.02 * lane - x, 0.3 - 0.01 * lane + x, row);
+#pragma unroll
+                for (int pc = 0; pc < NPC; ++pc) {
+                    row[kRowLen + 2 * pc] = 0.5 + x;
+                    row[kRowLen + 2 * pc + 1] = 0.25 - x;
+                }
+                row[kNode] = __longlong_as_double((long long)((lane * 7 + g) % 150));
+            }
+            __syncwarp();
+        }
         auto mma = [&](int t0, double (&d)[LY::NQ][2]) {
             if constexpr (V == 4) {
 #pragma unroll
@@ -175,6 +192,8 @@ int main() {
         run<2>(bsrc, out, blocks, groups, tiles, "no epilogue");
         run<3>(bsrc, out, blocks, groups, tiles, "two tiles per step");
         run<4>(bsrc, out, blocks, groups, tiles, "DMMAs only");
+        run<7>(bsrc, out, blocks, groups, tiles, "product loop + the group's geometry rows (32 lanes)");
+        run<8>(bsrc, out, blocks, groups, tiles, "product loop + the group's geometry rows (8 x tiles lanes)");
         run<5>(bsrc, out, blocks, groups, tiles, "next tile's A slots loaded ahead");
         run<6>(bsrc, out, blocks, groups, tiles, "DMMAs of tile t before the epilogue of t-1");
     }
