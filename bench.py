@@ -39,6 +39,15 @@ import sys
 import tempfile
 import time
 
+# torch.distributed.run exports OMP_NUM_THREADS=1 to its workers when several run on a node.
+# The host side of the setup (cone plan, proximity, mesh) is OpenMP code: every local rank
+# gets its share of the cores instead, and the reference arm (rank 0 alone) all of them.
+# Set before anything loads an OpenMP runtime.
+_LWS = int(os.environ.get("LOCAL_WORLD_SIZE", "1") or 1)
+if _LWS > 1:
+    _ref_arm = any(a == "reference" or a == "--impl=reference" for a in sys.argv[1:])
+    os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or 1) // (1 if _ref_arm else _LWS)))
+
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
