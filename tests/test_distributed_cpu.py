@@ -195,3 +195,26 @@ def test_exchange_layout_world2():
     want[perm] = S_sum + D_sum  # original order
     for x in res:
         assert np.allclose(x[5], want, rtol=0, atol=1e-12)  # every rank holds the full output
+
+
+def test_bench_gives_each_local_rank_its_share_of_the_cores():
+    # torch.distributed.run exports OMP_NUM_THREADS=1 to its workers; bench.py replaces it
+    # before any OpenMP runtime loads (the host setup is OpenMP code), and leaves a
+    # single-rank run alone
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = "import os, sys; sys.argv = ['bench.py'] + sys.argv[1:]; import bench; print(os.environ.get('OMP_NUM_THREADS'))"
+    cores = os.cpu_count() or 1
+
+    def run(env_extra, *argv):
+        env = dict(os.environ, **env_extra)
+        out = subprocess.run([sys.executable, "-c", code, *argv], cwd=root, env=env, capture_output=True, text=True)
+        assert out.returncode == 0, out.stderr
+        return out.stdout.strip().splitlines()[-1]
+
+    assert run({"LOCAL_WORLD_SIZE": "2", "OMP_NUM_THREADS": "1"}) == str(max(1, cores // 2))
+    assert run({"LOCAL_WORLD_SIZE": "2", "OMP_NUM_THREADS": "1"}, "--impl", "reference") == str(cores)
+    assert run({"LOCAL_WORLD_SIZE": "1", "OMP_NUM_THREADS": "3"}) == "3"
