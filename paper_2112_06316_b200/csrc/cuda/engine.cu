@@ -1084,9 +1084,15 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
                         item_seg.push_back(a + j < by_slot[sl].size() ? by_slot[sl][a + j] : -1);
                 }
             const std::int64_t n_item = std::int64_t(item_slot.size());
-            std::vector<std::int32_t> child(std::size_t(n_item) * kCbSegs * 8, -1),
-                cso(std::size_t(n_item) * kCbSegs * 8 * kCbMaxGrp, -1);
+            std::vector<std::int32_t> child(std::size_t(n_item) * kCbSegs * 8, -1);
             std::vector<std::vector<std::pair<std::uint32_t, std::int32_t>>> exc(n_item);
+            // unit lists (parent_cb.cu): per (item, warp of 4 segments), per octant with a child
+            // and per child-cell group met by one of the 4, the rows [gs, ge) in at most
+            // max_tiles 8-row tiles per unit (a larger group: two units) and the 4 child segments
+            constexpr int kW = kCbSegs / 4;
+            const int max_tiles = e.pipes_at(d, true, true, e.strategy).size() == 3 ? kCbMaxTiles3 : kCbMaxTiles;
+            std::vector<std::vector<std::int32_t>> ulist(static_cast<std::size_t>(n_item) * kW);
+            int too_long = 0;
             auto ordinal = [&](int ch, int gam) {
                 const auto b0 = CL.seg_gamma.begin() + CL.box_seg_begin[ch];
                 const auto b1 = CL.seg_gamma.begin() + CL.box_seg_begin[ch + 1];
@@ -1096,6 +1102,9 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
 #pragma omp parallel for schedule(dynamic, 256)
             for (std::int64_t it = 0; it < n_item; ++it) {
                 const int sl = item_slot[it];
+                // child segment of (item segment, octant, child-cell group), -1: none
+                std::int32_t cso[kCbSegs][8][kCbMaxGrp];
+                std::fill(&cso[0][0][0], &cso[0][0][0] + kCbSegs * 8 * kCbMaxGrp, -1);
                 for (int j = 0; j < kCbSegs; ++j) {
                     const int so = item_seg[it * kCbSegs + j];
                     if (so < 0) continue;
@@ -1108,7 +1117,7 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
                         const int o = (cc.x > pc.x ? 1 : 0) | (cc.y > pc.y ? 2 : 0) | (cc.z > pc.z ? 4 : 0);
                         const std::size_t so8 = std::size_t(sl) * 8 + o;
                         child[(std::size_t(it) * kCbSegs + j) * 8 + o] = ch;
-                        std::int32_t* cg = cso.data() + ((std::size_t(it) * kCbSegs + j) * 8 + o) * kCbMaxGrp;
+                        std::int32_t* cg = cso[j][o];
                         for (int g = 0; g < ngrp[so8]; ++g) cg[g] = ordinal(ch, ggc[so8 * kCbMaxGrp + g]);
                         for (int nd = 0; nd < P; ++nd) {
                             const std::int32_t host = CL.pev_seg[CL.pev_begin[so] + std::int64_t(nd) * nch + c];
@@ -1117,16 +1126,6 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
                         }
                     }
                 }
-            }
-            // unit lists (parent_cb.cu): per (item, warp of 4 segments), per octant with a child
-            // and per child-cell group met by one of the 4, the rows [gs, ge) in at most
-            // max_tiles 8-row tiles per unit (a larger group: two units) and the 4 child segments
-            constexpr int kW = kCbSegs / 4;
-            const int max_tiles = e.pipes_at(d, true, true, e.strategy).size() == 3 ? kCbMaxTiles3 : kCbMaxTiles;
-            std::vector<std::vector<std::int32_t>> ulist(static_cast<std::size_t>(n_item) * kW);
-#pragma omp parallel for schedule(dynamic, 256)
-            for (std::int64_t it = 0; it < n_item; ++it) {
-                const int sl = item_slot[it];
                 for (int w = 0; w < kW; ++w) {
                     std::vector<std::int32_t>& U = ulist[std::size_t(it) * kW + w];
                     for (int o = 0; o < 8; ++o) {
@@ -1135,8 +1134,7 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
                             std::int32_t c4[4];
                             bool any = false;
                             for (int c = 0; c < 4; ++c) {
-                                const std::size_t j = std::size_t(it) * kCbSegs + 4 * w + c;
-                                c4[c] = child[j * 8 + o] >= 0 ? cso[(j * 8 + o) * kCbMaxGrp + g] : -1;
+                                c4[c] = cso[4 * w + c][o][g];  // -1 without a child in this octant
                                 any = any || c4[c] >= 0;
                             }
                             if (!any) continue;
@@ -1150,9 +1148,13 @@ Engine::Engine(const OperatorSetup& s, int device) : d_(std::make_unique<Impl>()
                             }
                         }
                     }
-                    if (U.size() > std::size_t(kCbMaxUnits) * 5) throw std::logic_error("cell-batched unit list too long");
+                    if (U.size() > std::size_t(kCbMaxUnits) * 5) {
+#pragma omp atomic write
+                        too_long = 1;
+                    }
                 }
             }
+            if (too_long) throw std::logic_error("cell-batched unit list too long");
             std::vector<std::int32_t> unit_begin(ulist.size() + 1, 0);
             for (std::size_t i = 0; i < ulist.size(); ++i) {
                 const std::size_t nxt = std::size_t(unit_begin[i]) + ulist[i].size() / 5;
